@@ -1,0 +1,196 @@
+/*
+ * spock_b200.h -- C-ABI drop-in boundary of the B200-native SPOCK solver.
+ *
+ * The reference (arxiv/paper_2505_12078, CPU C++20/Eigen) exposes a C++ API:
+ *   SpockSolver(const Raocp&, SpockParams)      proj/include/spock/solver.hpp:99
+ *   SpockSolver::solve / solve_cp / apply_T     proj/include/spock/solver.hpp:103-112
+ *   TreeOperator::apply / apply_adjoint / m_norm proj/include/spock/tree_operator.hpp:38-52
+ *   proj_s1 / proj_s2 / proj_s3                  proj/include/spock/projections.hpp:49-65
+ * Every entry point below replaces one of those (cited per function).  The C++
+ * host layer of this package keeps the reference's semantics and error kinds
+ * behind these plain-pointer functions; no Eigen/torch types cross the ABI.
+ *
+ * Vectors are exchanged in the reference's PrimalLayout / DualLayout order
+ * (proj/include/spock/layout.hpp:14-52).  Pointers may be host or device
+ * memory; the library detects which (cudaPointerGetAttributes).
+ *
+ * Matrices are column-major (Eigen's default storage), packed back to back in
+ * node order with the reference's indexing: per non-root node at offset
+ * node-1, per leaf at node-num_nonleaf, per non-leaf at node
+ * (proj/include/spock/problem.hpp:25-58).
+ *
+ * Return codes map 1:1 onto the reference's exception kinds:
+ *   SPOCK_EINVAL   <- std::invalid_argument  (bad parameters / dimensions / data)
+ *   SPOCK_ERUNTIME <- std::runtime_error     (Cholesky failure, negative M-norm radicand)
+ * spock_last_error() returns the message of the last failure on this thread.
+ */
+#ifndef SPOCK_B200_H_
+#define SPOCK_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPOCK_OK 0
+#define SPOCK_EINVAL 1
+#define SPOCK_ERUNTIME 2
+#define SPOCK_ECUDA 3
+
+/* ConeKind, proj/include/spock/risk.hpp:8 */
+#define SPOCK_CONE_ZERO 0
+#define SPOCK_CONE_NONNEG 1
+#define SPOCK_CONE_SOC 2
+#define SPOCK_CONE_FREE 3
+
+/* RiskSpec::Kind, proj/include/spock/risk.hpp:27 */
+#define SPOCK_RISK_AVAR 0
+#define SPOCK_RISK_GENERAL 1
+
+/* SpockTermination, proj/include/spock/solver.hpp:37 */
+#define SPOCK_CONVERGED 0
+#define SPOCK_MAX_ITERS 1
+#define SPOCK_STALLED 2
+#define SPOCK_CANCELLED 3
+
+/* Flat description of a Raocp (proj/include/spock/problem.hpp:29-58) on a
+ * ScenarioTree given by raw arrays (ScenarioTree::from_arrays,
+ * proj/include/spock/tree.hpp:72-74).  All pointers are host memory. */
+typedef struct spock_problem_desc {
+  int32_t num_nodes, nx, nu;
+  int32_t horizon, stop_stage, num_events;
+  const int32_t* anc;       /* [nn], anc[0] = -1 */
+  const int32_t* event;     /* [nn] */
+  const double* prob;       /* [nn] */
+  const double* cond_prob;  /* [nn] */
+  /* per non-root node (nn-1 entries each) */
+  const double* A; /* nx*nx */
+  const double* B; /* nx*nu */
+  const double* c; /* nx */
+  const double* Q; /* nx*nx */
+  const double* R; /* nu*nu */
+  const double* q; /* nx */
+  const double* r; /* nu */
+  /* per leaf */
+  const double* QN; /* nx*nx */
+  const double* qN; /* nx */
+  /* per non-leaf: nc[i] constraint rows */
+  const int32_t* nc;
+  const double* Gx;   /* packed nc[i]*nx */
+  const double* Gu;   /* packed nc[i]*nu */
+  const double* C_lo; /* packed nc[i] */
+  const double* C_hi;
+  /* per leaf: ncN[j] terminal constraint rows */
+  const int32_t* ncN;
+  const double* GN; /* packed ncN[j]*nx */
+  const double* CN_lo;
+  const double* CN_hi;
+  /* per non-leaf risk spec (proj/include/spock/risk.hpp:26-48); n = children */
+  const int32_t* risk_kind;   /* SPOCK_RISK_* */
+  const int32_t* risk_rows;   /* rows of E */
+  const int32_t* risk_nnu;    /* columns of F */
+  const double* risk_E;       /* packed rows*n */
+  const double* risk_F;       /* packed rows*nnu */
+  const double* risk_b;       /* packed rows */
+  const double* risk_gamma;   /* [nnl], Avar only */
+  const double* risk_pi;      /* packed n, Avar only */
+  const int32_t* cone_nparts; /* [nnl] */
+  const int32_t* cone_kind;   /* packed parts */
+  const int32_t* cone_dim;    /* packed parts */
+  const double* x_init;       /* nx */
+} spock_problem_desc;
+
+/* SpockParams, proj/include/spock/solver.hpp:15-35.  std::function callbacks
+ * become (fnptr, user) pairs; they are polled every `poll_every` iterations
+ * (1 = every iteration, the reference's behaviour). */
+typedef struct spock_params {
+  double eps_abs, eps_rel;
+  double alpha; /* 0: 0.99 / power-iteration estimate of ||L|| */
+  int32_t aa_memory;
+  double c0, c1, c2;
+  double beta, sigma, lambda;
+  int32_t max_iters;
+  int32_t max_backtracks;
+  int32_t use_preconditioner;
+  void (*progress)(int32_t iter, double rnorm, char branch, void* user);
+  int32_t (*cancelled)(void* user);
+  void* user;
+  int32_t poll_every;
+} spock_params;
+
+/* SpockStatus, proj/include/spock/solver.hpp:41-49.  History buffers are
+ * caller-owned (capacity entries); *_len reports how many were written. */
+typedef struct spock_status {
+  int32_t iterations;
+  int32_t reason; /* SPOCK_CONVERGED ... */
+  double xi1_inf, xi2_inf;
+  int32_t k0_steps, k1_steps, k2_steps, stalled_steps;
+  double alpha;
+  double op_norm_estimate;
+  int32_t op_norm_iterations;
+  double op_norm_analytic_bound;
+  int32_t op_norm_converged;
+  double* rnorm_history;
+  char* branch_history;
+  int32_t history_capacity;
+  int32_t history_len;
+  /* operator applications issued by the solve (diagnostics) */
+  int64_t n_T, n_L, n_Lt;
+} spock_status;
+
+typedef struct spock_solver spock_solver;
+
+const char* spock_last_error(void);
+void spock_params_default(spock_params* p);
+
+/* SpockSolver::SpockSolver (proj/src/solver.cpp:79-114): validate, precondition,
+ * SOC epigraph data, layouts, offline factorisation (on device), ||L|| power
+ * iteration (on device), alpha, termination scalings. */
+int spock_solver_create(const spock_problem_desc* desc, const spock_params* params,
+                        spock_solver** out);
+void spock_solver_destroy(spock_solver* s);
+
+/* sizes of z (PrimalLayout::n) and eta (DualLayout::n) */
+int spock_solver_dims(const spock_solver* s, int64_t* nz, int64_t* neta);
+double spock_solver_alpha(const spock_solver* s);
+
+/* SpockSolver::solve(x_init, warm) (proj/src/solver.cpp:178-180,189-350).
+ * x_init may be NULL (problem's x_init); warm_z_scaled/warm_eta may be NULL
+ * (zero start).  Outputs (any may be NULL): z (original variables), z_scaled,
+ * eta. */
+int spock_solver_solve(spock_solver* s, const double* x_init, const double* warm_z_scaled,
+                       const double* warm_eta, double* out_z, double* out_z_scaled,
+                       double* out_eta, spock_status* status);
+/* SpockSolver::solve_cp (proj/src/solver.cpp:182-187): plain KM iterations */
+int spock_solver_solve_cp(spock_solver* s, const double* x_init, const double* warm_z_scaled,
+                          const double* warm_eta, double* out_z, double* out_z_scaled,
+                          double* out_eta, spock_status* status);
+
+/* SpockSolver::apply_T (proj/src/solver.cpp:148-164), scaled coordinates */
+int spock_solver_apply_T(spock_solver* s, const double* z, const double* eta, double* z_out,
+                         double* eta_out);
+/* TreeOperator::apply / apply_adjoint (proj/src/tree_operator.cpp:20-114) on
+ * the solver's (scaled) problem */
+int spock_op_apply(spock_solver* s, const double* z, double* eta);
+int spock_op_apply_adjoint(spock_solver* s, const double* eta, double* z);
+/* TreeOperator::m_norm (proj/src/tree_operator.cpp:214-222) */
+int spock_op_m_norm(spock_solver* s, const double* z, const double* eta, double alpha,
+                    double* out);
+/* proj_s1 / proj_s2 / proj_s3 (proj/src/projections.cpp:142-244), in place,
+ * on the solver's (scaled) problem; s1 uses the scaled x_init */
+int spock_proj_s1(spock_solver* s, double* z);
+int spock_proj_s2(spock_solver* s, double* z);
+int spock_proj_s3(spock_solver* s, double* eta);
+/* SpockSolver::unscale_primal / scale_primal (proj/src/solver.cpp:116-146) */
+int spock_solver_unscale_primal(spock_solver* s, const double* z_scaled, double* z);
+
+/* Timing helper for benchmarks: k back-to-back CP applications v <- T(v) on
+ * device-resident iterates (no host transfers); returns device milliseconds. */
+int spock_bench_T(spock_solver* s, int32_t k, int32_t use_graph, double* ms_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPOCK_B200_H_ */

@@ -1,0 +1,182 @@
+"""Python mirror of the reference's solver API over the C-ABI.
+
+``SpockSolver`` mirrors ``spock::SpockSolver`` (proj/include/spock/solver.hpp:99-145):
+construction performs the reference's setup (validation, preconditioning,
+SOC epigraph data, offline factorisation, ||L|| estimate) behind
+``spock_solver_create``; ``solve``/``solve_cp``/``apply_T`` and the operator
+entry points map 1:1 onto the C-ABI functions.  Errors surface as the
+reference's exception kinds: ``ValueError`` for std::invalid_argument and
+``RuntimeError`` for std::runtime_error.
+
+Vectors may be numpy arrays (host) or CUDA torch tensors (device); the library
+detects the pointer kind.  There is no CPU fallback: if the CUDA library is
+missing the constructor raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import capi
+from .problem import Raocp
+
+
+@dataclass
+class SolveResult:
+    z: np.ndarray
+    z_scaled: np.ndarray
+    eta: np.ndarray
+    status: dict = field(default_factory=dict)
+
+
+def _raise(lib, rc: int, prefix: str = "spock"):
+    if rc == capi.SPOCK_OK:
+        return
+    msg = lib.spock_last_error().decode() if hasattr(lib, "spock_last_error") else prefix
+    if rc == capi.SPOCK_EINVAL:
+        raise ValueError(msg)
+    raise RuntimeError(msg)
+
+
+def _ptr(a):
+    """Raw pointer of a numpy array or torch tensor (float64, contiguous)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        assert a.dtype == np.float64 and a.flags.c_contiguous
+        return a.ctypes.data
+    # torch tensor
+    assert a.dtype.is_floating_point and a.is_contiguous()
+    return a.data_ptr()
+
+
+def status_dict(st: capi.Status, rn: np.ndarray, br) -> dict:
+    n = min(st.history_len, st.history_capacity)
+    return dict(
+        iterations=st.iterations, reason=capi.TERMINATION.get(st.reason, str(st.reason)),
+        xi1_inf=st.xi1_inf, xi2_inf=st.xi2_inf, k0_steps=st.k0_steps, k1_steps=st.k1_steps,
+        k2_steps=st.k2_steps, stalled_steps=st.stalled_steps, alpha=st.alpha,
+        op_norm=dict(estimate=st.op_norm_estimate, iterations=st.op_norm_iterations,
+                     analytic_bound=st.op_norm_analytic_bound, converged=bool(st.op_norm_converged)),
+        rnorm_history=rn[:n].copy(), branches=br.raw[:n].decode(), history_len=st.history_len,
+        n_T=st.n_T, n_L=st.n_L, n_Lt=st.n_Lt)
+
+
+def make_status(capacity: int):
+    st = capi.Status()
+    rn = np.zeros(max(capacity, 1))
+    br = C.create_string_buffer(max(capacity, 1))
+    st.rnorm_history = rn.ctypes.data_as(C.POINTER(C.c_double))
+    st.branch_history = C.cast(br, C.c_char_p)
+    st.history_capacity = capacity
+    return st, rn, br
+
+
+class SpockSolver:
+    """spock::SpockSolver over the B200 C-ABI."""
+
+    def __init__(self, problem: Raocp, progress=None, cancelled=None, **params):
+        self.lib = capi.load_library()
+        self.problem = problem
+        self.packed = capi.pack_problem(problem)
+        self._cbs = []
+        prm = capi.default_params(**params)
+        if progress is not None:
+            cb = capi.PROGRESS_FN(lambda k, w, b, u: progress(k, w, b.decode()))
+            self._cbs.append(cb)
+            prm.progress = cb
+        if cancelled is not None:
+            cb2 = capi.CANCEL_FN(lambda u: int(bool(cancelled())))
+            self._cbs.append(cb2)
+            prm.cancelled = cb2
+        self.params = prm
+        h = C.c_void_p()
+        _raise(self.lib, self.lib.spock_solver_create(self.packed.ref(), C.byref(prm), C.byref(h)))
+        self.h = h
+        nz, ne = C.c_int64(), C.c_int64()
+        self.lib.spock_solver_dims(self.h, C.byref(nz), C.byref(ne))
+        self.nz, self.neta = nz.value, ne.value
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value:
+            self.lib.spock_solver_destroy(h)
+            self.h = None
+
+    @property
+    def alpha(self) -> float:
+        return self.lib.spock_solver_alpha(self.h)
+
+    def _run(self, fn, x_init, warm, capacity):
+        st, rn, br = make_status(capacity)
+        z = np.zeros(self.nz)
+        zs = np.zeros(self.nz)
+        e = np.zeros(self.neta)
+        x = None if x_init is None else np.ascontiguousarray(x_init, dtype=np.float64)
+        wz = we = None
+        if warm is not None:
+            wz = np.ascontiguousarray(warm[0], dtype=np.float64)
+            we = np.ascontiguousarray(warm[1], dtype=np.float64)
+        rc = fn(self.h, _ptr(x), _ptr(wz), _ptr(we), _ptr(z), _ptr(zs), _ptr(e), C.byref(st))
+        _raise(self.lib, rc)
+        return SolveResult(z, zs, e, status_dict(st, rn, br))
+
+    def solve(self, x_init=None, warm=None, history_capacity: int = 100000) -> SolveResult:
+        """SpockSolver::solve (proj/src/solver.cpp:176-180)."""
+        return self._run(self.lib.spock_solver_solve, x_init, warm, history_capacity)
+
+    def solve_cp(self, x_init=None, warm=None, history_capacity: int = 100000) -> SolveResult:
+        """SpockSolver::solve_cp (proj/src/solver.cpp:182-187)."""
+        return self._run(self.lib.spock_solver_solve_cp, x_init, warm, history_capacity)
+
+    def apply_T(self, z, eta, z_out=None, eta_out=None):
+        """SpockSolver::apply_T (proj/src/solver.cpp:148-164)."""
+        if z_out is None:
+            z_out = np.empty_like(z)
+        if eta_out is None:
+            eta_out = np.empty_like(eta)
+        _raise(self.lib, self.lib.spock_solver_apply_T(self.h, _ptr(z), _ptr(eta), _ptr(z_out), _ptr(eta_out)))
+        return z_out, eta_out
+
+    def apply_L(self, z, out=None):
+        out = np.empty(self.neta) if out is None else out
+        _raise(self.lib, self.lib.spock_op_apply(self.h, _ptr(z), _ptr(out)))
+        return out
+
+    def apply_Lt(self, eta, out=None):
+        out = np.empty(self.nz) if out is None else out
+        _raise(self.lib, self.lib.spock_op_apply_adjoint(self.h, _ptr(eta), _ptr(out)))
+        return out
+
+    def m_norm(self, z, eta, alpha: float) -> float:
+        o = C.c_double()
+        _raise(self.lib, self.lib.spock_op_m_norm(self.h, _ptr(z), _ptr(eta), alpha, C.byref(o)))
+        return o.value
+
+    def proj_s1(self, z):
+        z = np.array(z, dtype=np.float64)
+        _raise(self.lib, self.lib.spock_proj_s1(self.h, _ptr(z)))
+        return z
+
+    def proj_s2(self, z):
+        z = np.array(z, dtype=np.float64)
+        _raise(self.lib, self.lib.spock_proj_s2(self.h, _ptr(z)))
+        return z
+
+    def proj_s3(self, eta):
+        eta = np.array(eta, dtype=np.float64)
+        _raise(self.lib, self.lib.spock_proj_s3(self.h, _ptr(eta)))
+        return eta
+
+    def unscale_primal(self, zs):
+        out = np.empty(self.nz)
+        _raise(self.lib, self.lib.spock_solver_unscale_primal(self.h, _ptr(np.ascontiguousarray(zs)), _ptr(out)))
+        return out
+
+    def bench_T(self, k: int, use_graph: bool = True) -> float:
+        ms = C.c_double()
+        _raise(self.lib, self.lib.spock_bench_T(self.h, int(k), int(use_graph), C.byref(ms)))
+        return ms.value

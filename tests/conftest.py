@@ -1,0 +1,44 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (CUDA) device")
+    config.addinivalue_line("markers", "slow: long-running CPU test")
+
+
+def pytest_collection_modifyitems(config, items):
+    try:
+        import torch
+        has_gpu = torch.cuda.is_available()
+    except Exception:  # pragma: no cover
+        has_gpu = False
+    if has_gpu:
+        return
+    skip = pytest.mark.skip(reason="no CUDA device")
+    for it in items:
+        if "gpu" in it.keywords:
+            it.add_marker(skip)
+
+
+IMPLS = ["oracle", pytest.param("b200", marks=pytest.mark.gpu)]
+
+
+def make_solver(impl, problem, **params):
+    """Construct the oracle (CPU restatement) or the B200 solver on the same problem."""
+    if impl == "oracle":
+        from oracle.oracle import OracleSolver
+        return OracleSolver(problem, **params)
+    from paper_2505_12078_b200.solver import SpockSolver
+    return SpockSolver(problem, **params)
+
+
+@pytest.fixture(params=IMPLS)
+def impl(request):
+    return request.param
