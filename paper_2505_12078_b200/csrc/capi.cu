@@ -1,0 +1,200 @@
+// C-ABI of the B200 SPOCK solver (include/spock_b200.h).  Each entry point
+// forwards to the Engine and maps C++ exceptions onto the reference's error
+// kinds: std::invalid_argument -> SPOCK_EINVAL, numerical std::runtime_error
+// -> SPOCK_ERUNTIME, CUDA failures -> SPOCK_ECUDA.
+#include <cstring>
+#include <string>
+
+#include "../../include/spock_b200.h"
+#include "engine.hpp"
+
+struct spock_solver {
+  spock::Engine* eng = nullptr;
+  spock::OpNorm norm;
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return SPOCK_OK;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return SPOCK_EINVAL;
+  } catch (const spock::CudaError& e) {
+    g_err = e.what();
+    return SPOCK_ECUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return SPOCK_ERUNTIME;
+  }
+}
+
+spock::Params to_params(const spock_params* p) {
+  spock::Params q;
+  if (!p) return q;
+  q.eps_abs = p->eps_abs;
+  q.eps_rel = p->eps_rel;
+  q.alpha = p->alpha;
+  q.aa_memory = p->aa_memory;
+  q.c0 = p->c0, q.c1 = p->c1, q.c2 = p->c2;
+  q.beta = p->beta, q.sigma = p->sigma, q.lambda = p->lambda;
+  q.max_iters = p->max_iters;
+  q.max_backtracks = p->max_backtracks;
+  q.use_preconditioner = p->use_preconditioner != 0;
+  q.poll_every = p->poll_every > 0 ? p->poll_every : 1;
+  if (p->progress) {
+    auto f = p->progress;
+    void* u = p->user;
+    q.progress = [f, u](int k, double w, char b) { f(k, w, b, u); };
+  }
+  if (p->cancelled) {
+    auto f = p->cancelled;
+    void* u = p->user;
+    q.cancelled = [f, u]() { return f(u) != 0; };
+  }
+  return q;
+}
+
+int check(spock_solver* s) {
+  if (!s || !s->eng) {
+    g_err = "spock: null solver handle";
+    return SPOCK_EINVAL;
+  }
+  return SPOCK_OK;
+}
+}  // namespace
+
+extern "C" {
+
+const char* spock_last_error(void) { return g_err.c_str(); }
+
+void spock_params_default(spock_params* p) {
+  if (!p) return;
+  std::memset(p, 0, sizeof(*p));
+  p->eps_abs = 1e-6;
+  p->eps_rel = 1e-6;
+  p->alpha = 0.0;
+  p->aa_memory = 3;
+  p->c0 = p->c1 = p->c2 = 0.99;
+  p->beta = 0.5;
+  p->sigma = 0.1;
+  p->lambda = 1.0;
+  p->max_iters = 50000;
+  p->max_backtracks = 40;
+  p->use_preconditioner = 1;
+  p->poll_every = 1;
+}
+
+int spock_solver_create(const spock_problem_desc* desc, const spock_params* params, spock_solver** out) {
+  return guard([&] {
+    if (!out) throw std::invalid_argument("spock: null output handle");
+    auto* s = new spock_solver;
+    try {
+      s->eng = new spock::Engine(desc, to_params(params));
+    } catch (...) {
+      delete s;
+      throw;
+    }
+    *out = s;
+  });
+}
+
+void spock_solver_destroy(spock_solver* s) {
+  if (!s) return;
+  delete s->eng;
+  delete s;
+}
+
+int spock_solver_dims(const spock_solver* s, int64_t* nz, int64_t* neta) {
+  if (!s || !s->eng) return SPOCK_EINVAL;
+  if (nz) *nz = s->eng->nz();
+  if (neta) *neta = s->eng->neta();
+  return SPOCK_OK;
+}
+
+double spock_solver_alpha(const spock_solver* s) { return (s && s->eng) ? s->eng->alpha() : 0.0; }
+
+static int do_solve(spock_solver* s, const double* x0, const double* wz, const double* we, double* oz,
+                    double* ozs, double* oe, spock_status* st, bool sm) {
+  if (int rc = check(s)) return rc;
+  return guard([&] {
+    spock::Status S;
+    s->eng->solve_b(x0, wz, we, oz, ozs, oe, sm, S);
+    if (!st) return;
+    st->iterations = S.iterations;
+    st->reason = S.reason;
+    st->xi1_inf = S.xi1;
+    st->xi2_inf = S.xi2;
+    st->k0_steps = S.k0;
+    st->k1_steps = S.k1;
+    st->k2_steps = S.k2;
+    st->stalled_steps = S.stalled;
+    st->alpha = s->eng->alpha();
+    const auto& nrm = s->eng->op_norm();
+    st->op_norm_estimate = nrm.estimate;
+    st->op_norm_iterations = nrm.iterations;
+    st->op_norm_analytic_bound = nrm.analytic_bound;
+    st->op_norm_converged = nrm.converged;
+    const int n = int(S.rnorm.size());
+    for (int w = 0; w < n && w < st->history_capacity; ++w) {
+      if (st->rnorm_history) st->rnorm_history[w] = S.rnorm[w];
+      if (st->branch_history) st->branch_history[w] = S.branches[w];
+    }
+    st->history_len = n;
+    st->n_T = S.n_T;
+    st->n_L = S.n_L;
+    st->n_Lt = S.n_Lt;
+  });
+}
+
+int spock_solver_solve(spock_solver* s, const double* x_init, const double* wz, const double* we, double* oz,
+                       double* ozs, double* oe, spock_status* st) {
+  return do_solve(s, x_init, wz, we, oz, ozs, oe, st, true);
+}
+int spock_solver_solve_cp(spock_solver* s, const double* x_init, const double* wz, const double* we, double* oz,
+                          double* ozs, double* oe, spock_status* st) {
+  return do_solve(s, x_init, wz, we, oz, ozs, oe, st, false);
+}
+
+int spock_solver_apply_T(spock_solver* s, const double* z, const double* eta, double* zo, double* eo) {
+  if (int rc = check(s)) return rc;
+  return guard([&] { s->eng->apply_T_b(z, eta, zo, eo); });
+}
+int spock_op_apply(spock_solver* s, const double* z, double* eta) {
+  if (int rc = check(s)) return rc;
+  return guard([&] { s->eng->apply_L_b(z, eta); });
+}
+int spock_op_apply_adjoint(spock_solver* s, const double* eta, double* z) {
+  if (int rc = check(s)) return rc;
+  return guard([&] { s->eng->apply_Lt_b(eta, z); });
+}
+int spock_op_m_norm(spock_solver* s, const double* z, const double* eta, double alpha, double* out) {
+  if (int rc = check(s)) return rc;
+  return guard([&] { *out = s->eng->m_norm_b(z, eta, alpha); });
+}
+int spock_proj_s1(spock_solver* s, double* z) {
+  if (int rc = check(s)) return rc;
+  return guard([&] { s->eng->proj_s1_b(z); });
+}
+int spock_proj_s2(spock_solver* s, double* z) {
+  if (int rc = check(s)) return rc;
+  return guard([&] { s->eng->proj_s2_b(z); });
+}
+int spock_proj_s3(spock_solver* s, double* eta) {
+  if (int rc = check(s)) return rc;
+  return guard([&] { s->eng->proj_s3_b(eta); });
+}
+int spock_solver_unscale_primal(spock_solver* s, const double* zs, double* z) {
+  if (int rc = check(s)) return rc;
+  return guard([&] { s->eng->unscale_b(zs, z); });
+}
+int spock_bench_T(spock_solver* s, int32_t k, int32_t use_graph, double* ms_out) {
+  if (int rc = check(s)) return rc;
+  return guard([&] { *ms_out = s->eng->bench_T(k, use_graph != 0); });
+}
+
+}  // extern "C"

@@ -1,0 +1,163 @@
+// Device-side data layout of the B200 SPOCK solver.
+//
+// Everything lives in HBM, node-major, one contiguous block per node so that a
+// warp streams a node's matrix with coalesced 256 B requests (lanes walk the
+// rows of a column-major block).  Where a kernel needs the transpose of a
+// block (L* against L, the backward against the forward sweep), the block is
+// stored twice: each launch still reads every matrix once.
+//
+// Vectors z (primal) and eta (dual) use the reference's PrimalLayout and
+// DualLayout (proj/include/spock/layout.hpp:14-52) except that the head rows
+// of each stage-cost SOC segment are ordered [x rows; u rows] (the reference
+// orders them by ascending eigenvalue); spock_* boundary calls permute.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace spock {
+
+constexpr int kWarps = 8;          // warps per CTA in warp-per-node kernels
+constexpr int kMaxD = 256;         // max nx+nu (and any per-node GEMV length)
+constexpr int kMaxR = kMaxD / 32;  // rows per lane
+
+// S2 closed forms (kernel of M = [E' -I -I], MM' = a I + b 11')
+enum S2Kind : int { S2_AVAR = 0, S2_MAX = 1, S2_EQ = 2, S2_DENSE = 3 };
+
+struct Dev {
+  int nn, nnl, nl, nr, nx, nu, N;
+  int nz, neta;
+  // tree (proj/include/spock/tree.hpp:82-87)
+  const int* anc;
+  const int* cf;  // child_first
+  const int* cc;  // child_count
+  // primal layout
+  int u_base, tau_base, s_base, y_base;
+  const int* y_off;
+  const int* y_dim;
+  // dual layout
+  const int* s1_off;
+  const int* s1_nc;
+  const int* s1_ydim;
+  const int* s2_off;
+  const int* s2_dim;
+  const int* s3_off;
+  const int* s3_nc;
+  const int* s3_socdim;
+  // stage-cost SOC data per non-root (index node-1)
+  const int* px;
+  const int* pu;
+  const int64_t* hx_off;  // into Hx/HxT (px*nx each)
+  const int64_t* hu_off;  // into Hu/HuT (pu*nu each)
+  const double* Hx;       // px x nx col-major (L)
+  const double* HxT;      // nx x px col-major (L*)
+  const double* Hu;
+  const double* HuT;
+  const double* qk;      // (nx+nu) per non-root
+  const int64_t* a_off;  // translation a (p+2) per non-root
+  const double* a;
+  // terminal SOC data per leaf
+  const int* pN;
+  const int64_t* hn_off;
+  const double* HN;   // pN x nx
+  const double* HNT;  // nx x pN
+  const double* qkN;  // nx per leaf
+  const int64_t* aN_off;
+  const double* aN;
+  // stage constraints per non-leaf: diagonal fast path or dense
+  int g_diag;          // 1: every [Gx Gu] is square diagonal -> gd
+  const double* gd;    // (nx+nu) per non-leaf
+  const int64_t* g_off;  // row offsets
+  const double* Gx;      // nc x nx
+  const double* Gu;      // nc x nu
+  const double* GxT;     // nx x nc
+  const double* GuT;     // nu x nc
+  const double* lo;      // box per non-leaf, at g_off
+  const double* hi;
+  // terminal constraints per leaf
+  int gN_diag;
+  const double* gNd;  // nx per leaf
+  const int64_t* gN_off;
+  const double* GN;   // ncN x nx
+  const double* GNT;  // nx x ncN
+  const double* loN;
+  const double* hiN;
+  // risk per non-leaf: b at (y_off - y_base); dual cone of the y-copy rows
+  const double* rb;
+  const int* yc_nonneg;  // >=0: leading nonneg rows then free rows; -1: general parts
+  const int* yc_poff;    // general parts [yc_poff[i], yc_poff[i+1])
+  const int* yc_kind;
+  const int* yc_dim;
+  // S2 per non-leaf
+  const int* s2_kind;
+  const double* s2_gamma;
+  const int64_t* s2p_off;
+  const double* s2P;  // dense projectors (dim x dim)
+  // offline factors (Alg. 1) restructured for one-pass sweeps (see kernels.cu)
+  const double* M1;   // [Abar B] nx x (nx+nu) per non-root (forward)
+  const double* M1T;  // (nx+nu) x nx per non-root (backward)
+  const double* cvec; // nx per non-root
+  const double* K;    // nu x nx per non-leaf (forward)
+  const double* KT;   // nx x nu per non-leaf (backward)
+  const double* Rinv; // nu x nu per non-leaf
+  const double* g;    // nu per non-leaf: sum_c B_c' P_c c_c
+  const double* h;    // nx per non-leaf: sum_c Abar_c' P_c c_c
+  const double* xinit;  // scaled x_init (nx)
+  // scratch
+  double* T12;  // (nx+nu) per non-root: [Abar' q; B' q] of the child sweep
+  double* adj;  // (nx+nu) per non-root: L* stage-cost child terms
+  double* dvec; // nu per non-leaf
+};
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// acc[k] += sum_c A[(lane + 32k) + c*lda] * x[c]  for rows < m, columns < n.
+// A is column-major; each column is read by the warp as one coalesced run.
+__device__ __forceinline__ void warp_gemv(const double* __restrict__ A, int m, int n, int lda,
+                                          const double* x, double (&acc)[kMaxR]) {
+  const int l = lane_id();
+  int c = 0;
+  for (; c + 4 <= n; c += 4) {
+    const double x0 = x[c], x1 = x[c + 1], x2 = x[c + 2], x3 = x[c + 3];
+    const double* c0 = A + size_t(c) * lda;
+#pragma unroll
+    for (int k = 0; k < kMaxR; ++k) {
+      const int r = l + 32 * k;
+      if (k * 32 < m && r < m) {
+        const double a0 = __ldg(c0 + r), a1 = __ldg(c0 + lda + r), a2 = __ldg(c0 + 2 * lda + r),
+                     a3 = __ldg(c0 + 3 * lda + r);
+        acc[k] = fma(a0, x0, acc[k]);
+        acc[k] = fma(a1, x1, acc[k]);
+        acc[k] = fma(a2, x2, acc[k]);
+        acc[k] = fma(a3, x3, acc[k]);
+      }
+    }
+  }
+  for (; c < n; ++c) {
+    const double xc = x[c];
+    const double* col = A + size_t(c) * lda;
+#pragma unroll
+    for (int k = 0; k < kMaxR; ++k) {
+      const int r = l + 32 * k;
+      if (k * 32 < m && r < m) acc[k] = fma(__ldg(col + r), xc, acc[k]);
+    }
+  }
+}
+
+__device__ __forceinline__ void zero_acc(double (&acc)[kMaxR]) {
+#pragma unroll
+  for (int k = 0; k < kMaxR; ++k) acc[k] = 0.0;
+}
+
+}  // namespace spock

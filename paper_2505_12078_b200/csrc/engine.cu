@@ -1,0 +1,1169 @@
+// Device engine of the B200 SPOCK solver (see engine.hpp).
+//
+// Reference map (arxiv/paper_2505_12078):
+//   Engine::Engine       <- SpockSolver::SpockSolver   proj/src/solver.cpp:79-114
+//   Engine::factorize    <- make_solver_cache Alg. 1   proj/src/projections.cpp:59-140 (on device)
+//   Engine::power_iteration <- estimate_norm           proj/src/tree_operator.cpp:157-212 (on device)
+//   Engine::T            <- SpockSolver::apply_T       proj/src/solver.cpp:148-164
+//   Engine::solve_b      <- SpockSolver::run           proj/src/solver.cpp:189-350
+#include "engine.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+
+namespace spock {
+
+#define CK(x)                                                                                  \
+  do {                                                                                         \
+    cudaError_t e_ = (x);                                                                      \
+    if (e_ != cudaSuccess) throw CudaError(std::string("CUDA error: ") + cudaGetErrorString(e_) + \
+                                           " at " #x);                                         \
+  } while (0)
+
+namespace {
+void require(bool c, const char* m) {
+  if (!c) throw std::invalid_argument(m);
+}
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+}  // namespace
+
+void Params::validate() const {  // proj/src/solver.cpp:9-19
+  if (eps_abs <= 0.0 || eps_rel < 0.0) throw std::invalid_argument("SpockParams: bad tolerances");
+  if (alpha < 0.0) throw std::invalid_argument("SpockParams: alpha must be >= 0");
+  if (aa_memory < 1) throw std::invalid_argument("SpockParams: aa_memory must be >= 1");
+  if (c0 < 0.0 || c0 >= 1.0 || c1 < 0.0 || c1 >= 1.0 || c2 < 0.0 || c2 >= 1.0)
+    throw std::invalid_argument("SpockParams: c0, c1, c2 must be in [0, 1)");
+  if (beta <= 0.0 || beta >= 1.0 || sigma <= 0.0 || sigma >= 1.0)
+    throw std::invalid_argument("SpockParams: beta, sigma must be in (0, 1)");
+  if (lambda <= 0.0 || lambda >= 2.0) throw std::invalid_argument("SpockParams: lambda must be in (0, 2)");
+  if (max_iters < 1 || max_backtracks < 1) throw std::invalid_argument("SpockParams: bad iteration caps");
+  if (aa_memory > 15) throw std::invalid_argument("SpockParams: aa_memory above 15 is not supported on device");
+}
+
+template <class Ty>
+Ty* Engine::dalloc(size_t n) {
+  void* p = nullptr;
+  CK(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(Ty)));
+  CK(cudaMemsetAsync(p, 0, std::max<size_t>(n, 1) * sizeof(Ty), st_));
+  allocs_.push_back(p);
+  return static_cast<Ty*>(p);
+}
+template <class Ty>
+Ty* Engine::dupload(const std::vector<Ty>& h) {
+  Ty* d = dalloc<Ty>(h.size());
+  if (!h.empty()) CK(cudaMemcpyAsync(d, h.data(), h.size() * sizeof(Ty), cudaMemcpyHostToDevice, st_));
+  return d;
+}
+
+Engine::Engine(const spock_problem_desc* desc, const Params& prm) : prm_(prm) {
+  prm_.validate();
+  raw_ = problem_from_desc(desc);
+  p_ = raw_;
+  pc_ = prm_.use_preconditioner ? precondition_inplace(p_) : identity_precond(p_);
+  soc_ = soc_epigraph_data(p_);
+  lay_ = make_layouts(p_, soc_);
+  require(p_.nx + p_.nu <= kMaxD, "spock-b200: nx + nu above 256 is not supported");
+  stage_start_ = p_.tree.stage_start;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+  upload();
+  factorize();
+  norm_.analytic_bound = analytic_norm_bound(p_, soc_);
+  power_iteration();
+  alpha_ = prm_.alpha > 0.0 ? prm_.alpha : 0.99 / std::max(norm_.estimate, 1e-300);
+  CK(cudaStreamSynchronize(st_));
+}
+
+Engine::~Engine() {
+  if (bench_graph_) cudaGraphExecDestroy(bench_graph_);
+  if (st_) cudaStreamSynchronize(st_);
+  for (void* p : allocs_) cudaFree(p);
+  if (host_red_) cudaFreeHost(host_red_);
+  if (st_) cudaStreamDestroy(st_);
+}
+
+// ---------------------------------------------------------------------------
+void Engine::upload() {
+  const Tree& tr = p_.tree;
+  const int nn = tr.nn(), nnl = tr.nnl(), nl = tr.nl(), nr = nn - 1, nx = p_.nx, nu = p_.nu;
+  Dev& D = D_;
+  D.nn = nn, D.nnl = nnl, D.nl = nl, D.nr = nr, D.nx = nx, D.nu = nu, D.N = tr.horizon;
+  D.nz = int(lay_.nz), D.neta = int(lay_.neta);
+  D.anc = dupload(tr.anc);
+  D.cf = dupload(tr.child_first);
+  D.cc = dupload(tr.child_count);
+  D.u_base = lay_.u_base, D.tau_base = lay_.tau_base, D.s_base = lay_.s_base;
+  D.y_base = lay_.u_base + nnl * nu;
+  D.y_off = dupload(lay_.y_off);
+  D.y_dim = dupload(lay_.y_dim);
+  D.s1_off = dupload(lay_.seg1_off);
+  D.s1_nc = dupload(lay_.seg1_nc);
+  D.s1_ydim = dupload(lay_.seg1_ydim);
+  D.s2_off = dupload(lay_.seg2_off);
+  D.s2_dim = dupload(lay_.seg2_dim);
+  D.s3_off = dupload(lay_.seg3_off);
+  D.s3_nc = dupload(lay_.seg3_nc);
+  D.s3_socdim = dupload(lay_.seg3_socdim);
+
+  // stage-cost SOC data
+  {
+    std::vector<int> px(nr), pu(nr);
+    std::vector<int64_t> hxo(nr), huo(nr), ao(nr);
+    int64_t sx = 0, su = 0, sa = 0;
+    for (int k = 0; k < nr; ++k) {
+      px[k] = soc_.stage[k].px;
+      pu[k] = soc_.stage[k].pu;
+      hxo[k] = sx;
+      huo[k] = su;
+      ao[k] = sa;
+      sx += int64_t(px[k]) * nx;
+      su += int64_t(pu[k]) * nu;
+      sa += px[k] + pu[k] + 2;
+    }
+    std::vector<double> Hx(sx), HxT(sx), Hu(su), HuT(su), qk(size_t(nr) * (nx + nu)), a(sa);
+    for (int k = 0; k < nr; ++k) {
+      const SocBlock& b = soc_.stage[k];
+      for (int j = 0; j < nx; ++j)
+        for (int r = 0; r < b.px; ++r) {
+          const double v = b.Hx[r + size_t(j) * b.px];
+          Hx[hxo[k] + r + size_t(j) * b.px] = v;
+          HxT[hxo[k] + j + size_t(r) * nx] = v;
+        }
+      for (int j = 0; j < nu; ++j)
+        for (int r = 0; r < b.pu; ++r) {
+          const double v = b.Hu[r + size_t(j) * b.pu];
+          Hu[huo[k] + r + size_t(j) * b.pu] = v;
+          HuT[huo[k] + j + size_t(r) * nu] = v;
+        }
+      std::copy(b.qk.begin(), b.qk.end(), qk.begin() + size_t(k) * (nx + nu));
+      std::copy(b.a.begin(), b.a.end(), a.begin() + ao[k]);
+    }
+    D.px = dupload(px);
+    D.pu = dupload(pu);
+    D.hx_off = dupload(hxo);
+    D.hu_off = dupload(huo);
+    D.Hx = dupload(Hx);
+    D.HxT = dupload(HxT);
+    D.Hu = dupload(Hu);
+    D.HuT = dupload(HuT);
+    D.qk = dupload(qk);
+    D.a_off = dupload(ao);
+    D.a = dupload(a);
+  }
+  // terminal SOC data
+  {
+    std::vector<int> pN(nl);
+    std::vector<int64_t> ho(nl), ao(nl);
+    int64_t sh = 0, sa = 0;
+    for (int j = 0; j < nl; ++j) {
+      pN[j] = soc_.leaf[j].px;
+      ho[j] = sh;
+      ao[j] = sa;
+      sh += int64_t(pN[j]) * nx;
+      sa += pN[j] + 2;
+    }
+    std::vector<double> HN(sh), HNT(sh), qk(size_t(nl) * nx), a(sa);
+    for (int j = 0; j < nl; ++j) {
+      const SocBlock& b = soc_.leaf[j];
+      for (int c = 0; c < nx; ++c)
+        for (int r = 0; r < b.px; ++r) {
+          const double v = b.Hx[r + size_t(c) * b.px];
+          HN[ho[j] + r + size_t(c) * b.px] = v;
+          HNT[ho[j] + c + size_t(r) * nx] = v;
+        }
+      std::copy(b.qk.begin(), b.qk.begin() + nx, qk.begin() + size_t(j) * nx);
+      std::copy(b.a.begin(), b.a.end(), a.begin() + ao[j]);
+    }
+    D.pN = dupload(pN);
+    D.hn_off = dupload(ho);
+    D.HN = dupload(HN);
+    D.HNT = dupload(HNT);
+    D.qkN = dupload(qk);
+    D.aN_off = dupload(ao);
+    D.aN = dupload(a);
+  }
+  // boundary permutation of eta (stage SOC head rows)
+  {
+    std::vector<int> perm(lay_.neta);
+    for (int64_t i = 0; i < lay_.neta; ++i) perm[i] = int(i);
+    perm_identity_ = true;
+    for (int k = 0; k < nr; ++k) {
+      const SocBlock& b = soc_.stage[k];
+      for (int r = 0; r < b.px + b.pu; ++r) {
+        perm[lay_.seg2_off[k] + r] = lay_.seg2_off[k] + b.perm[r];
+        if (b.perm[r] != r) perm_identity_ = false;
+      }
+    }
+    perm_eta_ = dupload(perm);
+  }
+  // constraints
+  {
+    bool gdiag = true;
+    for (int i = 0; i < nnl && gdiag; ++i) {
+      if (p_.nc[i] != nx + nu) {
+        gdiag = false;
+        break;
+      }
+      const size_t o = size_t(p_.g_off[i]);
+      const int nc = p_.nc[i];
+      for (int c = 0; c < nx && gdiag; ++c)
+        for (int r = 0; r < nc; ++r)
+          if (r != c && p_.Gx[o * nx + r + size_t(c) * nc] != 0.0) {
+            gdiag = false;
+            break;
+          }
+      for (int c = 0; c < nu && gdiag; ++c)
+        for (int r = 0; r < nc; ++r)
+          if (r != nx + c && p_.Gu[o * nu + r + size_t(c) * nc] != 0.0) {
+            gdiag = false;
+            break;
+          }
+    }
+    D.g_diag = gdiag ? 1 : 0;
+    const int64_t rows = p_.g_off[nnl];
+    std::vector<int64_t> goff(p_.g_off.begin(), p_.g_off.end() - 1);
+    D.g_off = dupload(goff);
+    D.lo = dupload(p_.C_lo);
+    D.hi = dupload(p_.C_hi);
+    if (gdiag) {
+      std::vector<double> gd(size_t(nnl) * (nx + nu));
+      for (int i = 0; i < nnl; ++i) {
+        const size_t o = size_t(p_.g_off[i]);
+        const int nc = p_.nc[i];
+        for (int r = 0; r < nx; ++r) gd[size_t(i) * (nx + nu) + r] = p_.Gx[o * nx + r + size_t(r) * nc];
+        for (int r = 0; r < nu; ++r) gd[size_t(i) * (nx + nu) + nx + r] = p_.Gu[o * nu + nx + r + size_t(r) * nc];
+      }
+      D.gd = dupload(gd);
+    } else {
+      std::vector<double> GxT(size_t(rows) * nx), GuT(size_t(rows) * nu);
+      for (int i = 0; i < nnl; ++i) {
+        const size_t o = size_t(p_.g_off[i]);
+        const int nc = p_.nc[i];
+        for (int c = 0; c < nx; ++c)
+          for (int r = 0; r < nc; ++r) GxT[o * nx + c + size_t(r) * nx] = p_.Gx[o * nx + r + size_t(c) * nc];
+        for (int c = 0; c < nu; ++c)
+          for (int r = 0; r < nc; ++r) GuT[o * nu + c + size_t(r) * nu] = p_.Gu[o * nu + r + size_t(c) * nc];
+      }
+      D.Gx = dupload(p_.Gx);
+      D.Gu = dupload(p_.Gu);
+      D.GxT = dupload(GxT);
+      D.GuT = dupload(GuT);
+    }
+    bool gndiag = true;
+    for (int j = 0; j < nl && gndiag; ++j) {
+      if (p_.ncN[j] != nx) {
+        gndiag = false;
+        break;
+      }
+      const size_t o = size_t(p_.gN_off[j]);
+      for (int c = 0; c < nx && gndiag; ++c)
+        for (int r = 0; r < nx; ++r)
+          if (r != c && p_.GN[o * nx + r + size_t(c) * nx] != 0.0) {
+            gndiag = false;
+            break;
+          }
+    }
+    D.gN_diag = gndiag ? 1 : 0;
+    std::vector<int64_t> gnoff(p_.gN_off.begin(), p_.gN_off.end() - 1);
+    D.gN_off = dupload(gnoff);
+    D.loN = dupload(p_.CN_lo);
+    D.hiN = dupload(p_.CN_hi);
+    if (gndiag) {
+      std::vector<double> gd(size_t(nl) * nx);
+      for (int j = 0; j < nl; ++j) {
+        const size_t o = size_t(p_.gN_off[j]);
+        for (int r = 0; r < nx; ++r) gd[size_t(j) * nx + r] = p_.GN[o * nx + r + size_t(r) * nx];
+      }
+      D.gNd = dupload(gd);
+    } else {
+      const int64_t rN = p_.gN_off[nl];
+      std::vector<double> GNT(size_t(rN) * nx);
+      for (int j = 0; j < nl; ++j) {
+        const size_t o = size_t(p_.gN_off[j]);
+        const int nc = p_.ncN[j];
+        for (int c = 0; c < nx; ++c)
+          for (int r = 0; r < nc; ++r) GNT[o * nx + c + size_t(r) * nx] = p_.GN[o * nx + r + size_t(c) * nc];
+      }
+      D.GN = dupload(p_.GN);
+      D.GNT = dupload(GNT);
+    }
+  }
+  // risk: b, dual cone of the y-copy rows, S2 kind
+  {
+    std::vector<double> rb;
+    std::vector<int> ycn(nnl), ypo(nnl + 1, 0), ykind, ydim, s2k(nnl);
+    std::vector<double> s2g(nnl, 0.0);
+    std::vector<int64_t> s2po(nnl, 0);
+    std::vector<double> s2P;
+    for (int i = 0; i < nnl; ++i) {
+      const Risk& rs = p_.risk[i];
+      rb.insert(rb.end(), rs.b.begin(), rs.b.end());
+      std::vector<ConePart> dk;
+      for (const auto& cp : rs.cone) {
+        if (cp.kind == SPOCK_CONE_ZERO)
+          dk.push_back({SPOCK_CONE_FREE, cp.dim});
+        else if (cp.kind == SPOCK_CONE_FREE)
+          dk.push_back({SPOCK_CONE_ZERO, cp.dim});
+        else
+          dk.push_back(cp);
+      }
+      bool simple = true;
+      int nonneg = 0;
+      for (size_t t = 0; t < dk.size(); ++t) {
+        if (t == 0 && dk[t].kind == SPOCK_CONE_NONNEG)
+          nonneg = dk[t].dim;
+        else if (dk[t].kind != SPOCK_CONE_FREE)
+          simple = false;
+      }
+      ycn[i] = simple ? nonneg : -1;
+      for (const auto& cp : dk) {
+        ykind.push_back(cp.kind);
+        ydim.push_back(cp.dim);
+      }
+      ypo[i + 1] = int(ykind.size());
+      // S2 closed form detection on E (exact structure of the AV@R forms)
+      const int n = rs.n, ny = rs.rows;
+      auto E = [&](int r, int c) { return rs.E[r + size_t(c) * ny]; };
+      int kind = S2_DENSE;
+      double gam = 0.0;
+      if (rs.nnu == 0) {
+        if (ny == 2 * n + 1 && E(0, 0) > 0.0) {
+          gam = E(0, 0);
+          bool ok = true;
+          for (int c = 0; c < n && ok; ++c)
+            for (int r = 0; r < ny; ++r) {
+              double want = 0.0;
+              if (r < n) want = (r == c) ? gam : 0.0;
+              else if (r < 2 * n) want = (r - n == c) ? -1.0 : 0.0;
+              else want = 1.0;
+              if (E(r, c) != want) {
+                ok = false;
+                break;
+              }
+            }
+          if (ok) kind = S2_AVAR;
+        } else if (ny == n + 1) {
+          bool ok = true;
+          for (int c = 0; c < n && ok; ++c)
+            for (int r = 0; r < ny; ++r) {
+              const double want = r < n ? ((r == c) ? -1.0 : 0.0) : 1.0;
+              if (E(r, c) != want) {
+                ok = false;
+                break;
+              }
+            }
+          if (ok) kind = S2_MAX;
+        } else if (ny == n) {
+          bool ok = true;
+          for (int c = 0; c < n && ok; ++c)
+            for (int r = 0; r < ny; ++r)
+              if (E(r, c) != (r == c ? 1.0 : 0.0)) {
+                ok = false;
+                break;
+              }
+          if (ok) kind = S2_EQ;
+        }
+      }
+      s2k[i] = kind;
+      s2g[i] = gam;
+      if (kind == S2_DENSE) {
+        // projector onto ker M, M = [E' -I -I; F' 0 0] (projections.cpp:114-137):
+        // N = I - M'(MM')^+ M with a relative eigenvalue threshold on MM'
+        const int dim = ny + 2 * n, mr = n + rs.nnu;
+        require(dim <= kMaxD, "spock-b200: general risk spec with y+2*children above 256 is not supported");
+        Mat M(mr, dim);
+        for (int c = 0; c < n; ++c) {
+          for (int r = 0; r < ny; ++r) M(c, r) = E(r, c);
+          M(c, ny + c) = -1.0;
+          M(c, ny + n + c) = -1.0;
+        }
+        for (int c = 0; c < rs.nnu; ++c)
+          for (int r = 0; r < ny; ++r) M(n + c, r) = rs.F[r + size_t(c) * ny];
+        Mat MM(mr, mr);
+        for (int a2 = 0; a2 < mr; ++a2)
+          for (int b2 = 0; b2 < mr; ++b2) {
+            double s = 0.0;
+            for (int t = 0; t < dim; ++t) s += M(a2, t) * M(b2, t);
+            MM(a2, b2) = s;
+          }
+        Vec w;
+        Mat V;
+        sym_eig(MM, w, V);
+        const double lmax = w.empty() ? 0.0 : w.back();
+        Mat Pinv(mr, mr);
+        for (int t = 0; t < mr; ++t) {
+          if (!(w[t] > 1e-14 * lmax)) continue;
+          for (int b2 = 0; b2 < mr; ++b2)
+            for (int a2 = 0; a2 < mr; ++a2) Pinv(a2, b2) += V(a2, t) * V(b2, t) / w[t];
+        }
+        s2po[i] = int64_t(s2P.size());
+        s2P.resize(s2P.size() + size_t(dim) * dim);
+        double* N = &s2P[s2po[i]];
+        for (int c = 0; c < dim; ++c)
+          for (int r = 0; r < dim; ++r) {
+            double s = (r == c) ? 1.0 : 0.0;
+            for (int a2 = 0; a2 < mr; ++a2) {
+              double t2 = 0.0;
+              for (int b2 = 0; b2 < mr; ++b2) t2 += Pinv(a2, b2) * M(b2, c);
+              s -= M(a2, r) * t2;
+            }
+            N[r + size_t(c) * dim] = s;
+          }
+      }
+    }
+    D.rb = dupload(rb);
+    D.yc_nonneg = dupload(ycn);
+    D.yc_poff = dupload(ypo);
+    D.yc_kind = dupload(ykind);
+    D.yc_dim = dupload(ydim);
+    D.s2_kind = dupload(s2k);
+    D.s2_gamma = dupload(s2g);
+    D.s2p_off = dupload(s2po);
+    D.s2P = dupload(s2P);
+  }
+  // factor buffers (filled by factorize) and scratch
+  D.M1 = dalloc<double>(size_t(nr) * nx * (nx + nu));
+  D.M1T = dalloc<double>(size_t(nr) * nx * (nx + nu));
+  D.cvec = dupload(p_.c);
+  D.K = dalloc<double>(size_t(nnl) * nu * nx);
+  D.KT = dalloc<double>(size_t(nnl) * nu * nx);
+  D.Rinv = dalloc<double>(size_t(nnl) * nu * nu);
+  D.g = dalloc<double>(size_t(nnl) * nu);
+  D.h = dalloc<double>(size_t(nnl) * nx);
+  xinit_ = dalloc<double>(nx);
+  D.xinit = xinit_;
+  D.T12 = dalloc<double>(size_t(nr) * (nx + nu));
+  D.adj = dalloc<double>(size_t(nr) * (nx + nu));
+  D.dvec = dalloc<double>(size_t(nnl) * nu);
+  // termination scalings d1 (z) and d2 (eta), proj/src/solver.cpp:100-109
+  {
+    std::vector<double> d1(lay_.nz, 1.0), d2(lay_.neta, 1.0);
+    if (!pc_.is_identity) {
+      for (int i = 0; i < nn; ++i) {
+        const Vec& s = tr.leaf(i) ? pc_.sxN : pc_.sx;
+        for (int k = 0; k < nx; ++k) d1[1 + size_t(i) * nx + k] = s[k];
+        if (i < nnl)
+          for (int k = 0; k < nu; ++k) d1[lay_.u_base + size_t(i) * nu + k] = pc_.su[k];
+      }
+      for (int i = 0; i < nnl; ++i)
+        for (int k = 0; k < lay_.seg1_nc[i]; ++k)
+          d2[lay_.seg1_off[i] + lay_.seg1_ydim[i] + 1 + k] = pc_.cstr_scale[i];
+    }
+    d1_ = dupload(d1);
+    d2_ = dupload(d2);
+  }
+  partial_ = dalloc<double>(size_t(4) * kMaxDots * kRedBlocks);
+  red_out_ = dalloc<double>(256);
+  CK(cudaMallocHost(&host_red_, 256 * sizeof(double)));
+  for (int t = 0; t < 3; ++t) {
+    scratch_z_[t] = dalloc<double>(lay_.nz);
+    scratch_e_[t] = dalloc<double>(lay_.neta);
+  }
+  set_xinit(raw_.x_init.data());
+}
+
+void Engine::set_xinit(const double* x) {
+  std::vector<double> xs(p_.nx);
+  for (int k = 0; k < p_.nx; ++k) xs[k] = pc_.is_identity ? x[k] : pc_.sx[k] * x[k];
+  CK(cudaMemcpyAsync(xinit_, xs.data(), sizeof(double) * p_.nx, cudaMemcpyHostToDevice, st_));
+  CK(cudaStreamSynchronize(st_));
+}
+
+// ---------------------------------------------------------------------------
+// Alg. 1 on device, stage by stage (projections.cpp:77-112), followed by the
+// per-iteration factors of the restructured sweep (see kernels.cu).
+void Engine::factorize() {
+  const Tree& tr = p_.tree;
+  const int nn = tr.nn(), nr = nn - 1, nx = p_.nx, nu = p_.nu, N = tr.horizon;
+  std::vector<void*> tmp;
+  auto talloc = [&](size_t n) {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(double)));
+    tmp.push_back(p);
+    return static_cast<double*>(p);
+  };
+  double* dA = talloc(size_t(nr) * nx * nx);
+  double* dB = talloc(size_t(nr) * nx * nu);
+  CK(cudaMemcpyAsync(dA, p_.A.data(), sizeof(double) * p_.A.size(), cudaMemcpyHostToDevice, st_));
+  CK(cudaMemcpyAsync(dB, p_.B.data(), sizeof(double) * p_.B.size(), cudaMemcpyHostToDevice, st_));
+  double* P = talloc(size_t(nn) * nx * nx);
+  double* PB = talloc(size_t(nr) * nx * nu);
+  double* PA = talloc(size_t(nr) * nx * nx);
+  double* e = talloc(size_t(nr) * nx);
+  double* rt = talloc(size_t(nr) * nu * nu);
+  double* kt = talloc(size_t(nr) * nu * nx);
+  double* ge = talloc(size_t(nr) * nu);
+  double* tt = talloc(size_t(nr) * nx * nx);
+  double* pt = talloc(size_t(nr) * nx * nx);
+  double* he = talloc(size_t(nr) * nx);
+  int* derr = nullptr;
+  CK(cudaMalloc(&derr, sizeof(int)));
+  tmp.push_back(derr);
+  CK(cudaMemsetAsync(derr, 0, sizeof(int), st_));
+  // leaves: P = I
+  {
+    std::vector<double> I(size_t(nn) * nx * nx, 0.0);
+    for (int j = tr.stage_start[N]; j < nn; ++j)
+      for (int k = 0; k < nx; ++k) I[size_t(j) * nx * nx + k + size_t(k) * nx] = 1.0;
+    CK(cudaMemcpyAsync(P, I.data(), sizeof(double) * I.size(), cudaMemcpyHostToDevice, st_));
+    CK(cudaStreamSynchronize(st_));
+  }
+  // pointer arrays for batched GEMMs (rebuilt per stage)
+  const size_t maxw = size_t(nr) + 1;
+  const double** hA = new const double*[maxw];
+  const double** hBp = new const double*[maxw];
+  double** hC = new double*[maxw];
+  const double** dAp = nullptr;
+  const double** dBp = nullptr;
+  double** dCp = nullptr;
+  CK(cudaMalloc(&dAp, sizeof(void*) * maxw));
+  CK(cudaMalloc(&dBp, sizeof(void*) * maxw));
+  CK(cudaMalloc(&dCp, sizeof(void*) * maxw));
+  tmp.push_back(dAp);
+  tmp.push_back(dBp);
+  tmp.push_back(dCp);
+  auto gemm = [&](int cnt, int m, int n, int k, int lda, int ldb, int ldc, int ta, int tb, double alpha,
+                  double beta) {
+    if (cnt <= 0) return;
+    CK(cudaMemcpyAsync(dAp, hA, sizeof(void*) * cnt, cudaMemcpyHostToDevice, st_));
+    CK(cudaMemcpyAsync(dBp, hBp, sizeof(void*) * cnt, cudaMemcpyHostToDevice, st_));
+    CK(cudaMemcpyAsync(dCp, hC, sizeof(void*) * cnt, cudaMemcpyHostToDevice, st_));
+    BGemmArgs G{dAp, dBp, dCp, m, n, k, lda, ldb, ldc, ta, tb, alpha, beta};
+    launch_bgemm(G, cnt, st_);
+    CK(cudaStreamSynchronize(st_));  // host pointer arrays are reused
+  };
+  Alg1Args A1{};
+  A1.nx = nx;
+  A1.nu = nu;
+  A1.cf = D_.cf;
+  A1.cc = D_.cc;
+  A1.anc = D_.anc;
+  A1.A = dA;
+  A1.B = dB;
+  A1.rt = rt;
+  A1.kt = kt;
+  A1.ge = ge;
+  A1.pt = pt;
+  A1.he = he;
+  A1.P = P;
+  A1.K = const_cast<double*>(D_.K);
+  A1.KT = const_cast<double*>(D_.KT);
+  A1.Rinv = const_cast<double*>(D_.Rinv);
+  A1.g = const_cast<double*>(D_.g);
+  A1.h = const_cast<double*>(D_.h);
+  A1.M1 = const_cast<double*>(D_.M1);
+  A1.M1T = const_cast<double*>(D_.M1T);
+  A1.err = derr;
+  const int smem = int(sizeof(double) * (2 * nu * nu + nu * nx));
+  if (smem > 48 * 1024) CK(set_alg1_smem(smem));
+  const double* dcv = D_.cvec;
+  for (int t = N - 1; t >= 0; --t) {
+    const int cb = tr.stage_start[t + 1], ce = tr.stage_start[t + 2], cnt = ce - cb;
+    const int pb = tr.stage_start[t], pe = tr.stage_start[t + 1];
+    // PB = P_c B, PA = P_c A, e = P_c c
+    for (int c = cb; c < ce; ++c) {
+      hA[c - cb] = P + size_t(c) * nx * nx;
+      hBp[c - cb] = dB + size_t(c - 1) * nx * nu;
+      hC[c - cb] = PB + size_t(c - 1) * nx * nu;
+    }
+    gemm(cnt, nx, nu, nx, nx, nx, nx, 0, 0, 1.0, 0.0);
+    for (int c = cb; c < ce; ++c) {
+      hBp[c - cb] = dA + size_t(c - 1) * nx * nx;
+      hC[c - cb] = PA + size_t(c - 1) * nx * nx;
+    }
+    gemm(cnt, nx, nx, nx, nx, nx, nx, 0, 0, 1.0, 0.0);
+    for (int c = cb; c < ce; ++c) {
+      hBp[c - cb] = dcv + size_t(c - 1) * nx;
+      hC[c - cb] = e + size_t(c - 1) * nx;
+    }
+    gemm(cnt, nx, 1, nx, nx, nx, nx, 0, 0, 1.0, 0.0);
+    // rt = B'PB, kt = B'PA, ge = B'e
+    for (int c = cb; c < ce; ++c) {
+      hA[c - cb] = dB + size_t(c - 1) * nx * nu;
+      hBp[c - cb] = PB + size_t(c - 1) * nx * nu;
+      hC[c - cb] = rt + size_t(c - 1) * nu * nu;
+    }
+    gemm(cnt, nu, nu, nx, nx, nx, nu, 1, 0, 1.0, 0.0);
+    for (int c = cb; c < ce; ++c) {
+      hBp[c - cb] = PA + size_t(c - 1) * nx * nx;
+      hC[c - cb] = kt + size_t(c - 1) * nu * nx;
+    }
+    gemm(cnt, nu, nx, nx, nx, nx, nu, 1, 0, 1.0, 0.0);
+    for (int c = cb; c < ce; ++c) {
+      hBp[c - cb] = e + size_t(c - 1) * nx;
+      hC[c - cb] = ge + size_t(c - 1) * nu;
+    }
+    gemm(cnt, nu, 1, nx, nx, nx, nu, 1, 0, 1.0, 0.0);
+    // parents: Rt, Cholesky, Rinv, K, g
+    A1.b = pb;
+    launch_alg1_parent(A1, pe - pb, st_);
+    // children: Abar = A + B K_anc -> M1, M1'
+    A1.b = cb;
+    launch_alg1_child_abar(A1, cnt, st_);
+    // tt = P_c Abar ; pt = Abar' tt ; he = Abar' e
+    for (int c = cb; c < ce; ++c) {
+      hA[c - cb] = P + size_t(c) * nx * nx;
+      hBp[c - cb] = D_.M1 + size_t(c - 1) * nx * (nx + nu);
+      hC[c - cb] = tt + size_t(c - 1) * nx * nx;
+    }
+    gemm(cnt, nx, nx, nx, nx, nx, nx, 0, 0, 1.0, 0.0);
+    for (int c = cb; c < ce; ++c) {
+      hA[c - cb] = D_.M1 + size_t(c - 1) * nx * (nx + nu);
+      hBp[c - cb] = tt + size_t(c - 1) * nx * nx;
+      hC[c - cb] = pt + size_t(c - 1) * nx * nx;
+    }
+    gemm(cnt, nx, nx, nx, nx, nx, nx, 1, 0, 1.0, 0.0);
+    for (int c = cb; c < ce; ++c) {
+      hBp[c - cb] = e + size_t(c - 1) * nx;
+      hC[c - cb] = he + size_t(c - 1) * nx;
+    }
+    gemm(cnt, nx, 1, nx, nx, nx, nx, 1, 0, 1.0, 0.0);
+    // parents: P = I + K'K + sum pt ; h = sum he
+    A1.b = pb;
+    launch_alg1_parent2(A1, pe - pb, st_);
+  }
+  CK(cudaGetLastError());
+  int herr = 0;
+  CK(cudaMemcpyAsync(&herr, derr, sizeof(int), cudaMemcpyDeviceToHost, st_));
+  CK(cudaStreamSynchronize(st_));
+  delete[] hA;
+  delete[] hBp;
+  delete[] hC;
+  for (void* p : tmp) cudaFree(p);
+  if (herr) throw std::runtime_error("make_solver_cache: Cholesky failed (corrupt dynamics data)");
+}
+
+// ---------------------------------------------------------------------------
+void Engine::sync() { CK(cudaStreamSynchronize(st_)); }
+
+void Engine::L(const double* z, double* eta) { launch_L(D_, z, 1.0, nullptr, 0.0, nullptr, eta, 0.0, false, st_); }
+
+void Engine::Lt(const double* eta, double* z) { launch_Lt(D_, eta, nullptr, z, 0.0, 1.0, 0.0, st_); }
+
+// one CP application (solver.cpp:148-164), internal layout; zo/eo must not
+// alias z/eta
+void Engine::T(const double* z, const double* eta, double* zo, double* eo) {
+  launch_Lt(D_, eta, z, zo, 1.0, -alpha_, -alpha_, st_);
+  launch_s1(D_, stage_start_.data(), zo, st_);
+  launch_s2(D_, zo, st_);
+  launch_L(D_, zo, 2.0, z, -1.0, eta, eo, alpha_, true, st_);
+}
+
+void Engine::dots(std::initializer_list<std::pair<const double*, const double*>> pairs, int64_t n_default,
+                  const std::vector<int64_t>& ns, double* host_out) {
+  DotArgs A{};
+  int j = 0;
+  for (const auto& pr : pairs) {
+    A.x[j] = pr.first;
+    A.y[j] = pr.second;
+    A.n[j] = int(j < int(ns.size()) ? ns[j] : n_default);
+    ++j;
+  }
+  A.ndots = j;
+  launch_dots(A, partial_, red_out_, st_);
+  CK(cudaMemcpyAsync(host_red_, red_out_, sizeof(double) * j, cudaMemcpyDeviceToHost, st_));
+  sync();
+  for (int k = 0; k < j; ++k) host_out[k] = host_red_[k];
+}
+
+// power iteration on L*L (tree_operator.cpp:157-205) with device operators
+void Engine::power_iteration() {
+  const int64_t nz = lay_.nz, ne = lay_.neta;
+  std::vector<double> v(nz);
+  philox_normals(0x9E3779B97F4A7C15ull, nz, v.data());
+  double vn = 0.0;
+  for (double x : v) vn += x * x;
+  vn = std::sqrt(vn);
+  for (auto& x : v) x /= vn;
+  double* dv = scratch_z_[0];
+  double* du = scratch_e_[0];
+  double* dw = scratch_z_[1];
+  CK(cudaMemcpyAsync(dv, v.data(), sizeof(double) * nz, cudaMemcpyHostToDevice, st_));
+  const double tol = 1e-6;
+  const int max_iters = 500;
+  double prev = 0.0, prev_change = 0.0;
+  for (int it = 1; it <= max_iters; ++it) {
+    L(dv, du);
+    double r;
+    dots({{du, du}}, ne, {}, &r);
+    const double est = std::sqrt(r);
+    norm_.estimate = est;
+    norm_.iterations = it;
+    if (est == 0.0) {
+      norm_.converged = true;
+      break;
+    }
+    if (it > 2) {
+      const double change = std::fabs(est - prev);
+      double ratio = prev_change > 0.0 ? change / prev_change : 0.0;
+      ratio = std::min(ratio, 0.999);
+      const double remaining = change * ratio / (1.0 - ratio);
+      if (change + remaining <= tol * est) {
+        norm_.converged = true;
+        break;
+      }
+      prev_change = change;
+    } else if (it == 2) {
+      prev_change = std::fabs(est - prev);
+    }
+    prev = est;
+    Lt(du, dw);
+    double wn2;
+    dots({{dw, dw}}, nz, {}, &wn2);
+    const double wn = std::sqrt(wn2);
+    if (wn == 0.0) {
+      norm_.converged = true;
+      break;
+    }
+    launch_axpby(int(nz), 1.0 / wn, dw, 0.0, nullptr, dv, st_);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// boundary conversions
+void Engine::copy_in_z(const double* src, double* dst) {
+  CK(cudaMemcpyAsync(dst, src, sizeof(double) * lay_.nz, cudaMemcpyDefault, st_));
+}
+void Engine::to_internal_eta(const double* src, double* dst) {
+  if (perm_identity_) {
+    CK(cudaMemcpyAsync(dst, src, sizeof(double) * lay_.neta, cudaMemcpyDefault, st_));
+    return;
+  }
+  const double* s = src;
+  if (!is_device_ptr(src)) {
+    CK(cudaMemcpyAsync(scratch_e_[2], src, sizeof(double) * lay_.neta, cudaMemcpyHostToDevice, st_));
+    s = scratch_e_[2];
+  }
+  launch_gather(int(lay_.neta), perm_eta_, s, dst, st_);
+}
+void Engine::from_internal_eta(const double* src, double* dst) {
+  if (perm_identity_) {
+    CK(cudaMemcpyAsync(dst, src, sizeof(double) * lay_.neta, cudaMemcpyDefault, st_));
+    return;
+  }
+  if (is_device_ptr(dst)) {
+    launch_scatter(int(lay_.neta), perm_eta_, src, dst, st_);
+  } else {
+    launch_scatter(int(lay_.neta), perm_eta_, src, scratch_e_[2], st_);
+    CK(cudaMemcpyAsync(dst, scratch_e_[2], sizeof(double) * lay_.neta, cudaMemcpyDeviceToHost, st_));
+  }
+}
+void Engine::copy_out(const double* src, double* dst, int64_t n) {
+  CK(cudaMemcpyAsync(dst, src, sizeof(double) * n, cudaMemcpyDefault, st_));
+}
+
+void Engine::apply_T_b(const double* z, const double* eta, double* zo, double* eo) {
+  double *iz = scratch_z_[0], *ie = scratch_e_[0], *oz = scratch_z_[1], *oe = scratch_e_[1];
+  copy_in_z(z, iz);
+  to_internal_eta(eta, ie);
+  T(iz, ie, oz, oe);
+  copy_out(oz, zo, lay_.nz);
+  from_internal_eta(oe, eo);
+  sync();
+}
+void Engine::apply_L_b(const double* z, double* eta) {
+  copy_in_z(z, scratch_z_[0]);
+  L(scratch_z_[0], scratch_e_[0]);
+  from_internal_eta(scratch_e_[0], eta);
+  sync();
+}
+void Engine::apply_Lt_b(const double* eta, double* z) {
+  to_internal_eta(eta, scratch_e_[0]);
+  Lt(scratch_e_[0], scratch_z_[0]);
+  copy_out(scratch_z_[0], z, lay_.nz);
+  sync();
+}
+double Engine::m_norm_b(const double* z, const double* eta, double alpha) {  // tree_operator.cpp:214-222
+  copy_in_z(z, scratch_z_[0]);
+  to_internal_eta(eta, scratch_e_[0]);
+  L(scratch_z_[0], scratch_e_[1]);
+  double r[3];
+  dots({{scratch_z_[0], scratch_z_[0]}, {scratch_e_[0], scratch_e_[1]}, {scratch_e_[0], scratch_e_[0]}}, 0,
+       {lay_.nz, lay_.neta, lay_.neta}, r);
+  const double rad = r[0] - 2.0 * alpha * r[1] + r[2];
+  if (rad < -1e-12 * std::max(1.0, r[0] + r[2]))
+    throw std::runtime_error("m_norm: negative radicand (alpha violates alpha*||L|| < 1)");
+  return std::sqrt(std::max(0.0, rad));
+}
+void Engine::proj_s1_b(double* z) {
+  copy_in_z(z, scratch_z_[0]);
+  launch_s1(D_, stage_start_.data(), scratch_z_[0], st_);
+  copy_out(scratch_z_[0], z, lay_.nz);
+  sync();
+}
+void Engine::proj_s2_b(double* z) {
+  copy_in_z(z, scratch_z_[0]);
+  launch_s2(D_, scratch_z_[0], st_);
+  copy_out(scratch_z_[0], z, lay_.nz);
+  sync();
+}
+void Engine::proj_s3_b(double* eta) {
+  to_internal_eta(eta, scratch_e_[0]);
+  launch_s3(D_, scratch_e_[0], st_);
+  from_internal_eta(scratch_e_[0], eta);
+  sync();
+}
+void Engine::unscale_b(const double* zs, double* z) {  // solver.cpp:116-130
+  std::vector<double> h(lay_.nz);
+  CK(cudaMemcpyAsync(h.data(), zs, sizeof(double) * lay_.nz, cudaMemcpyDefault, st_));
+  sync();
+  if (!pc_.is_identity) {
+    const Tree& tr = p_.tree;
+    for (int i = 0; i < tr.nn(); ++i) {
+      const Vec& s = tr.leaf(i) ? pc_.sxN : pc_.sx;
+      for (int k = 0; k < p_.nx; ++k) h[1 + size_t(i) * p_.nx + k] /= s[k];
+      if (i < tr.nnl())
+        for (int k = 0; k < p_.nu; ++k) h[lay_.u_base + size_t(i) * p_.nu + k] /= pc_.su[k];
+    }
+  }
+  CK(cudaMemcpyAsync(z, h.data(), sizeof(double) * lay_.nz, cudaMemcpyDefault, st_));
+  sync();
+}
+
+// ---------------------------------------------------------------------------
+// SuperMann / CP loop (proj/src/solver.cpp:189-350).  State lives on device;
+// one host round trip per iteration (omega, xi norms and the Anderson Gram
+// matrix come back together) plus one per line-search trial.
+void Engine::solve_b(const double* x_init, const double* wz, const double* we, double* oz, double* ozs, double* oe,
+                     bool supermann, Status& st) {
+  const int64_t nz = lay_.nz, ne = lay_.neta, nv = nz + ne;
+  set_xinit(x_init ? x_init : raw_.x_init.data());
+  const int m = prm_.aa_memory;
+  // pair buffers: [z | eta] contiguous so Anderson works on the stacked vector
+  std::vector<double*> bufs;
+  auto pair = [&]() {
+    double* p = nullptr;
+    CK(cudaMallocAsync(&p, sizeof(double) * nv, st_));
+    bufs.push_back(p);
+    return p;
+  };
+  double *V = pair(), *TV = pair(), *R = pair(), *C = pair(), *TC = pair(), *CR = pair(), *PV = pair(),
+         *PSI = pair();
+  double *Lrz = nullptr, *cLrz = nullptr, *Lsre = nullptr, *tmpz = nullptr, *tmpe = nullptr;
+  CK(cudaMallocAsync(&Lrz, sizeof(double) * ne, st_));
+  CK(cudaMallocAsync(&cLrz, sizeof(double) * ne, st_));
+  CK(cudaMallocAsync(&Lsre, sizeof(double) * nz, st_));
+  CK(cudaMallocAsync(&tmpz, sizeof(double) * nz, st_));
+  CK(cudaMallocAsync(&tmpe, sizeof(double) * ne, st_));
+  std::vector<double*> RH(m + 1), DH(m);  // residual / difference history, newest at index 0
+  for (auto& p : RH) p = pair();
+  for (auto& p : DH) p = pair();
+  CK(cudaMemsetAsync(V, 0, sizeof(double) * nv, st_));
+  if (wz || we) {
+    if (!wz || !we) throw std::invalid_argument("solve: warm start has wrong dimensions");
+    copy_in_z(wz, V);
+    to_internal_eta(we, V + nz);
+  }
+  auto cleanup = [&]() {
+    for (double* p : bufs) cudaFreeAsync(p, st_);
+    cudaFreeAsync(Lrz, st_);
+    cudaFreeAsync(cLrz, st_);
+    cudaFreeAsync(Lsre, st_);
+    cudaFreeAsync(tmpz, st_);
+    cudaFreeAsync(tmpe, st_);
+    cudaStreamSynchronize(st_);
+  };
+  const double alpha = alpha_;
+  auto refresh = [&](const double* v, double* tv, double* r, double* lrz) {  // T, r = v - Tv, L rz
+    T(v, v + nz, tv, tv + nz);
+    ++st.n_T;
+    launch_axpby(int(nv), 1.0, v, -1.0, tv, r, st_);
+    L(r, lrz);
+    ++st.n_L;
+  };
+  // queue the M-norm dots of (r, lrz) into red_out_[base..base+3)
+  auto queue_mnorm = [&](const double* r, const double* lrz, int base) {
+    DotArgs A{};
+    A.x[0] = r, A.y[0] = r, A.n[0] = int(nz);
+    A.x[1] = r + nz, A.y[1] = lrz, A.n[1] = int(ne);
+    A.x[2] = r + nz, A.y[2] = r + nz, A.n[2] = int(ne);
+    A.ndots = 3;
+    launch_dots(A, partial_, red_out_ + base, st_);
+  };
+  auto mnorm_of = [&](const double* h) {  // solver.cpp:166-174
+    const double rad = h[0] - 2.0 * alpha * h[1] + h[2];
+    if (rad < -1e-12 * std::max(1.0, h[0] + h[2]))
+      throw std::runtime_error("spock: negative M-norm radicand (alpha too large)");
+    return std::sqrt(std::max(0.0, rad));
+  };
+  auto fetch = [&](int n) {
+    CK(cudaMemcpyAsync(host_red_, red_out_, sizeof(double) * n, cudaMemcpyDeviceToHost, st_));
+    sync();
+  };
+  int aa_k = 0;  // Anderson call counter
+  int aa_cols = 0;
+  try {
+    refresh(V, TV, R, Lrz);
+    queue_mnorm(R, Lrz, 0);
+    bool have_omega = false;
+    double omega = 0.0, zeta = 0.0, omega_safe = 0.0, th1 = 0.0, th2 = 0.0;
+    for (int k = 0;; ++k) {
+      // xi residuals (solver.cpp:240-244)
+      Lt(R + nz, Lsre);
+      ++st.n_Lt;
+      XiArgs X{};
+      X.x[0] = R, X.y[0] = Lsre, X.d[0] = d1_, X.n[0] = int(nz);
+      X.x[1] = R + nz, X.y[1] = Lrz, X.d[1] = d2_, X.n[1] = int(ne);
+      X.alpha = alpha;
+      launch_xi(X, partial_ + kMaxDots * kRedBlocks, red_out_ + 4, st_);
+      // Anderson push (solver.cpp:57-63) and Gram of the differences
+      int ngram = 0;
+      if (supermann) {
+        std::rotate(RH.begin(), RH.end() - 1, RH.end());
+        std::rotate(DH.begin(), DH.end() - 1, DH.end());
+        CK(cudaMemcpyAsync(RH[0], R, sizeof(double) * nv, cudaMemcpyDeviceToDevice, st_));
+        if (aa_k == 0)
+          CK(cudaMemcpyAsync(DH[0], R, sizeof(double) * nv, cudaMemcpyDeviceToDevice, st_));
+        else
+          launch_axpby(int(nv), 1.0, RH[0], -1.0, RH[1], DH[0], st_);
+        aa_cols = std::min(aa_cols + 1, m);
+        if (aa_k > m) {
+          // Gram of the differences and M_d' r, in chunks of kMaxDots dots
+          std::vector<std::pair<const double*, const double*>> prs;
+          for (int a = 0; a < aa_cols; ++a)
+            for (int b = a; b < aa_cols; ++b) prs.push_back({DH[a], DH[b]});
+          for (int a = 0; a < aa_cols; ++a) prs.push_back({DH[a], R});
+          for (size_t c0 = 0; c0 < prs.size(); c0 += kMaxDots) {
+            DotArgs A{};
+            int j = 0;
+            for (size_t q = c0; q < prs.size() && j < kMaxDots; ++q, ++j) {
+              A.x[j] = prs[q].first, A.y[j] = prs[q].second, A.n[j] = int(nv);
+            }
+            A.ndots = j;
+            launch_dots(A, partial_ + 2 * kMaxDots * kRedBlocks, red_out_ + 8 + c0, st_);
+          }
+          ngram = int(prs.size());
+        }
+      }
+      fetch(8 + ngram);
+      if (!have_omega) {
+        omega = mnorm_of(host_red_);
+        zeta = omega_safe = omega;
+        have_omega = true;
+      }
+      const double n1 = host_red_[4], n2 = host_red_[5];
+      if (k == 0) {
+        th1 = std::max(prm_.eps_abs, prm_.eps_rel * n1);
+        th2 = std::max(prm_.eps_abs, prm_.eps_rel * n2);
+      }
+      st.iterations = k;
+      st.xi1 = n1;
+      st.xi2 = n2;
+      int reason = -1;
+      if (!std::isfinite(n1) || !std::isfinite(n2) || !std::isfinite(omega))
+        reason = SPOCK_STALLED;
+      else if (n1 <= th1 && n2 <= th2)
+        reason = SPOCK_CONVERGED;
+      else if (k >= prm_.max_iters)
+        reason = SPOCK_MAX_ITERS;
+      else if (prm_.cancelled && (k % std::max(1, prm_.poll_every) == 0) && prm_.cancelled())
+        reason = SPOCK_CANCELLED;
+      if (reason >= 0) {
+        st.reason = reason;
+        if (ozs) copy_out(TV, ozs, nz);
+        if (oe) from_internal_eta(TV + nz, oe);
+        sync();
+        if (oz) unscale_b(TV, oz);
+        cleanup();
+        return;
+      }
+      st.rnorm.push_back(omega);
+      if (!supermann) {
+        std::swap(V, TV);
+        st.branches.push_back('K');
+        if (prm_.progress) prm_.progress(k, omega, 'K');
+        refresh(V, TV, R, Lrz);
+        queue_mnorm(R, Lrz, 0);
+        have_omega = false;
+        continue;
+      }
+      // Anderson direction (solver.cpp:64-76)
+      const int kk = aa_k++;
+      if (kk <= m) {
+        launch_axpby(int(nv), -1.0, R, 0.0, nullptr, PSI, st_);
+      } else {
+        // kappa = argmin ||M_d kappa - r|| by column-pivoted Cholesky of the
+        // Gram matrix (the R factor of a column-pivoted QR of M_d)
+        const int cols = aa_cols;
+        std::vector<double> G(cols * cols), gr(cols);
+        int j = 0;
+        for (int a = 0; a < cols; ++a)
+          for (int b = a; b < cols; ++b) {
+            G[a + b * cols] = G[b + a * cols] = host_red_[8 + j];
+            ++j;
+          }
+        for (int a = 0; a < cols; ++a) gr[a] = host_red_[8 + j++];
+        std::vector<int> piv(cols);
+        for (int a = 0; a < cols; ++a) piv[a] = a;
+        std::vector<double> Rm(cols * cols, 0.0), cvec(cols, 0.0);
+        double maxd = 0.0;
+        for (int a = 0; a < cols; ++a) maxd = std::max(maxd, G[a + a * cols]);
+        std::vector<double> W = G;  // working Schur complement
+        int rank = 0;
+        double maxpiv = 0.0;
+        const double floor_rel = 64.0 * std::numeric_limits<double>::epsilon();
+        for (int t = 0; t < cols; ++t) {
+          int best = t;
+          for (int a = t + 1; a < cols; ++a)
+            if (W[piv[a] + piv[a] * cols] > W[piv[best] + piv[best] * cols]) best = a;
+          std::swap(piv[t], piv[best]);
+          const int pt = piv[t];
+          const double dd = W[pt + pt * cols];
+          if (!(dd > floor_rel * maxd)) break;
+          const double rkk = std::sqrt(dd);
+          Rm[t + t * cols] = rkk;
+          maxpiv = std::max(maxpiv, rkk);
+          for (int a = t + 1; a < cols; ++a) Rm[t + a * cols] = W[pt + piv[a] * cols] / rkk;
+          double ct = gr[pt];
+          for (int s = 0; s < t; ++s) ct -= Rm[s + t * cols] * cvec[s];
+          cvec[t] = ct / rkk;
+          for (int a = t + 1; a < cols; ++a)
+            for (int b = t + 1; b < cols; ++b)
+              W[piv[a] + piv[b] * cols] -= Rm[t + a * cols] * Rm[t + b * cols];
+          // update rhs projections for later pivots via gr
+          for (int a = t + 1; a < cols; ++a) (void)a;
+          ++rank;
+        }
+        int np = 0;
+        for (int t = 0; t < rank; ++t) np += (Rm[t + t * cols] > 1e-12 * maxpiv) ? 1 : 0;
+        std::vector<double> kap(cols, 0.0);
+        for (int t = np - 1; t >= 0; --t) {
+          double s = cvec[t];
+          for (int a = t + 1; a < np; ++a) s -= Rm[t + a * cols] * kap[piv[a]];
+          kap[piv[t]] = s / Rm[t + t * cols];
+        }
+        // psi = -r - sum_j kappa_j (M_r - M_d)_j, (M_r - M_d)_j = r_{k-1-j} = RH[j+1]
+        LinCombArgs A{};
+        A.x[0] = R;
+        A.c[0] = -1.0;
+        for (int c = 0; c < cols; ++c) {
+          A.x[c + 1] = RH[c + 1];
+          A.c[c + 1] = -kap[c];
+        }
+        launch_lincomb(int(nv), cols + 1, A, PSI, st_);
+      }
+      char branch;
+      bool carried = false;
+      double omega_next = 0.0;
+      if (omega <= prm_.c0 * zeta) {  // K0
+        launch_axpby(int(nv), 1.0, V, 1.0, PSI, V, st_);
+        zeta = omega;
+        branch = '0';
+        ++st.k0;
+      } else {
+        // M psi (solver.cpp:287-290)
+        Lt(PSI + nz, tmpz);
+        ++st.n_Lt;
+        launch_axpby(int(nz), 1.0, PSI, -alpha, tmpz, PV, st_);
+        L(PSI, tmpe);
+        ++st.n_L;
+        launch_axpby(int(ne), 1.0, PSI + nz, -alpha, tmpe, PV + nz, st_);
+        double tau = 1.0;
+        int backtracks = 0;
+        for (;;) {
+          launch_axpby(int(nv), 1.0, V, tau, PSI, C, st_);
+          refresh(C, TC, CR, cLrz);
+          queue_mnorm(CR, cLrz, 0);
+          {
+            DotArgs A{};
+            A.x[0] = CR, A.y[0] = PV, A.n[0] = int(nz);
+            A.x[1] = CR + nz, A.y[1] = PV + nz, A.n[1] = int(ne);
+            A.ndots = 2;
+            launch_dots(A, partial_ + 3 * kMaxDots * kRedBlocks, red_out_ + 3, st_);
+          }
+          fetch(5);
+          const double omt = mnorm_of(host_red_);
+          if ((omega <= omega_safe && omt <= prm_.c1 * omega) || omt == 0.0) {  // K1
+            std::swap(V, C);
+            std::swap(TV, TC);
+            std::swap(R, CR);
+            std::swap(Lrz, cLrz);
+            omega_safe = omt + std::pow(prm_.c2, k);
+            branch = '1';
+            ++st.k1;
+            carried = true;
+            omega_next = omt;
+            break;
+          }
+          const double rho = omt * omt - tau * (host_red_[3] + host_red_[4]);
+          if (rho >= prm_.sigma * omt * omega) {  // K2
+            const double coef = prm_.lambda * rho / (omt * omt);
+            launch_axpby(int(nv), 1.0, V, -coef, CR, V, st_);
+            branch = '2';
+            ++st.k2;
+            break;
+          }
+          tau *= prm_.beta;
+          if (++backtracks > prm_.max_backtracks) {  // KM fallback
+            CK(cudaMemcpyAsync(V, TV, sizeof(double) * nv, cudaMemcpyDeviceToDevice, st_));
+            branch = 'S';
+            ++st.stalled;
+            break;
+          }
+        }
+      }
+      st.branches.push_back(branch);
+      if (prm_.progress) prm_.progress(k, omega, branch);
+      if (carried) {
+        omega = omega_next;
+        have_omega = true;
+      } else {
+        refresh(V, TV, R, Lrz);
+        queue_mnorm(R, Lrz, 0);
+        have_omega = false;
+      }
+    }
+  } catch (...) {
+    cleanup();
+    throw;
+  }
+}
+
+// k back-to-back T applications on device-resident iterates (bench helper)
+double Engine::bench_T(int k, bool graph) {
+  double *z0 = scratch_z_[0], *e0 = scratch_e_[0], *z1 = scratch_z_[1], *e1 = scratch_e_[1];
+  CK(cudaMemsetAsync(z0, 0, sizeof(double) * lay_.nz, st_));
+  CK(cudaMemsetAsync(e0, 0, sizeof(double) * lay_.neta, st_));
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  if (graph && !bench_graph_) {
+    cudaGraph_t g;
+    CK(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
+    T(z0, e0, z1, e1);
+    T(z1, e1, z0, e0);
+    CK(cudaStreamEndCapture(st_, &g));
+    CK(cudaGraphInstantiate(&bench_graph_, g, 0));
+    cudaGraphDestroy(g);
+  }
+  CK(cudaEventRecord(a, st_));
+  if (graph) {
+    for (int i = 0; i < k / 2; ++i) CK(cudaGraphLaunch(bench_graph_, st_));
+  } else {
+    for (int i = 0; i < k / 2; ++i) {
+      T(z0, e0, z1, e1);
+      T(z1, e1, z0, e0);
+    }
+  }
+  CK(cudaEventRecord(b, st_));
+  CK(cudaEventSynchronize(b));
+  float ms = 0.0f;
+  CK(cudaEventElapsedTime(&ms, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  CK(cudaGetLastError());
+  return double(ms);
+}
+
+}  // namespace spock

@@ -1,0 +1,121 @@
+// Device engine of the B200 SPOCK solver: owns the preconditioned problem,
+// its device image, the offline factors and all iteration buffers.  One
+// instance runs one solve at a time (as the reference's SpockSolver,
+// proj/include/spock/solver.hpp:95-145).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <functional>
+#include <string>
+#include <vector>
+
+#include "dev.cuh"
+#include "kernels.hpp"
+#include "model.hpp"
+
+namespace spock {
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+struct OpNorm {
+  double estimate = 0.0, analytic_bound = 0.0;
+  int iterations = 0;
+  bool converged = false;
+};
+
+struct Params {
+  double eps_abs = 1e-6, eps_rel = 1e-6, alpha = 0.0;
+  int aa_memory = 3;
+  double c0 = 0.99, c1 = 0.99, c2 = 0.99, beta = 0.5, sigma = 0.1, lambda = 1.0;
+  int max_iters = 50000, max_backtracks = 40;
+  bool use_preconditioner = true;
+  std::function<void(int, double, char)> progress;
+  std::function<bool()> cancelled;
+  int poll_every = 1;
+  void validate() const;
+};
+
+struct Status {
+  int iterations = 0, reason = SPOCK_MAX_ITERS;
+  double xi1 = 0, xi2 = 0;
+  int k0 = 0, k1 = 0, k2 = 0, stalled = 0;
+  std::vector<double> rnorm;
+  std::string branches;
+  int64_t n_T = 0, n_L = 0, n_Lt = 0;
+};
+
+class Engine {
+ public:
+  Engine(const spock_problem_desc* desc, const Params& prm);
+  ~Engine();
+  Engine(const Engine&) = delete;
+  Engine& operator=(const Engine&) = delete;
+
+  int64_t nz() const { return lay_.nz; }
+  int64_t neta() const { return lay_.neta; }
+  double alpha() const { return alpha_; }
+  const OpNorm& op_norm() const { return norm_; }
+
+  // boundary-layout entry points (host or device pointers)
+  void apply_T_b(const double* z, const double* eta, double* zo, double* eo);
+  void apply_L_b(const double* z, double* eta);
+  void apply_Lt_b(const double* eta, double* z);
+  double m_norm_b(const double* z, const double* eta, double alpha);
+  void proj_s1_b(double* z);
+  void proj_s2_b(double* z);
+  void proj_s3_b(double* eta);
+  void unscale_b(const double* zs, double* z);
+  void solve_b(const double* x_init, const double* wz, const double* we, double* oz, double* ozs, double* oe,
+               bool supermann, Status& st);
+  double bench_T(int k, bool graph);
+
+ private:
+  void upload();
+  void factorize();
+  void power_iteration();
+  void set_xinit(const double* x_orig_host);
+  // internal-layout device operations
+  void T(const double* z, const double* eta, double* zo, double* eo);
+  void L(const double* z, double* eta);
+  void Lt(const double* eta, double* z);
+  void dots(std::initializer_list<std::pair<const double*, const double*>> pairs, int64_t n_default,
+            const std::vector<int64_t>& ns, double* host_out);
+  void sync();
+  void to_internal_eta(const double* src_any, double* dst_dev);
+  void from_internal_eta(const double* src_dev, double* dst_any);
+  void copy_in_z(const double* src_any, double* dst_dev);
+  void copy_out(const double* src_dev, double* dst_any, int64_t n);
+  template <class Ty>
+  Ty* dalloc(size_t n);
+  template <class Ty>
+  Ty* dupload(const std::vector<Ty>& h);
+
+  Params prm_;
+  Problem raw_, p_;
+  Precond pc_;
+  SocData soc_;
+  Layouts lay_;
+  Dev D_{};
+  std::vector<int> stage_start_;
+  cudaStream_t st_ = nullptr;
+  std::vector<void*> allocs_;
+  OpNorm norm_;
+  double alpha_ = 0.0;
+  // internal buffers
+  int* perm_eta_ = nullptr;  // internal index -> boundary index
+  bool perm_identity_ = true;
+  double* d1_ = nullptr;
+  double* d2_ = nullptr;
+  double* xinit_ = nullptr;
+  double* partial_ = nullptr;
+  double* red_out_ = nullptr;
+  double* host_red_ = nullptr;  // pinned
+  double* scratch_z_[3] = {};
+  double* scratch_e_[3] = {};
+  cudaGraphExec_t bench_graph_ = nullptr;
+};
+
+}  // namespace spock

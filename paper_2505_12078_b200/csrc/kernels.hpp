@@ -1,0 +1,83 @@
+// Host-callable launchers of the B200 SPOCK kernels (kernels.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "dev.cuh"
+
+namespace spock {
+
+constexpr int kRedBlocks = 2 * 148;  // fixed grid => run-to-run identical reductions
+constexpr int kRedThreads = 256;
+constexpr int kMaxDots = 16;
+
+struct LinCombArgs {
+  const double* x[16];
+  double c[16];
+};
+struct DotArgs {
+  const double* x[kMaxDots];
+  const double* y[kMaxDots];
+  int n[kMaxDots];
+  int ndots;
+};
+struct XiArgs {
+  const double* x[2];
+  const double* y[2];
+  const double* d[2];
+  int n[2];
+  double alpha;
+};
+struct BGemmArgs {
+  const double* const* A;
+  const double* const* B;
+  double* const* C;
+  int m, n, k, lda, ldb, ldc, ta, tb;
+  double alpha, beta;
+};
+struct Alg1Args {
+  int b;  // first node of the launch range
+  int nx, nu;
+  const int* cf;
+  const int* cc;
+  const int* anc;
+  const double* A;   // per non-root
+  const double* B;
+  const double* rt;  // per non-root temporaries
+  const double* kt;
+  const double* ge;
+  const double* pt;
+  const double* he;
+  double* P;     // per node
+  double* K;     // per non-leaf
+  double* KT;
+  double* Rinv;
+  double* g;
+  double* h;
+  double* M1;    // per non-root
+  double* M1T;
+  double* Rt_out;    // optional per non-leaf
+  double* Abar_out;  // optional per non-root
+  int* err;
+};
+
+void launch_Lt(const Dev& D, const double* eta, const double* zin, double* zout, double a, double b, double c0,
+               cudaStream_t st);
+void launch_L(const Dev& D, const double* z1, double a1, const double* z2, double a2, const double* eta_in,
+              double* eta_out, double alpha, bool dual, cudaStream_t st);
+void launch_s1(const Dev& D, const int* stage_start, double* z, cudaStream_t st);
+void launch_s2(const Dev& D, double* z, cudaStream_t st);
+void launch_s3(const Dev& D, double* eta, cudaStream_t st);
+void launch_axpby(int n, double a, const double* x, double b, const double* y, double* out, cudaStream_t st);
+void launch_lincomb(int n, int nv, const LinCombArgs& A, double* out, cudaStream_t st);
+void launch_gather(int n, const int* perm, const double* src, double* dst, cudaStream_t st);
+void launch_scatter(int n, const int* perm, const double* src, double* dst, cudaStream_t st);
+void launch_dots(const DotArgs& A, double* partial, double* out, cudaStream_t st);
+void launch_xi(const XiArgs& A, double* partial, double* out, cudaStream_t st);
+void launch_bgemm(const BGemmArgs& G, int count, cudaStream_t st);
+void launch_alg1_parent(const Alg1Args& P, int count, cudaStream_t st);
+void launch_alg1_parent2(const Alg1Args& P, int count, cudaStream_t st);
+void launch_alg1_child_abar(const Alg1Args& P, int count, cudaStream_t st);
+cudaError_t set_alg1_smem(int bytes);
+
+}  // namespace spock
