@@ -185,9 +185,16 @@ int spock_proj_s3(spock_solver* s, double* eta);
 /* SpockSolver::unscale_primal / scale_primal (proj/src/solver.cpp:116-146) */
 int spock_solver_unscale_primal(spock_solver* s, const double* z_scaled, double* z);
 
-/* Timing helper for benchmarks: k back-to-back CP applications v <- T(v) on
- * device-resident iterates (no host transfers); returns device milliseconds. */
-int spock_bench_T(spock_solver* s, int32_t k, int32_t use_graph, double* ms_out);
+/* Benchmark helpers (not part of the reference API).
+ * spock_bench_T: k back-to-back CP applications v <- T(v) on device-resident
+ * iterates; with flush_l2 a 256 MiB buffer is rewritten between applications
+ * outside the timed events.  Returns total device milliseconds.
+ * spock_bench_kernels: average device ms of [L*, S1 sweeps, S2, L+S3, T].
+ * spock_traffic_model: algorithmic bytes of the same five launch classes and
+ * the number of kernel launches per T. */
+int spock_bench_T(spock_solver* s, int32_t k, int32_t use_graph, int32_t flush_l2, double* ms_out);
+int spock_bench_kernels(spock_solver* s, int32_t k, int32_t flush_l2, double* ms5);
+int spock_traffic_model(spock_solver* s, double* bytes5, int32_t* launches_per_T);
 
 #ifdef __cplusplus
 }

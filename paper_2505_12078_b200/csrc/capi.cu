@@ -192,9 +192,20 @@ int spock_solver_unscale_primal(spock_solver* s, const double* zs, double* z) {
   if (int rc = check(s)) return rc;
   return guard([&] { s->eng->unscale_b(zs, z); });
 }
-int spock_bench_T(spock_solver* s, int32_t k, int32_t use_graph, double* ms_out) {
+int spock_bench_T(spock_solver* s, int32_t k, int32_t use_graph, int32_t flush_l2, double* ms_out) {
   if (int rc = check(s)) return rc;
-  return guard([&] { *ms_out = s->eng->bench_T(k, use_graph != 0); });
+  return guard([&] { *ms_out = s->eng->bench_T(k, use_graph != 0, flush_l2 != 0); });
+}
+int spock_bench_kernels(spock_solver* s, int32_t k, int32_t flush_l2, double* ms5) {
+  if (int rc = check(s)) return rc;
+  return guard([&] { s->eng->bench_kernels(k, flush_l2 != 0, ms5); });
+}
+int spock_traffic_model(spock_solver* s, double* bytes5, int32_t* launches_per_T) {
+  if (int rc = check(s)) return rc;
+  return guard([&] {
+    s->eng->traffic(bytes5);
+    if (launches_per_T) *launches_per_T = s->eng->launches_per_T();
+  });
 }
 
 }  // extern "C"

@@ -832,6 +832,54 @@ void Engine::unscale_b(const double* zs, double* z) {  // solver.cpp:116-130
 }
 
 // ---------------------------------------------------------------------------
+// Anderson least squares min ||M_d kappa - r|| from the Gram matrix G = M_d'M_d
+// and gr = M_d'r: column-pivoted Cholesky of G is the R factor of the
+// column-pivoted QR of M_d (same pivot order: largest remaining column norm),
+// and R' c = P'gr gives c = Q'r.  Pivots at or below 64 eps of the largest
+// Gram diagonal are treated as zero (the Gram form cannot resolve the QR's
+// 1e-12 threshold below sqrt(eps)); the remaining ones use the reference's
+// 1e-12 relative threshold (solver.cpp:73-75).  R is indexed by original column.
+std::vector<double> aa_kappa(const std::vector<double>& G, const std::vector<double>& gr, int cols) {
+  std::vector<int> piv(cols);
+  for (int a = 0; a < cols; ++a) piv[a] = a;
+  std::vector<double> W = G, Rm(size_t(cols) * cols, 0.0), cv(cols, 0.0);
+  auto R = [&](int s, int c) -> double& { return Rm[size_t(s) + size_t(c) * cols]; };
+  double maxd = 0.0;
+  for (int a = 0; a < cols; ++a) maxd = std::max(maxd, G[a + a * cols]);
+  const double floor_rel = 64.0 * std::numeric_limits<double>::epsilon();
+  int rank = 0;
+  double maxpiv = 0.0;
+  for (int t = 0; t < cols; ++t) {
+    int best = t;
+    for (int a = t + 1; a < cols; ++a)
+      if (W[piv[a] + piv[a] * cols] > W[piv[best] + piv[best] * cols]) best = a;
+    std::swap(piv[t], piv[best]);
+    const int pt = piv[t];
+    const double dd = W[pt + pt * cols];
+    if (!(dd > floor_rel * maxd)) break;
+    const double rkk = std::sqrt(dd);
+    R(t, pt) = rkk;
+    maxpiv = std::max(maxpiv, rkk);
+    for (int a = t + 1; a < cols; ++a) R(t, piv[a]) = W[pt + piv[a] * cols] / rkk;
+    double ct = gr[pt];
+    for (int s = 0; s < t; ++s) ct -= R(s, pt) * cv[s];
+    cv[t] = ct / rkk;
+    for (int a = t + 1; a < cols; ++a)
+      for (int b = t + 1; b < cols; ++b) W[piv[a] + piv[b] * cols] -= R(t, piv[a]) * R(t, piv[b]);
+    ++rank;
+  }
+  int np = 0;
+  for (int t = 0; t < rank; ++t) np += (R(t, piv[t]) > 1e-12 * maxpiv) ? 1 : 0;
+  std::vector<double> kap(cols, 0.0);
+  for (int t = np - 1; t >= 0; --t) {
+    double s = cv[t];
+    for (int a = t + 1; a < np; ++a) s -= R(t, piv[a]) * kap[piv[a]];
+    kap[piv[t]] = s / R(t, piv[t]);
+  }
+  return kap;
+}
+
+// ---------------------------------------------------------------------------
 // SuperMann / CP loop (proj/src/solver.cpp:189-350).  State lives on device;
 // one host round trip per iteration (omega, xi norms and the Anderson Gram
 // matrix come back together) plus one per line-search trial.
@@ -949,8 +997,8 @@ void Engine::solve_b(const double* x_init, const double* wz, const double* we, d
       fetch(8 + ngram);
       if (!have_omega) {
         omega = mnorm_of(host_red_);
-        zeta = omega_safe = omega;
         have_omega = true;
+        if (k == 0) zeta = omega_safe = omega;  // solver.cpp:233-235
       }
       const double n1 = host_red_[4], n2 = host_red_[5];
       if (k == 0) {
@@ -1004,45 +1052,7 @@ void Engine::solve_b(const double* x_init, const double* wz, const double* we, d
             ++j;
           }
         for (int a = 0; a < cols; ++a) gr[a] = host_red_[8 + j++];
-        std::vector<int> piv(cols);
-        for (int a = 0; a < cols; ++a) piv[a] = a;
-        std::vector<double> Rm(cols * cols, 0.0), cvec(cols, 0.0);
-        double maxd = 0.0;
-        for (int a = 0; a < cols; ++a) maxd = std::max(maxd, G[a + a * cols]);
-        std::vector<double> W = G;  // working Schur complement
-        int rank = 0;
-        double maxpiv = 0.0;
-        const double floor_rel = 64.0 * std::numeric_limits<double>::epsilon();
-        for (int t = 0; t < cols; ++t) {
-          int best = t;
-          for (int a = t + 1; a < cols; ++a)
-            if (W[piv[a] + piv[a] * cols] > W[piv[best] + piv[best] * cols]) best = a;
-          std::swap(piv[t], piv[best]);
-          const int pt = piv[t];
-          const double dd = W[pt + pt * cols];
-          if (!(dd > floor_rel * maxd)) break;
-          const double rkk = std::sqrt(dd);
-          Rm[t + t * cols] = rkk;
-          maxpiv = std::max(maxpiv, rkk);
-          for (int a = t + 1; a < cols; ++a) Rm[t + a * cols] = W[pt + piv[a] * cols] / rkk;
-          double ct = gr[pt];
-          for (int s = 0; s < t; ++s) ct -= Rm[s + t * cols] * cvec[s];
-          cvec[t] = ct / rkk;
-          for (int a = t + 1; a < cols; ++a)
-            for (int b = t + 1; b < cols; ++b)
-              W[piv[a] + piv[b] * cols] -= Rm[t + a * cols] * Rm[t + b * cols];
-          // update rhs projections for later pivots via gr
-          for (int a = t + 1; a < cols; ++a) (void)a;
-          ++rank;
-        }
-        int np = 0;
-        for (int t = 0; t < rank; ++t) np += (Rm[t + t * cols] > 1e-12 * maxpiv) ? 1 : 0;
-        std::vector<double> kap(cols, 0.0);
-        for (int t = np - 1; t >= 0; --t) {
-          double s = cvec[t];
-          for (int a = t + 1; a < np; ++a) s -= Rm[t + a * cols] * kap[piv[a]];
-          kap[piv[t]] = s / Rm[t + t * cols];
-        }
+        const std::vector<double> kap = aa_kappa(G, gr, cols);
         // psi = -r - sum_j kappa_j (M_r - M_d)_j, (M_r - M_d)_j = r_{k-1-j} = RH[j+1]
         LinCombArgs A{};
         A.x[0] = R;
@@ -1130,40 +1140,133 @@ void Engine::solve_b(const double* x_init, const double* wz, const double* we, d
   }
 }
 
-// k back-to-back T applications on device-resident iterates (bench helper)
-double Engine::bench_T(int k, bool graph) {
-  double *z0 = scratch_z_[0], *e0 = scratch_e_[0], *z1 = scratch_z_[1], *e1 = scratch_e_[1];
-  CK(cudaMemsetAsync(z0, 0, sizeof(double) * lay_.nz, st_));
-  CK(cudaMemsetAsync(e0, 0, sizeof(double) * lay_.neta, st_));
-  cudaEvent_t a, b;
-  CK(cudaEventCreate(&a));
-  CK(cudaEventCreate(&b));
+// k back-to-back T applications on device-resident iterates (bench helper).
+// With flush, a 256 MiB buffer is rewritten between applications (outside the
+// per-application event pair) so no application reads the previous one's
+// L2-resident data; the result is the sum of per-application device times.
+void Engine::flush_l2() {
+  const size_t n = size_t(256) << 20;
+  if (!flush_buf_) flush_buf_ = dalloc<double>(n / sizeof(double));
+  CK(cudaMemsetAsync(flush_buf_, int(0x5a), n, st_));
+}
+
+double Engine::bench_T(int k, bool graph, bool flush) {
+  double *z[2] = {scratch_z_[0], scratch_z_[1]}, *e[2] = {scratch_e_[0], scratch_e_[1]};
+  CK(cudaMemsetAsync(z[0], 0, sizeof(double) * lay_.nz, st_));
+  CK(cudaMemsetAsync(e[0], 0, sizeof(double) * lay_.neta, st_));
   if (graph && !bench_graph_) {
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
-    T(z0, e0, z1, e1);
-    T(z1, e1, z0, e0);
+    T(z[0], e[0], z[1], e[1]);
+    T(z[1], e[1], z[0], e[0]);
     CK(cudaStreamEndCapture(st_, &g));
     CK(cudaGraphInstantiate(&bench_graph_, g, 0));
     cudaGraphDestroy(g);
   }
-  CK(cudaEventRecord(a, st_));
-  if (graph) {
-    for (int i = 0; i < k / 2; ++i) CK(cudaGraphLaunch(bench_graph_, st_));
+  std::vector<cudaEvent_t> ev(2 * ((k + 1) / 2) + 2);
+  for (auto& x : ev) CK(cudaEventCreate(&x));
+  const int pairs = (k + 1) / 2;
+  double total = 0.0;
+  if (flush) {
+    for (int i = 0; i < pairs; ++i) {
+      for (int h = 0; h < 2; ++h) {
+        flush_l2();
+        CK(cudaEventRecord(ev[2 * i + h], st_));
+        T(z[h], e[h], z[1 - h], e[1 - h]);
+        CK(cudaEventRecord(ev[ev.size() - 1], st_));
+        CK(cudaEventSynchronize(ev[ev.size() - 1]));
+        float ms = 0.0f;
+        CK(cudaEventElapsedTime(&ms, ev[2 * i + h], ev[ev.size() - 1]));
+        total += ms;
+      }
+    }
   } else {
-    for (int i = 0; i < k / 2; ++i) {
-      T(z0, e0, z1, e1);
-      T(z1, e1, z0, e0);
+    CK(cudaEventRecord(ev[0], st_));
+    for (int i = 0; i < pairs; ++i) {
+      if (graph) {
+        CK(cudaGraphLaunch(bench_graph_, st_));
+      } else {
+        T(z[0], e[0], z[1], e[1]);
+        T(z[1], e[1], z[0], e[0]);
+      }
+    }
+    CK(cudaEventRecord(ev[1], st_));
+    CK(cudaEventSynchronize(ev[1]));
+    float ms = 0.0f;
+    CK(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+    total = ms;
+  }
+  for (auto& x : ev) cudaEventDestroy(x);
+  CK(cudaGetLastError());
+  return total * double(k) / double(2 * pairs);
+}
+
+// average device ms per launch class over k repetitions:
+// ms[0] L* (child+node), ms[1] S1 (all stages), ms[2] S2, ms[3] L+S3 dual, ms[4] whole T
+void Engine::bench_kernels(int k, bool flush, double* ms) {
+  double *z0 = scratch_z_[0], *e0 = scratch_e_[0], *z1 = scratch_z_[1], *e1 = scratch_e_[1];
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  for (int c = 0; c < 5; ++c) ms[c] = 0.0;
+  for (int i = 0; i < k; ++i) {
+    for (int c = 0; c < 5; ++c) {
+      if (flush) flush_l2();
+      CK(cudaEventRecord(a, st_));
+      switch (c) {
+        case 0: launch_Lt(D_, e0, z0, z1, 1.0, -alpha_, -alpha_, st_); break;
+        case 1: launch_s1(D_, stage_start_.data(), z1, st_); break;
+        case 2: launch_s2(D_, z1, st_); break;
+        case 3: launch_L(D_, z1, 2.0, z0, -1.0, e0, e1, alpha_, true, st_); break;
+        case 4: T(z0, e0, z1, e1); break;
+      }
+      CK(cudaEventRecord(b, st_));
+      CK(cudaEventSynchronize(b));
+      float t = 0.0f;
+      CK(cudaEventElapsedTime(&t, a, b));
+      ms[c] += t;
     }
   }
-  CK(cudaEventRecord(b, st_));
-  CK(cudaEventSynchronize(b));
-  float ms = 0.0f;
-  CK(cudaEventElapsedTime(&ms, a, b));
+  for (int c = 0; c < 5; ++c) ms[c] /= std::max(k, 1);
   cudaEventDestroy(a);
   cudaEventDestroy(b);
   CK(cudaGetLastError());
-  return double(ms);
+}
+
+// Algorithmic bytes per launch class (each operand read or written once per
+// launch): [L*, S1, S2, L+S3, T]
+void Engine::traffic(double* out) const {
+  const Tree& tr = p_.tree;
+  const int nn = tr.nn(), nnl = tr.nnl(), nx = p_.nx, nu = p_.nu, m = nx + nu;
+  double lt = 0, s1 = 0, s2 = 0, ld = 0;
+  for (int k = 0; k < nn - 1; ++k) {
+    const int px = soc_.stage[k].px, pu = soc_.stage[k].pu, p = px + pu;
+    lt += double(px) * nx + double(pu) * nu + m + (p + 2) + m + 2;        // H', qk, eta seg, adj, tau in/out
+    ld += double(px) * nx + double(pu) * nu + m + 2.0 * (p + 2) + (p + 2)  // H, qk, a, eta in, eta out
+          + 2.0 * m + 2;                                                    // (x,u)_anc of z+ and z, tau
+    s1 += double(m) * nx + (nx + m)   // backward: M1', q in (xbar), T12 out
+          + double(nx) * m + m + 2 * nx;  // forward: M1, (x,d)_anc, c, x out
+  }
+  for (int i = 0; i < nnl; ++i) {
+    const int ny = lay_.y_dim[i], nc = p_.nc[i], nch = tr.child_count[i];
+    const double g = D_.g_diag ? m : double(nc) * m;
+    lt += 2.0 * ny + 1 + nc + g + double(nch) * m + 2.0 * (m + ny + 1);  // eta, b, G, adj sums, z in/out
+    ld += 2.0 * ny + ny + 1 + (ny + 1 + nc) * 2.0 + g + 2.0 * m + 2.0 * nc + 2;  // y of z+,z, b, eta in/out, G, xu, box
+    s1 += double(nx) * nu + nx + nu + double(nu) * nu + double(nch) * m + nu  // KT, h, g, Rinv, T12 of children, d
+          + double(nu) * nx + nu + nu + nu;                                    // forward K, d, u out
+    s2 += 2.0 * (ny + 2 * nch) + (D_.s2_kind ? 0.0 : 0.0);
+  }
+  for (int j = 0; j < nn - nnl; ++j) {
+    const int pN = soc_.leaf[j].px, nc = p_.ncN[j];
+    const double g = D_.gN_diag ? nx : double(nc) * nx;
+    lt += nc + g + double(pN) * nx + (pN + 2) + nx + 2.0 * (nx + 1);
+    ld += g + double(pN) * nx + nx + 2.0 * (pN + 2) + (pN + 2) + 2.0 * (nc) + nc * 2.0 + 2.0 * (nx + 1);
+  }
+  out[0] = 8.0 * lt;
+  out[1] = 8.0 * s1;
+  out[2] = 8.0 * s2;
+  out[3] = 8.0 * ld;
+  out[4] = out[0] + out[1] + out[2] + out[3];
 }
 
 }  // namespace spock

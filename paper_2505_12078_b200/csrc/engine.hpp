@@ -70,7 +70,10 @@ class Engine {
   void unscale_b(const double* zs, double* z);
   void solve_b(const double* x_init, const double* wz, const double* we, double* oz, double* ozs, double* oe,
                bool supermann, Status& st);
-  double bench_T(int k, bool graph);
+  double bench_T(int k, bool graph, bool flush);
+  void bench_kernels(int k, bool flush, double* ms);
+  void traffic(double* bytes) const;
+  int launches_per_T() const { return 2 + 2 * (p_.tree.horizon + 1) + 1 + 1; }
 
  private:
   void upload();
@@ -116,6 +119,8 @@ class Engine {
   double* scratch_z_[3] = {};
   double* scratch_e_[3] = {};
   cudaGraphExec_t bench_graph_ = nullptr;
+  double* flush_buf_ = nullptr;
+  void flush_l2();
 };
 
 }  // namespace spock

@@ -176,7 +176,21 @@ class SpockSolver:
         _raise(self.lib, self.lib.spock_solver_unscale_primal(self.h, _ptr(np.ascontiguousarray(zs)), _ptr(out)))
         return out
 
-    def bench_T(self, k: int, use_graph: bool = True) -> float:
+    def bench_T(self, k: int, use_graph: bool = True, flush_l2: bool = False) -> float:
+        """Device ms for k back-to-back CP applications (benchmark helper)."""
         ms = C.c_double()
-        _raise(self.lib, self.lib.spock_bench_T(self.h, int(k), int(use_graph), C.byref(ms)))
+        _raise(self.lib, self.lib.spock_bench_T(self.h, int(k), int(use_graph), int(flush_l2), C.byref(ms)))
         return ms.value
+
+    def bench_kernels(self, k: int, flush_l2: bool = True) -> np.ndarray:
+        """Average device ms of [L*, S1 sweeps, S2, L+S3, T]."""
+        out = np.zeros(5)
+        _raise(self.lib, self.lib.spock_bench_kernels(self.h, int(k), int(flush_l2), out.ctypes.data))
+        return out
+
+    def traffic_model(self):
+        """Algorithmic bytes of [L*, S1, S2, L+S3, T] and kernel launches per T."""
+        out = np.zeros(5)
+        n = C.c_int32()
+        _raise(self.lib, self.lib.spock_traffic_model(self.h, out.ctypes.data, C.byref(n)))
+        return out, n.value
