@@ -94,6 +94,9 @@ struct Dev {
   const int64_t* s2p_off;
   const double* s2P;  // dense projectors (dim x dim)
   // offline factors (Alg. 1) restructured for one-pass sweeps (see kernels.cu)
+  // per-node strides of the factor blocks (even numbers of doubles: 16 B
+  // aligned blocks for TMA bulk copies)
+  int64_t m1_stride, k_stride, r_stride;
   const double* M1;   // [Abar B] nx x (nx+nu) per non-root (forward)
   const double* M1T;  // (nx+nu) x nx per non-root (backward)
   const double* cvec; // nx per non-root

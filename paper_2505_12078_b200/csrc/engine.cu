@@ -8,6 +8,8 @@
 //   Engine::solve_b      <- SpockSolver::run           proj/src/solver.cpp:189-350
 #include "engine.hpp"
 
+#include <cstdlib>
+
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -23,6 +25,7 @@ namespace spock {
   } while (0)
 
 namespace {
+inline int64_t pad2(int64_t n) { return (n + 1) & ~int64_t(1); }
 void require(bool c, const char* m) {
   if (!c) throw std::invalid_argument(m);
 }
@@ -80,9 +83,74 @@ Engine::Engine(const spock_problem_desc* desc, const Params& prm) : prm_(prm) {
   upload();
   factorize();
   norm_.analytic_bound = analytic_norm_bound(p_, soc_);
+  setup_fused();
   power_iteration();
   alpha_ = prm_.alpha > 0.0 ? prm_.alpha : 0.99 / std::max(norm_.estimate, 1e-300);
   CK(cudaStreamSynchronize(st_));
+}
+
+// Persistent dataflow T (fused.cu): flags, ticket, shared-memory staging size
+// and grid.  Falls back to the per-stage kernels only for shapes the fused
+// kernel does not cover (constraint rows above 256) or on request
+// (SPOCK_T_UNFUSED=1, used by the tests that compare both paths).
+void Engine::setup_fused() {
+  const Tree& tr = p_.tree;
+  const int nn = tr.nn(), nnl = tr.nnl(), nx = p_.nx, nu = p_.nu, m = nx + nu;
+  fused_ok_ = true;
+  for (int i = 0; i < nnl; ++i)
+    if (p_.nc[i] > kMaxD) fused_ok_ = false;
+  for (int j = 0; j < tr.nl(); ++j)
+    if (p_.ncN[j] > kMaxD) fused_ok_ = false;
+  const char* env = std::getenv("SPOCK_T_UNFUSED");
+  if (env && env[0] == '1') fused_ok_ = false;
+  if (!fused_ok_) return;
+  // largest per-item set of staged blocks (even doubles each)
+  int64_t mx = 0;
+  for (int i = 0; i < nn; ++i) {
+    const bool leaf = tr.leaf(i), root = i == 0;
+    int64_t b = 0, f = 0;
+    if (!root) {
+      const int px = soc_.stage[i - 1].px, pu = soc_.stage[i - 1].pu;
+      b += pad2(int64_t(px) * nx) + pad2(int64_t(pu) * nu) + pad2(int64_t(m) * nx);
+      f += pad2(int64_t(nx) * m) + pad2(int64_t(px) * nx) + pad2(int64_t(pu) * nu);
+    }
+    if (!leaf) {
+      b += pad2(int64_t(nx) * nu) + pad2(int64_t(nu) * nu);
+      f += pad2(int64_t(nu) * nx);
+    } else {
+      const int pN = soc_.leaf[i - tr.nnl()].px;
+      b += pad2(int64_t(pN) * nx);
+      f += pad2(int64_t(pN) * nx);
+    }
+    mx = std::max(mx, std::max(b, f));
+  }
+  FusedArgs& F = fargs_;
+  F = FusedArgs{};
+  F.stage_smem = 1;
+  F.mat_doubles = int(mx);
+  int dev = 0, sms = 148, smem_optin = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  CK(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  if (fused_smem_bytes(F) + 4096 > smem_optin) {  // blocks too large to stage: stream from L2/HBM
+    F.stage_smem = 0;
+    F.mat_doubles = 0;
+  }
+  const int bytes = fused_smem_bytes(F);
+  CK(fused_configure(bytes));
+  int occ = 0;
+  F.D = D_;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fused_kernel_ptr(), 256, bytes));
+  fused_grid_ = std::max(1, std::min(occ, 4)) * sms;
+  const int total = nnl + 2 * nn;
+  fused_grid_ = std::min(fused_grid_, total);
+  const size_t fb = 8 + sizeof(int) * size_t(nnl + 2 * nn);
+  fused_sync_bytes_ = fb;
+  char* buf = dalloc<char>(fb);
+  F.ticket = reinterpret_cast<unsigned long long*>(buf);
+  F.flagS2 = reinterpret_cast<int*>(buf + 8);
+  F.flagB = F.flagS2 + nnl;
+  F.flagF = F.flagB + nn;
 }
 
 Engine::~Engine() {
@@ -127,8 +195,8 @@ void Engine::upload() {
       hxo[k] = sx;
       huo[k] = su;
       ao[k] = sa;
-      sx += int64_t(px[k]) * nx;
-      su += int64_t(pu[k]) * nu;
+      sx += pad2(int64_t(px[k]) * nx);
+      su += pad2(int64_t(pu[k]) * nu);
       sa += px[k] + pu[k] + 2;
     }
     std::vector<double> Hx(sx), HxT(sx), Hu(su), HuT(su), qk(size_t(nr) * (nx + nu)), a(sa);
@@ -170,7 +238,7 @@ void Engine::upload() {
       pN[j] = soc_.leaf[j].px;
       ho[j] = sh;
       ao[j] = sa;
-      sh += int64_t(pN[j]) * nx;
+      sh += pad2(int64_t(pN[j]) * nx);
       sa += pN[j] + 2;
     }
     std::vector<double> HN(sh), HNT(sh), qk(size_t(nl) * nx), a(sa);
@@ -433,12 +501,15 @@ void Engine::upload() {
     D.s2P = dupload(s2P);
   }
   // factor buffers (filled by factorize) and scratch
-  D.M1 = dalloc<double>(size_t(nr) * nx * (nx + nu));
-  D.M1T = dalloc<double>(size_t(nr) * nx * (nx + nu));
+  D.m1_stride = pad2(int64_t(nx) * (nx + nu));
+  D.k_stride = pad2(int64_t(nx) * nu);
+  D.r_stride = pad2(int64_t(nu) * nu);
+  D.M1 = dalloc<double>(size_t(nr) * D.m1_stride);
+  D.M1T = dalloc<double>(size_t(nr) * D.m1_stride);
   D.cvec = dupload(p_.c);
-  D.K = dalloc<double>(size_t(nnl) * nu * nx);
-  D.KT = dalloc<double>(size_t(nnl) * nu * nx);
-  D.Rinv = dalloc<double>(size_t(nnl) * nu * nu);
+  D.K = dalloc<double>(size_t(nnl) * D.k_stride);
+  D.KT = dalloc<double>(size_t(nnl) * D.k_stride);
+  D.Rinv = dalloc<double>(size_t(nnl) * D.r_stride);
   D.g = dalloc<double>(size_t(nnl) * nu);
   D.h = dalloc<double>(size_t(nnl) * nx);
   xinit_ = dalloc<double>(nx);
@@ -546,6 +617,9 @@ void Engine::factorize() {
   Alg1Args A1{};
   A1.nx = nx;
   A1.nu = nu;
+  A1.m1_stride = D_.m1_stride;
+  A1.k_stride = D_.k_stride;
+  A1.r_stride = D_.r_stride;
   A1.cf = D_.cf;
   A1.cc = D_.cc;
   A1.anc = D_.anc;
@@ -614,12 +688,12 @@ void Engine::factorize() {
     // tt = P_c Abar ; pt = Abar' tt ; he = Abar' e
     for (int c = cb; c < ce; ++c) {
       hA[c - cb] = P + size_t(c) * nx * nx;
-      hBp[c - cb] = D_.M1 + size_t(c - 1) * nx * (nx + nu);
+      hBp[c - cb] = D_.M1 + size_t(c - 1) * D_.m1_stride;
       hC[c - cb] = tt + size_t(c - 1) * nx * nx;
     }
     gemm(cnt, nx, nx, nx, nx, nx, nx, 0, 0, 1.0, 0.0);
     for (int c = cb; c < ce; ++c) {
-      hA[c - cb] = D_.M1 + size_t(c - 1) * nx * (nx + nu);
+      hA[c - cb] = D_.M1 + size_t(c - 1) * D_.m1_stride;
       hBp[c - cb] = tt + size_t(c - 1) * nx * nx;
       hC[c - cb] = pt + size_t(c - 1) * nx * nx;
     }
@@ -654,6 +728,18 @@ void Engine::Lt(const double* eta, double* z) { launch_Lt(D_, eta, nullptr, z, 0
 // one CP application (solver.cpp:148-164), internal layout; zo/eo must not
 // alias z/eta
 void Engine::T(const double* z, const double* eta, double* zo, double* eo) {
+  if (fused_ok_) {
+    FusedArgs F = fargs_;
+    F.D = D_;
+    F.z = z;
+    F.eta = eta;
+    F.zo = zo;
+    F.eo = eo;
+    F.alpha = alpha_;
+    CK(cudaMemsetAsync(F.ticket, 0, fused_sync_bytes_, st_));
+    launch_T_fused(F, fused_grid_, st_);
+    return;
+  }
   launch_Lt(D_, eta, z, zo, 1.0, -alpha_, -alpha_, st_);
   launch_s1(D_, stage_start_.data(), zo, st_);
   launch_s2(D_, zo, st_);

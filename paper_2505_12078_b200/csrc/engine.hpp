@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "dev.cuh"
+#include "fused.hpp"
 #include "kernels.hpp"
 #include "model.hpp"
 
@@ -73,10 +74,11 @@ class Engine {
   double bench_T(int k, bool graph, bool flush);
   void bench_kernels(int k, bool flush, double* ms);
   void traffic(double* bytes) const;
-  int launches_per_T() const { return 2 + 2 * (p_.tree.horizon + 1) + 1 + 1; }
+  int launches_per_T() const { return fused_ok_ ? 1 : 2 + 2 * (p_.tree.horizon + 1) + 1 + 1; }
 
  private:
   void upload();
+  void setup_fused();
   void factorize();
   void power_iteration();
   void set_xinit(const double* x_orig_host);
@@ -119,6 +121,10 @@ class Engine {
   double* scratch_z_[3] = {};
   double* scratch_e_[3] = {};
   cudaGraphExec_t bench_graph_ = nullptr;
+  bool fused_ok_ = false;
+  FusedArgs fargs_{};
+  int fused_grid_ = 0;
+  size_t fused_sync_bytes_ = 0;
   double* flush_buf_ = nullptr;
   void flush_l2();
 };

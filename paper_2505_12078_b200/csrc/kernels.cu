@@ -563,7 +563,7 @@ __global__ void __launch_bounds__(32 * kWarps) k_s1_back(Dev D, int b, int e, co
     __syncwarp();
     double t[kMaxR];
     zero_acc(t);
-    warp_gemv(D.KT + size_t(i) * nx * nu, nx, nu, nx, xs, t);  // K' ubar
+    warp_gemv(D.KT + size_t(i) * D.k_stride, nx, nu, nx, xs, t);  // K' ubar
     const double* h = D.h + size_t(i) * nx;
 #pragma unroll
     for (int k = 0; k < kMaxR; ++k) {
@@ -596,7 +596,7 @@ __global__ void __launch_bounds__(32 * kWarps) k_s1_back(Dev D, int b, int e, co
     }
     __syncwarp();
     zero_acc(t);
-    warp_gemv(D.Rinv + size_t(i) * nu * nu, nu, nu, nu, xs, t);
+    warp_gemv(D.Rinv + size_t(i) * D.r_stride, nu, nu, nu, xs, t);
     double* dv = D.dvec + size_t(i) * nu;
 #pragma unroll
     for (int k = 0; k < kMaxR; ++k) {
@@ -614,7 +614,7 @@ __global__ void __launch_bounds__(32 * kWarps) k_s1_back(Dev D, int b, int e, co
     __syncwarp();
     double t[kMaxR];
     zero_acc(t);
-    warp_gemv(D.M1T + size_t(i - 1) * (nx + nu) * nx, nx + nu, nx, nx + nu, xs, t);
+    warp_gemv(D.M1T + size_t(i - 1) * D.m1_stride, nx + nu, nx, nx + nu, xs, t);
     double* T = D.T12 + size_t(i - 1) * (nx + nu);
 #pragma unroll
     for (int k = 0; k < kMaxR; ++k) {
@@ -652,7 +652,7 @@ __global__ void __launch_bounds__(32 * kWarps) k_s1_fwd(Dev D, int b, int e, dou
       x[k] = 0.0;
       (void)r;
     }
-    warp_gemv(D.M1 + size_t(i - 1) * nx * (nx + nu), nx, nx + nu, nx, xs, x);
+    warp_gemv(D.M1 + size_t(i - 1) * D.m1_stride, nx, nx + nu, nx, xs, x);
 #pragma unroll
     for (int k = 0; k < kMaxR; ++k) {
       const int r = l + 32 * k;
@@ -674,7 +674,7 @@ __global__ void __launch_bounds__(32 * kWarps) k_s1_fwd(Dev D, int b, int e, dou
     __syncwarp();
     double u[kMaxR];
     zero_acc(u);
-    warp_gemv(D.K + size_t(i) * nu * nx, nu, nx, nu, xs, u);
+    warp_gemv(D.K + size_t(i) * D.k_stride, nu, nx, nu, xs, u);
     const double* dv = D.dvec + size_t(i) * nu;
 #pragma unroll
     for (int k = 0; k < kMaxR; ++k) {
@@ -961,14 +961,14 @@ __global__ void k_alg1_parent(Alg1Args P) {
     }
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < nu * nu; e += blockDim.x) P.Rinv[size_t(i) * nu * nu + e] = Ri[e];
+  for (int e = threadIdx.x; e < nu * nu; e += blockDim.x) P.Rinv[size_t(i) * P.r_stride + e] = Ri[e];
   // K = -Rinv kt (nu x nx), stored as K (nu x nx) and K' (nx x nu)
   for (int e = threadIdx.x; e < nu * nx; e += blockDim.x) {
     const int r = e % nu, c = e / nu;
     double s = 0.0;
     for (int t = 0; t < nu; ++t) s += Ri[r + t * nu] * kt[t + c * nu];
-    P.K[size_t(i) * nu * nx + e] = -s;
-    P.KT[size_t(i) * nx * nu + c + size_t(r) * nx] = -s;
+    P.K[size_t(i) * P.k_stride + e] = -s;
+    P.KT[size_t(i) * P.k_stride + c + size_t(r) * nx] = -s;
   }
 }
 
@@ -977,7 +977,7 @@ __global__ void k_alg1_parent2(Alg1Args P) {
   const int i = P.b + blockIdx.x;
   const int nu = P.nu, nx = P.nx;
   const int c0 = P.cf[i], nch = P.cc[i];
-  const double* K = P.K + size_t(i) * nu * nx;
+  const double* K = P.K + size_t(i) * P.k_stride;
   for (int e = threadIdx.x; e < nx * nx; e += blockDim.x) {
     const int r = e % nx, c = e / nx;
     double s = (r == c) ? 1.0 : 0.0;
@@ -1000,9 +1000,9 @@ __global__ void k_alg1_child_abar(Alg1Args P) {
   const int k = c - 1, nx = P.nx, nu = P.nu, an = P.anc[c];
   const double* A = P.A + size_t(k) * nx * nx;
   const double* B = P.B + size_t(k) * nx * nu;
-  const double* K = P.K + size_t(an) * nu * nx;
-  double* M1 = P.M1 + size_t(k) * nx * (nx + nu);
-  double* M1T = P.M1T + size_t(k) * (nx + nu) * nx;
+  const double* K = P.K + size_t(an) * P.k_stride;
+  double* M1 = P.M1 + size_t(k) * P.m1_stride;
+  double* M1T = P.M1T + size_t(k) * P.m1_stride;
   for (int e = threadIdx.x; e < nx * nx; e += blockDim.x) {
     const int r = e % nx, col = e / nx;
     double s = A[e];

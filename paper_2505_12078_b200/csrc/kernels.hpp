@@ -38,6 +38,7 @@ struct BGemmArgs {
 struct Alg1Args {
   int b;  // first node of the launch range
   int nx, nu;
+  int64_t m1_stride, k_stride, r_stride;
   const int* cf;
   const int* cc;
   const int* anc;
