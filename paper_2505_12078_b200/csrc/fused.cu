@@ -238,23 +238,51 @@ __device__ void item_s2(const FusedArgs& F, int i, double* red, double* vec) {
   __syncthreads();
 }
 
-// staging helper: copy `doubles` from global to the next free slot of the
-// matrix area (16 B aligned, sizes are even numbers of doubles by layout)
-struct Stager {
-  double* base;
-  int off = 0;
-  uint32_t bytes = 0;
-  bool on;
-  __device__ const double* take(const double* g, int doubles, uint64_t* bar) {
-    if (!on || doubles <= 0) return g;
-    double* d = base + off;
-    const int padded = (doubles + 1) & ~1;
-    off += padded;
-    bytes += uint32_t(padded) * 8u;
-    bulk_g2s(d, g, uint32_t(padded) * 8u, bar);
-    return d;
+// release a completion flag: CTA barrier, then one fenced release store
+// (the semaphore pattern of CUTLASS's GenericBarrier)
+__device__ __forceinline__ void cta_release(int* flag) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    st_release(flag, 1);
   }
-};
+}
+
+// issue the bulk copies of one item's blocks (thread 0); returns staged (or
+// global) pointers through `out`
+__device__ void stage_blocks(const FusedArgs& F, Smem& S, const double* const* src, const int* doubles, int n,
+                             const double** out) {
+  if (threadIdx.x != 0) return;
+  if (!F.stage_smem) {
+    for (int k = 0; k < n; ++k) out[k] = src[k];
+    return;
+  }
+  fence_proxy_async();
+  uint32_t total = 0;
+  for (int k = 0; k < n; ++k) total += uint32_t((doubles[k] + 1) & ~1) * 8u;
+  if (total)
+    mbar_expect_tx(&S.bar, total);
+  else
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&S.bar)) : "memory");
+  int off = 0;
+  for (int k = 0; k < n; ++k) {
+    if (doubles[k] <= 0) {
+      out[k] = src[k];
+      continue;
+    }
+    const int padded = (doubles[k] + 1) & ~1;
+    bulk_g2s(S.mat + off, src[k], uint32_t(padded) * 8u, &S.bar);
+    out[k] = S.mat + off;
+    off += padded;
+  }
+}
+
+__device__ __forceinline__ void wait_blocks(const FusedArgs& F, Smem& S, uint32_t& phase) {
+  if (!F.stage_smem) return;
+  while (!mbar_try_wait(&S.bar, phase)) {
+  }
+  phase ^= 1u;
+}
 
 __device__ void item_back(const FusedArgs& F, int i, Smem& S, uint32_t& phase) {
   const Dev& D = F.D;
@@ -263,54 +291,45 @@ __device__ void item_back(const FusedArgs& F, int i, Smem& S, uint32_t& phase) {
   const double al = F.alpha;
   const double* z = F.z;
   const double* eta = F.eta;
-  // ---- prefetch this node's blocks (one thread issues the bulk copies)
-  const double *HxT = nullptr, *HuT = nullptr, *M1T = nullptr, *KT = nullptr, *Ri = nullptr, *HNT = nullptr;
   int px = 0, pu = 0, pN = 0;
   if (!root) px = D.px[i - 1], pu = D.pu[i - 1];
   if (leaf) pN = D.pN[i - D.nnl];
+  // ---- 1. prefetch this node's blocks: H_x', H_u' (own stage SOC), M1' (own
+  // sweep block), K', Rt^-1 (non-leaf) or H_N' (leaf)
   __shared__ const double* sp[6];
-  if (t == 0) {
-    Stager st{S.mat, 0, 0, F.stage_smem != 0};
-    fence_proxy_async();
-    // expect_tx must precede completion; account the total first
-    uint32_t total = 0;
-    auto pad = [](int d) { return uint32_t(((d + 1) & ~1) * 8); };
-    if (st.on) {
-      if (!root) total += pad(px * nx) + pad(pu * nu) + pad(m * nx);
-      if (!leaf) total += pad(nx * nu) + pad(nu * nu);
-      if (leaf) total += pad(pN * nx);
-      if (total) mbar_expect_tx(&S.bar, total);
-    }
-    const double *a = nullptr, *b = nullptr, *c = nullptr, *d = nullptr, *e = nullptr, *f = nullptr;
+  {
+    const double* src[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    int dbl[6] = {0, 0, 0, 0, 0, 0};
     if (!root) {
-      a = st.take(D.HxT + D.hx_off[i - 1], px * nx, &S.bar);
-      b = st.take(D.HuT + D.hu_off[i - 1], pu * nu, &S.bar);
-      c = st.take(D.M1T + size_t(i - 1) * D.m1_stride, m * nx, &S.bar);
+      src[0] = D.HxT + D.hx_off[i - 1], dbl[0] = px * nx;
+      src[1] = D.HuT + D.hu_off[i - 1], dbl[1] = pu * nu;
+      src[2] = D.M1T + size_t(i - 1) * D.m1_stride, dbl[2] = m * nx;
     }
     if (!leaf) {
-      d = st.take(D.KT + size_t(i) * D.k_stride, nx * nu, &S.bar);
-      e = st.take(D.Rinv + size_t(i) * D.r_stride, nu * nu, &S.bar);
+      src[3] = D.KT + size_t(i) * D.k_stride, dbl[3] = nx * nu;
+      src[4] = D.Rinv + size_t(i) * D.r_stride, dbl[4] = nu * nu;
     } else {
-      f = st.take(D.HNT + D.hn_off[i - D.nnl], pN * nx, &S.bar);
+      src[5] = D.HNT + D.hn_off[i - D.nnl], dbl[5] = pN * nx;
     }
-    sp[0] = a, sp[1] = b, sp[2] = c, sp[3] = d, sp[4] = e, sp[5] = f;
-    if (!(st.on && total)) {
-      // nothing in flight: complete the phase locally so the wait below passes
-      if (st.on) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&S.bar)) : "memory");
-    }
+    stage_blocks(F, S, src, dbl, 6, sp);
   }
-  __syncthreads();
-  HxT = sp[0], HuT = sp[1], M1T = sp[2], KT = sp[3], Ri = sp[4], HNT = sp[5];
   double* V = S.vec;
-  double* head = V;            // p (<= kMaxD)
-  double* gx = head + kSlot;   // nx + nu : G' ec, then L* (x,u)
-  double* xb = gx + kSlot;     // nx + nu : (xbar, ubar)
-  double* q = xb + kSlot;      // nx
-  double* tv = q + kSlot;      // nx + nu scratch
-  double* rhs = tv + kSlot;    // nu
+  double* head = V;          // own stage-SOC head (p), later the leaf head (pN)
+  double* gx = head + kSlot; // G' ec (+ leaf terms): L* (x, u) without the children
+  double* xb = gx + kSlot;   // z (x, u) of this node
+  double* q = xb + kSlot;    // q (nx)
+  double* tv = q + kSlot;    // scratch (m)
+  double* rhs = tv + kSlot;  // scratch (m)
   double* red = S.red;
-  // ---- work independent of the children (overlaps the bulk copies)
-  // own G' ec (non-leaf) or leaf constraint term
+  // ---- 2. everything that does not depend on the children
+  double rsum = 0.0, rsumN = 0.0;
+  if (!root) {
+    const int o2 = D.s2_off[i - 1], p = px + pu;
+    for (int r = t; r < p; r += kFT) head[r] = eta[o2 + r];
+    rsum = eta[o2 + p] + eta[o2 + p + 1];
+  }
+  for (int r = t; r < (leaf ? nx : m); r += kFT)
+    xb[r] = r < nx ? z[1 + size_t(i) * nx + r] : z[D.u_base + size_t(i) * nu + (r - nx)];
   if (!leaf) {
     const int ny = D.y_dim[i], nc = D.s1_nc[i];
     const double* ec = eta + D.s1_off[i] + ny + 1;
@@ -318,10 +337,10 @@ __device__ void item_back(const FusedArgs& F, int i, Smem& S, uint32_t& phase) {
       const double* gd = D.gd + size_t(i) * m;
       for (int r = t; r < m; r += kFT) gx[r] = gd[r] * ec[r];
     } else {
-      for (int r = t; r < nc; r += kFT) tv[r] = ec[r];
+      for (int r = t; r < nc; r += kFT) rhs[r] = ec[r];
       __syncthreads();
-      cta_gemv(D.GxT + D.g_off[i] * nx, nx, nc, nx, tv, gx, false, red);
-      cta_gemv(D.GuT + D.g_off[i] * nu, nu, nc, nu, tv, gx + nx, false, red);
+      cta_gemv(D.GxT + D.g_off[i] * nx, nx, nc, nx, rhs, gx, false, red);
+      cta_gemv(D.GuT + D.g_off[i] * nu, nu, nc, nu, rhs, gx + nx, false, red);
     }
   } else {
     const int j = i - D.nnl, nc = D.s3_nc[j];
@@ -330,24 +349,16 @@ __device__ void item_back(const FusedArgs& F, int i, Smem& S, uint32_t& phase) {
       const double* gd = D.gNd + size_t(j) * nx;
       for (int r = t; r < nx; r += kFT) gx[r] = gd[r] * ec[r];
     } else {
-      for (int r = t; r < nc; r += kFT) tv[r] = ec[r];
+      for (int r = t; r < nc; r += kFT) rhs[r] = ec[r];
       __syncthreads();
-      cta_gemv(D.GNT + D.gN_off[j] * nx, nx, nc, nx, tv, gx, false, red);
+      cta_gemv(D.GNT + D.gN_off[j] * nx, nx, nc, nx, rhs, gx, false, red);
     }
   }
   __syncthreads();
-  // ---- matrices resident
-  if (F.stage_smem) {
-    while (!mbar_try_wait(&S.bar, phase)) {
-    }
-    phase ^= 1u;
-  }
-  const double* qkv = root ? nullptr : D.qk + size_t(i - 1) * m;
-  if (!root) {  // own stage SOC adjoint term for the parent
-    const int o2 = D.s2_off[i - 1], p = px + pu;
-    for (int r = t; r < p; r += kFT) head[r] = eta[o2 + r];
-    const double rsum = eta[o2 + p] + eta[o2 + p + 1];
-    __syncthreads();
+  const double *HxT = sp[0], *HuT = sp[1], *M1T = sp[2], *KT = sp[3], *Ri = sp[4], *HNT = sp[5];
+  wait_blocks(F, S, phase);
+  if (!root) {  // own stage-SOC adjoint term for the parent: adj_i = H' head - rsum/2 qk
+    const double* qkv = D.qk + size_t(i - 1) * m;
     for (int r = t; r < m; r += kFT) tv[r] = -0.5 * rsum * qkv[r];
     __syncthreads();
     cta_gemv(HxT, nx, px, nx, head, tv, true, red);
@@ -355,54 +366,51 @@ __device__ void item_back(const FusedArgs& F, int i, Smem& S, uint32_t& phase) {
     double* adj = D.adj + size_t(i - 1) * m;
     for (int r = t; r < m; r += kFT) adj[r] = tv[r];
   }
-  if (leaf) {  // terminal SOC adjoint term: x part of L* eta
-    const int j = i - D.nnl, p = pN;
+  if (leaf) {  // terminal SOC term of L* (x part): + H_N' head_N - rsum_N/2 qk_N
+    const int j = i - D.nnl;
     const double* hd = eta + D.s3_off[j] + D.s3_nc[j];
     __syncthreads();
-    for (int r = t; r < p; r += kFT) head[r] = hd[r];
-    const double rsum = hd[p] + hd[p + 1];
+    for (int r = t; r < pN; r += kFT) head[r] = hd[r];
+    rsumN = hd[pN] + hd[pN + 1];
     __syncthreads();
-    cta_gemv(HNT, nx, p, nx, head, gx, true, red);
+    cta_gemv(HNT, nx, pN, nx, head, gx, true, red);
     const double* qk = D.qkN + size_t(j) * nx;
-    for (int r = t; r < nx; r += kFT) gx[r] -= 0.5 * rsum * qk[r];
+    for (int r = t; r < nx; r += kFT) {
+      gx[r] -= 0.5 * rsumN * qk[r];
+      q[r] = -(xb[r] - al * gx[r]);  // leaf: q = -xbar
+    }
     __syncthreads();
-  }
-  // ---- children results
-  const int c0 = D.cf[i], nch = D.cc[i];
-  if (t == 0)
-    for (int c = 0; c < nch; ++c) wait_flag(F.flagB + c0 + c, 1);
-  __syncthreads();
-  for (int r = t; r < m; r += kFT) {
-    if (leaf && r >= nx) break;
-    double v = gx[r];
-    for (int c = 0; c < nch; ++c) v += ldcg(D.adj + size_t(c0 + c - 1) * m + r);
-    const double zv = r < nx ? z[1 + size_t(i) * nx + r] : z[D.u_base + size_t(i) * nu + (r - nx)];
-    xb[r] = zv - al * v;  // (xbar, ubar)
-  }
-  __syncthreads();
-  if (leaf) {
-    for (int r = t; r < nx; r += kFT) q[r] = -xb[r];
   } else {
+    // ---- 3. children (flags), then q, d
+    const int c0 = D.cf[i], nch = D.cc[i];
+    if (t == 0)
+      for (int c = 0; c < nch; ++c) wait_flag(F.flagB + c0 + c, 1);
+    __syncthreads();
     const double* h = D.h + size_t(i) * nx;
     const double* gv = D.g + size_t(i) * nu;
     for (int r = t; r < m; r += kFT) {
-      double v = 0.0;
-      for (int c = 0; c < nch; ++c) v += ldcg(D.T12 + size_t(c0 + c - 1) * m + r);
-      if (r < nx)
-        q[r] = h[r] - xb[r] + v;
-      else
-        rhs[r - nx] = xb[r] - gv[r - nx] - v;
+      double lt = gx[r], tq = 0.0;
+      for (int c = 0; c < nch; ++c) {
+        const size_t o = size_t(c0 + c - 1) * m + r;
+        lt += ldcg(D.adj + o);
+        tq += ldcg(D.T12 + o);
+      }
+      const double w = xb[r] - al * lt;  // (xbar, ubar)
+      if (r < nx) {
+        q[r] = h[r] - w + tq;
+      } else {
+        xb[r] = w;  // ubar
+        rhs[r - nx] = w - gv[r - nx] - tq;
+      }
     }
-    __syncthreads();
-    for (int r = t; r < nx; r += kFT) tv[r] = 0.0;
     __syncthreads();
     cta_gemv(KT, nx, nu, nx, xb + nx, tv, false, red);  // K' ubar
     for (int r = t; r < nx; r += kFT) q[r] -= tv[r];
-    cta_gemv(Ri, nu, nu, nu, rhs, tv, false, red);  // d
+    cta_gemv(Ri, nu, nu, nu, rhs, tv + nx, false, red);  // d
     double* dv = D.dvec + size_t(i) * nu;
-    for (int r = t; r < nu; r += kFT) dv[r] = tv[r];
+    for (int r = t; r < nu; r += kFT) dv[r] = tv[nx + r];
+    __syncthreads();
   }
-  __syncthreads();
   if (!root) {
     cta_gemv(M1T, m, nx, m, q, tv, false, red);
     double* T12 = D.T12 + size_t(i - 1) * m;
@@ -411,9 +419,7 @@ __device__ void item_back(const FusedArgs& F, int i, Smem& S, uint32_t& phase) {
     const double sc = eta[D.s1_off[0] + D.y_dim[0]];
     F.zo[0] = z[0] - al * sc - al;  // CP primal step on s0 (solver.cpp:153-154)
   }
-  __threadfence();
-  __syncthreads();
-  if (t == 0) st_release(F.flagB + i, 1);
+  cta_release(F.flagB + i);
 }
 
 __device__ void item_fwd(const FusedArgs& F, int c, Smem& S, uint32_t& phase) {
@@ -429,66 +435,52 @@ __device__ void item_fwd(const FusedArgs& F, int c, Smem& S, uint32_t& phase) {
   if (!root) px = D.px[c - 1], pu = D.pu[c - 1];
   if (leaf) pN = D.pN[c - D.nnl];
   __shared__ const double* sp[5];
-  if (t == 0) {
-    Stager st{S.mat, 0, 0, F.stage_smem != 0};
-    fence_proxy_async();
-    uint32_t total = 0;
-    auto pad = [](int d) { return uint32_t(((d + 1) & ~1) * 8); };
-    if (st.on) {
-      if (!root) total += pad(nx * m) + pad(px * nx) + pad(pu * nu);
-      if (!leaf) total += pad(nu * nx);
-      if (leaf) total += pad(pN * nx);
-      if (total) mbar_expect_tx(&S.bar, total);
-    }
-    const double *a = nullptr, *b = nullptr, *cc = nullptr, *d = nullptr, *e = nullptr;
+  {
+    const double* src[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    int dbl[5] = {0, 0, 0, 0, 0};
     if (!root) {
-      a = st.take(D.M1 + size_t(c - 1) * D.m1_stride, nx * m, &S.bar);
-      b = st.take(D.Hx + D.hx_off[c - 1], px * nx, &S.bar);
-      cc = st.take(D.Hu + D.hu_off[c - 1], pu * nu, &S.bar);
+      src[0] = D.M1 + size_t(c - 1) * D.m1_stride, dbl[0] = nx * m;
+      src[1] = D.Hx + D.hx_off[c - 1], dbl[1] = px * nx;
+      src[2] = D.Hu + D.hu_off[c - 1], dbl[2] = pu * nu;
     }
     if (!leaf)
-      d = st.take(D.K + size_t(c) * D.k_stride, nu * nx, &S.bar);
+      src[3] = D.K + size_t(c) * D.k_stride, dbl[3] = nu * nx;
     else
-      e = st.take(D.HN + D.hn_off[c - D.nnl], pN * nx, &S.bar);
-    sp[0] = a, sp[1] = b, sp[2] = cc, sp[3] = d, sp[4] = e;
-    if (st.on && !total) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&S.bar)) : "memory");
+      src[4] = D.HN + D.hn_off[c - D.nnl], dbl[4] = pN * nx;
+    stage_blocks(F, S, src, dbl, 5, sp);
   }
+  double* V = S.vec;
+  double* xd = V;              // [x_anc+; d_anc]
+  double* xn = xd + kSlot;     // own (x+, u+)
+  double* zown = xn + kSlot;   // own (x, u) of z
+  double* ahat = zown + kSlot; // anc (x^, u^)
+  double* val = ahat + kSlot;  // segment values
+  double* pv = val + kSlot;    // p / alpha
+  double* red = S.red;
+  // independent of the parent
+  for (int r = t; r < (leaf ? nx : m); r += kFT)
+    zown[r] = r < nx ? z[1 + size_t(c) * nx + r] : z[D.u_base + size_t(c) * nu + (r - nx)];
+  const int an = root ? 0 : D.anc[c];
+  if (!root)
+    for (int r = t; r < m; r += kFT)
+      ahat[r] = -(r < nx ? z[1 + size_t(an) * nx + r] : z[D.u_base + size_t(an) * nu + (r - nx)]);
+  double dself = 0.0;  // own d entry for thread t < nu
   __syncthreads();
   const double *M1 = sp[0], *Hx = sp[1], *Hu = sp[2], *K = sp[3], *HN = sp[4];
-  double* V = S.vec;
-  double* xd = V;             // [x_anc+; d_anc]  (m)
-  double* xn = xd + kSlot;    // own (x+, u+)     (m)
-  double* hat = xn + kSlot;   // own (x^, u^)     (m)
-  double* ahat = hat + kSlot; // anc (x^, u^)     (m)
-  double* val = ahat + kSlot; // segment values (<= kMaxD)
-  double* pv = val + kSlot;   // p / alpha       (<= kMaxD + 2)
-  double* red = S.red;
-  // ---- dependencies: parent forward (root: own backward), S2 of self/parent
-  if (t == 0) {
-    if (root)
-      wait_flag(F.flagB + 0, 1);
-    else
-      wait_flag(F.flagF + D.anc[c], 1);
-    if (!leaf) wait_flag(F.flagS2 + c, 1);
-    if (!root) wait_flag(F.flagS2 + D.anc[c], 1);
-  }
+  wait_blocks(F, S, phase);
+  // ---- parent forward (root: own backward)
+  if (t == 0) wait_flag(root ? F.flagB : F.flagF + an, 1);
   __syncthreads();
-  if (F.stage_smem) {
-    while (!mbar_try_wait(&S.bar, phase)) {
-    }
-    phase ^= 1u;
-  }
-  const int an = root ? 0 : D.anc[c];
+  if (!leaf && t < nu) dself = ldcg(D.dvec + size_t(c) * nu + t);
   if (!root) {
     for (int r = t; r < m; r += kFT) {
       if (r < nx) {
         const double xp = ldcg(zo + 1 + size_t(an) * nx + r);
         xd[r] = xp;
-        ahat[r] = 2.0 * xp - z[1 + size_t(an) * nx + r];
+        ahat[r] += 2.0 * xp;
       } else {
         xd[r] = ldcg(D.dvec + size_t(an) * nu + (r - nx));
-        const double up = ldcg(zo + D.u_base + size_t(an) * nu + (r - nx));
-        ahat[r] = 2.0 * up - z[D.u_base + size_t(an) * nu + (r - nx)];
+        ahat[r] += 2.0 * ldcg(zo + D.u_base + size_t(an) * nu + (r - nx));
       }
     }
     __syncthreads();
@@ -501,22 +493,25 @@ __device__ void item_fwd(const FusedArgs& F, int c, Smem& S, uint32_t& phase) {
   __syncthreads();
   if (!leaf) {
     cta_gemv(K, nu, nx, nu, xn, xn + nx, false, red);
-    const double* dv = D.dvec + size_t(c) * nu;
-    for (int r = t; r < nu; r += kFT) xn[nx + r] += ldcg(dv + r);
+    if (t < nu) xn[nx + t] += dself;
     __syncthreads();
   }
   for (int r = t; r < (leaf ? nx : m); r += kFT) {
-    if (r < nx) {
+    if (r < nx)
       zo[1 + size_t(c) * nx + r] = xn[r];
-      hat[r] = 2.0 * xn[r] - z[1 + size_t(c) * nx + r];
-    } else {
+    else
       zo[D.u_base + size_t(c) * nu + (r - nx)] = xn[r];
-      hat[r] = 2.0 * xn[r] - z[D.u_base + size_t(c) * nu + (r - nx)];
-    }
+  }
+  // children need only (x+, u+) and d: release before the dual work
+  cta_release(F.flagF + c);
+  for (int r = t; r < (leaf ? nx : m); r += kFT) zown[r] = 2.0 * xn[r] - zown[r];  // own (x^, u^)
+  if (t == 0) {
+    if (!leaf) wait_flag(F.flagS2 + c, 1);
+    if (!root) wait_flag(F.flagS2 + an, 1);
   }
   __syncthreads();
-  // ---- dual segments owned by c
-  auto dual = [&](int off, int d) {  // eo[off..off+d) from val[0..d) (pre-projection values)
+  const double* hat = zown;
+  auto dual = [&](int off, int d) {
     for (int r = t; r < d; r += kFT) {
       const double p = eta[off + r] + al * val[r];
       val[r] = p;
@@ -650,9 +645,6 @@ __device__ void item_fwd(const FusedArgs& F, int c, Smem& S, uint32_t& phase) {
     for (int r = t; r < p + 2; r += kFT) eo[so + r] = val[r] - al * pv[r];
     __syncthreads();
   }
-  __threadfence();
-  __syncthreads();
-  if (t == 0) st_release(F.flagF + c, 1);
 }
 
 __global__ void __launch_bounds__(kFT, 1) k_T_fused(FusedArgs F) {
