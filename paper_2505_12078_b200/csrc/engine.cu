@@ -104,44 +104,59 @@ void Engine::setup_fused() {
   const char* env = std::getenv("SPOCK_T_UNFUSED");
   if (env && env[0] == '1') fused_ok_ = false;
   if (!fused_ok_) return;
-  // largest per-item set of staged blocks (even doubles each)
-  int64_t mx = 0;
+  // largest per-item set of staged blocks and prefetched vector spans (even
+  // doubles each), mirroring make_plan in fused.cu
+  int64_t mx = 0, vx = 0;
   for (int i = 0; i < nn; ++i) {
     const bool leaf = tr.leaf(i), root = i == 0;
-    int64_t b = 0, f = 0;
+    int64_t b = 0, f = 0, vb = pad2(nx), vf = pad2(nx);
     if (!root) {
-      const int px = soc_.stage[i - 1].px, pu = soc_.stage[i - 1].pu;
+      const int px = soc_.stage[i - 1].px, pu = soc_.stage[i - 1].pu, p = px + pu;
       b += pad2(int64_t(px) * nx) + pad2(int64_t(pu) * nu) + pad2(int64_t(m) * nx);
       f += pad2(int64_t(nx) * m) + pad2(int64_t(px) * nx) + pad2(int64_t(pu) * nu);
+      vb += pad2(p + 2) + pad2(m);
+      vf += pad2(nx) + pad2(nu) + pad2(nx) + 2 * pad2(p + 2) + pad2(m);
     }
     if (!leaf) {
+      const int nc = p_.nc[i], ny = lay_.y_dim[i];
       b += pad2(int64_t(nx) * nu) + pad2(int64_t(nu) * nu);
       f += pad2(int64_t(nu) * nx);
+      vb += pad2(nu) + pad2(nc) + (D_.g_diag ? pad2(m) : 0) + pad2(nx) + pad2(nu);
+      vf += pad2(nu) + (D_.g_diag ? pad2(m) : 0) + 2 * pad2(nc);
+      if (ny + 1 + nc <= kMaxD) vf += pad2(ny + 1 + nc) + pad2(ny);
     } else {
-      const int pN = soc_.leaf[i - tr.nnl()].px;
+      const int j = i - tr.nnl(), pN = soc_.leaf[j].px, nc = p_.ncN[j];
       b += pad2(int64_t(pN) * nx);
       f += pad2(int64_t(pN) * nx);
+      vb += pad2(nc) + (D_.gN_diag ? pad2(nx) : 0) + pad2(pN + 2) + pad2(nx);
+      vf += pad2(nc + pN + 2) + pad2(pN + 2) + pad2(nx) + (D_.gN_diag ? pad2(nx) : 0) + 2 * pad2(nc);
     }
     mx = std::max(mx, std::max(b, f));
+    vx = std::max(vx, std::max(vb, vf));
   }
   FusedArgs& F = fargs_;
   F = FusedArgs{};
   F.stage_smem = 1;
   F.mat_doubles = int(mx);
+  F.vec_doubles = int(vx);
   int dev = 0, sms = 148, smem_optin = 0;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   CK(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  if (fused_smem_bytes(F) + 4096 > smem_optin) {  // blocks too large to stage: stream from L2/HBM
+  if (fused_smem_bytes(F) + 8192 > smem_optin) {  // blocks too large to stage: stream from L2/HBM
     F.stage_smem = 0;
     F.mat_doubles = 0;
+  }
+  if (fused_smem_bytes(F) + 8192 > smem_optin) {  // even the vector ring does not fit
+    fused_ok_ = false;
+    return;
   }
   const int bytes = fused_smem_bytes(F);
   CK(fused_configure(bytes));
   int occ = 0;
   F.D = D_;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fused_kernel_ptr(), 256, bytes));
-  fused_grid_ = std::max(1, std::min(occ, 4)) * sms;
+  fused_grid_ = std::max(1, std::min(occ, 2)) * sms;
   const int total = nnl + 2 * nn;
   fused_grid_ = std::min(fused_grid_, total);
   const size_t fb = 8 + sizeof(int) * size_t(nnl + 2 * nn);

@@ -9,13 +9,15 @@
 //   [0, nnl)            S2 of parent i (no dependencies)
 //   [nnl, nnl+nn)       backward item of node nn-1 ... 0 (children first)
 //   [nnl+nn, nnl+2nn)   forward item of node 0 ... nn-1 (parents first)
-// An item only waits on items with smaller tickets, which were taken by CTAs
-// that are already running, so the schedule cannot deadlock whatever the
-// residency.  Each CTA issues TMA bulk copies (cp.async.bulk, mbarrier
-// completion) of its node's matrices into shared memory *before* it waits on
-// the completion flags of its children (backward) or parent (forward); the
-// flag wait then overlaps the HBM traffic and the dependent chain of 2N+2
-// levels costs one flag hop plus a shared-memory GEMV per level.
+// An item only waits on items with smaller tickets.  A CTA holds at most two
+// items: the one it computes and the next one, whose operands are already in
+// flight into the other half of a two-slot shared-memory ring: the node's
+// matrices by TMA bulk copies (cp.async.bulk + mbarrier) and every operand
+// that does not depend on other items (z and eta segments, box data, SOC
+// translations, ...) by cp.async.  The smallest unfinished item is always
+// either being computed or the prefetched next item of a CTA whose current
+// item is done, so the schedule cannot deadlock.  Completion is published per
+// node with release/acquire flags (CTA barrier + one fenced release store).
 //
 // Backward item (node i), restructured Alg. 2 (see kernels.cu header):
 //   adj_i = H_i' head_i - rsum_i/2 qk_i                 (own stage SOC, for the parent)
@@ -24,7 +26,7 @@
 //   d_i = Rt_i^{-1}(ubar_i - sum_c [B_c' q_c] - g_i)
 //   [Abar_i' q_i; B_i' q_i] -> T12_i for the parent
 // Forward item (node c):
-//   x_c = [Abar_c B_c][x_anc; d_anc] + c_c,  u_c = K_c x_c + d_c
+//   x_c = [Abar_c B_c][x_anc; d_anc] + c_c,  u_c = K_c x_c + d_c  (flag released here)
 //   then every dual segment owned by c: eta+ = p - a Pi_S3(p / a),
 //   p = eta + a L(2 z+ - z).
 #include <cuda_runtime.h>
@@ -38,9 +40,10 @@ namespace spock {
 
 namespace {
 
-constexpr int kFT = 256;  // threads per CTA
-constexpr int kSlot = kMaxD + 8;  // doubles per vector slot in shared memory
-constexpr int kSlots = 6;
+constexpr int kFT = 256;   // threads per CTA
+constexpr int kMaxSpans = 24;
+constexpr int kSlot = kMaxD + 8;  // doubles per scratch vector slot
+constexpr int kScratch = 6;       // scratch slots per CTA
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -51,6 +54,9 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -68,6 +74,14 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t phase) {
       : "memory");
   return ok != 0;
 }
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
@@ -80,17 +94,20 @@ __device__ __forceinline__ void st_release(int* p, int v) {
 // loads of data produced by other CTAs in this launch: L2 only (no stale L1)
 __device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
 
-struct Smem {
-  uint64_t bar;
-  int item;
-  int pad_;
-  double* mat;  // matrix staging area (dynamic smem)
-  double* vec;  // vector scratch
-  double* red;  // 2*kFT doubles
-};
+__device__ void wait_flag(const int* f) {
+  while (ld_acquire(f) < 1) __nanosleep(20);
+}
+// CTA barrier, then one fenced release store (CUTLASS GenericBarrier pattern)
+__device__ __forceinline__ void cta_release(int* flag) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    st_release(flag, 1);
+  }
+}
 
-// y[r] = (acc ? y[r] : 0) + sum_c A[r + c*lda] x[c], r < m <= kFT; every
-// thread of the CTA participates (column slices reduced in fixed order).
+// y[r] = (acc ? y[r] : 0) + sum_c A[r + c*lda] x[c], r < m <= kFT; all threads
+// participate (column slices reduced in fixed order => deterministic).
 __device__ void cta_gemv(const double* A, int m, int n, int lda, const double* x, double* y, bool acc,
                          double* red) {
   const int t = threadIdx.x;
@@ -98,8 +115,16 @@ __device__ void cta_gemv(const double* A, int m, int n, int lda, const double* x
   const int slices = max(1, kFT / m);
   const int r = t % m, s = t / m;
   double v = 0.0;
-  if (s < slices && n > 0)
-    for (int c = s; c < n; c += slices) v = fma(A[r + size_t(c) * lda], x[c], v);
+  if (s < slices && n > 0) {
+    int c = s;
+    for (; c + 3 * slices < n; c += 4 * slices) {
+      v = fma(A[r + size_t(c) * lda], x[c], v);
+      v = fma(A[r + size_t(c + slices) * lda], x[c + slices], v);
+      v = fma(A[r + size_t(c + 2 * slices) * lda], x[c + 2 * slices], v);
+      v = fma(A[r + size_t(c + 3 * slices) * lda], x[c + 3 * slices], v);
+    }
+    for (; c < n; c += slices) v = fma(A[r + size_t(c) * lda], x[c], v);
+  }
   if (t < m * slices) red[t] = v;
   __syncthreads();
   if (t < m) {
@@ -110,7 +135,6 @@ __device__ void cta_gemv(const double* A, int m, int n, int lda, const double* x
   __syncthreads();
 }
 
-// sum over the CTA, result broadcast to all threads
 __device__ double cta_sum(double v, double* red) {
   v = warp_sum(v);
   const int w = threadIdx.x >> 5;
@@ -118,12 +142,13 @@ __device__ double cta_sum(double v, double* red) {
   if ((threadIdx.x & 31) == 0) red[w] = v;
   __syncthreads();
   double s = 0.0;
+#pragma unroll
   for (int k = 0; k < kFT / 32; ++k) s += red[k];
   __syncthreads();
   return s;
 }
 
-// translated SOC projection of v[0..d) (axis last) in place: v <- a + Pi_SOC(v - a)
+// v <- a + Pi_SOC(v - a), axis last, in place (projections.cpp:11-37)
 __device__ void cta_soc_project(double* v, const double* a, int d, double* red) {
   const int t = threadIdx.x;
   double s = 0.0;
@@ -133,7 +158,6 @@ __device__ void cta_soc_project(double* v, const double* a, int d, double* red) 
   }
   const double hn = sqrt(cta_sum(s, red));
   const double tt = v[d - 1];
-  __syncthreads();
   if (hn <= tt) {
   } else if (hn <= -tt) {
     for (int r = t; r < d; r += kFT) v[r] = 0.0;
@@ -147,8 +171,173 @@ __device__ void cta_soc_project(double* v, const double* a, int d, double* red) 
   __syncthreads();
 }
 
-__device__ void wait_flag(const int* f, int epoch) {
-  while (ld_acquire(f) < epoch) __nanosleep(32);
+// ---------------------------------------------------------------------------
+// Prefetch plan of one item: matrices (bulk) and independent vector spans.
+enum Span : int {
+  // backward
+  B_HEAD = 0, B_QK, B_ZX, B_ZU, B_EC, B_GD, B_H, B_G, B_HEADN, B_QKN,
+  // forward
+  F_ZX = 0, F_ZU, F_AX, F_AU, F_CV, F_SEG2, F_A, F_QK, F_GD, F_LO, F_HI, F_SEG3, F_AN, F_QKN, F_GND, F_LON,
+  F_HIN, F_SEG1, F_RB
+};
+
+struct Plan {
+  int kind;  // 0 S2, 1 backward, 2 forward
+  int node;
+  int nmat;
+  const double* msrc[6];
+  int mdbl[6];
+  int nspan;
+  const double* vsrc[kMaxSpans];
+  int vn[kMaxSpans];
+};
+
+__device__ void make_plan(const FusedArgs& F, int it, Plan& P) {
+  const Dev& D = F.D;
+  const int nnl = D.nnl, nn = D.nn, nx = D.nx, nu = D.nu, m = nx + nu;
+  P.nmat = 0;
+  P.nspan = 0;
+  for (int k = 0; k < kMaxSpans; ++k) P.vsrc[k] = nullptr, P.vn[k] = 0;
+  auto mat = [&](const double* s, int n) {
+    P.msrc[P.nmat] = s;
+    P.mdbl[P.nmat] = n;
+    ++P.nmat;
+  };
+  auto vec = [&](int id, const double* s, int n) {
+    P.vsrc[id] = s;
+    P.vn[id] = n;
+    P.nspan = max(P.nspan, id + 1);
+  };
+  if (it < nnl) {
+    P.kind = 0;
+    P.node = it;
+    return;
+  }
+  const double* z = F.z;
+  const double* eta = F.eta;
+  if (it < nnl + nn) {
+    const int i = nn - 1 - (it - nnl);
+    P.kind = 1;
+    P.node = i;
+    const bool leaf = D.cc[i] == 0, root = i == 0;
+    if (!root) {
+      const int px = D.px[i - 1], pu = D.pu[i - 1];
+      mat(D.HxT + D.hx_off[i - 1], px * nx);
+      mat(D.HuT + D.hu_off[i - 1], pu * nu);
+      mat(D.M1T + size_t(i - 1) * D.m1_stride, m * nx);
+      vec(B_HEAD, eta + D.s2_off[i - 1], px + pu + 2);
+      vec(B_QK, D.qk + size_t(i - 1) * m, m);
+    }
+    vec(B_ZX, z + 1 + size_t(i) * nx, nx);
+    if (!leaf) {
+      mat(D.KT + size_t(i) * D.k_stride, nx * nu);
+      mat(D.Rinv + size_t(i) * D.r_stride, nu * nu);
+      vec(B_ZU, z + D.u_base + size_t(i) * nu, nu);
+      const int nc = D.s1_nc[i];
+      vec(B_EC, eta + D.s1_off[i] + D.y_dim[i] + 1, nc);
+      if (D.g_diag) vec(B_GD, D.gd + size_t(i) * m, m);
+      vec(B_H, D.h + size_t(i) * nx, nx);
+      vec(B_G, D.g + size_t(i) * nu, nu);
+    } else {
+      const int j = i - nnl, pN = D.pN[j], nc = D.s3_nc[j];
+      mat(D.HNT + D.hn_off[j], pN * nx);
+      vec(B_EC, eta + D.s3_off[j], nc);
+      if (D.gN_diag) vec(B_GD, D.gNd + size_t(j) * nx, nx);
+      vec(B_HEADN, eta + D.s3_off[j] + nc, pN + 2);
+      vec(B_QKN, D.qkN + size_t(j) * nx, nx);
+    }
+    return;
+  }
+  const int c = it - nnl - nn;
+  P.kind = 2;
+  P.node = c;
+  const bool leaf = D.cc[c] == 0, root = c == 0;
+  vec(F_ZX, z + 1 + size_t(c) * nx, nx);
+  if (!leaf) vec(F_ZU, z + D.u_base + size_t(c) * nu, nu);
+  if (!root) {
+    const int px = D.px[c - 1], pu = D.pu[c - 1], an = D.anc[c], p = px + pu;
+    mat(D.M1 + size_t(c - 1) * D.m1_stride, nx * m);
+    mat(D.Hx + D.hx_off[c - 1], px * nx);
+    mat(D.Hu + D.hu_off[c - 1], pu * nu);
+    vec(F_AX, z + 1 + size_t(an) * nx, nx);
+    vec(F_AU, z + D.u_base + size_t(an) * nu, nu);
+    vec(F_CV, D.cvec + size_t(c - 1) * nx, nx);
+    vec(F_SEG2, eta + D.s2_off[c - 1], p + 2);
+    vec(F_A, D.a + D.a_off[c - 1], p + 2);
+    vec(F_QK, D.qk + size_t(c - 1) * m, m);
+  }
+  if (!leaf) {
+    mat(D.K + size_t(c) * D.k_stride, nu * nx);
+    const int nc = D.s1_nc[c], ny = D.y_dim[c];
+    if (D.g_diag) vec(F_GD, D.gd + size_t(c) * m, m);
+    vec(F_LO, D.lo + D.g_off[c], nc);
+    vec(F_HI, D.hi + D.g_off[c], nc);
+    if (ny + 1 + nc <= kMaxD) {
+      vec(F_SEG1, eta + D.s1_off[c], ny + 1 + nc);
+      vec(F_RB, D.rb + (D.y_off[c] - D.y_base), ny);
+    }
+  } else {
+    const int j = c - nnl, pN = D.pN[j], nc = D.s3_nc[j];
+    mat(D.HN + D.hn_off[j], pN * nx);
+    vec(F_SEG3, eta + D.s3_off[j], nc + pN + 2);
+    vec(F_AN, D.aN + D.aN_off[j], pN + 2);
+    vec(F_QKN, D.qkN + size_t(j) * nx, nx);
+    if (D.gN_diag) vec(F_GND, D.gNd + size_t(j) * nx, nx);
+    vec(F_LON, D.loN + D.gN_off[j], nc);
+    vec(F_HIN, D.hiN + D.gN_off[j], nc);
+  }
+}
+
+struct Slot {
+  double* mat;
+  double* vec;
+  uint64_t* bar;
+  int voff[kMaxSpans];  // span offsets in vec
+  const double* mp[6];  // staged (or global) matrix pointers
+};
+
+// issue the prefetch of an item into a slot; every thread takes part (vector
+// spans by cp.async), thread 0 issues the bulk copies; commits one cp.async
+// group per item
+__device__ void issue(const FusedArgs& F, const Plan& P, Slot& S) {
+  const int t = threadIdx.x;
+  int off = 0;
+  for (int k = 0; k < P.nspan; ++k) {
+    if (t == 0) S.voff[k] = off;
+    off += (P.vn[k] + 1) & ~1;
+  }
+  off = 0;
+  for (int k = 0; k < P.nspan; ++k) {
+    const double* src = P.vsrc[k];
+    double* dst = S.vec + off;
+    for (int e = t; e < P.vn[k]; e += kFT) cp_async8(dst + e, src + e);
+    off += (P.vn[k] + 1) & ~1;
+  }
+  cp_async_commit();
+  if (t == 0) {
+    if (F.stage_smem && P.nmat > 0) {
+      fence_proxy_async();
+      uint32_t total = 0;
+      for (int k = 0; k < P.nmat; ++k) total += uint32_t((P.mdbl[k] + 1) & ~1) * 8u;
+      if (total)
+        mbar_expect_tx(S.bar, total);
+      else
+        mbar_arrive(S.bar);
+      int mo = 0;
+      for (int k = 0; k < P.nmat; ++k) {
+        if (P.mdbl[k] <= 0) {
+          S.mp[k] = P.msrc[k];
+          continue;
+        }
+        const int padded = (P.mdbl[k] + 1) & ~1;
+        bulk_g2s(S.mat + mo, P.msrc[k], uint32_t(padded) * 8u, S.bar);
+        S.mp[k] = S.mat + mo;
+        mo += padded;
+      }
+    } else {
+      for (int k = 0; k < P.nmat; ++k) S.mp[k] = P.msrc[k];
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -183,7 +372,7 @@ __device__ void item_s2(const FusedArgs& F, int i, double* red, double* vec) {
   const int kind = D.s2_kind[i];
   if (kind == S2_DENSE) {
     const int dim = ny + 2 * n;
-    double* w = vec;  // dim <= kMaxD
+    double* w = vec;
     for (int r = t; r < dim; r += kFT) w[r] = r < ny ? wy(r) : (r < ny + n ? wtau(r - ny) : ws(r - ny - n));
     __syncthreads();
     double* o = w + kSlot;
@@ -238,127 +427,60 @@ __device__ void item_s2(const FusedArgs& F, int i, double* red, double* vec) {
   __syncthreads();
 }
 
-// release a completion flag: CTA barrier, then one fenced release store
-// (the semaphore pattern of CUTLASS's GenericBarrier)
-__device__ __forceinline__ void cta_release(int* flag) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    st_release(flag, 1);
-  }
-}
-
-// issue the bulk copies of one item's blocks (thread 0); returns staged (or
-// global) pointers through `out`
-__device__ void stage_blocks(const FusedArgs& F, Smem& S, const double* const* src, const int* doubles, int n,
-                             const double** out) {
-  if (threadIdx.x != 0) return;
-  if (!F.stage_smem) {
-    for (int k = 0; k < n; ++k) out[k] = src[k];
-    return;
-  }
-  fence_proxy_async();
-  uint32_t total = 0;
-  for (int k = 0; k < n; ++k) total += uint32_t((doubles[k] + 1) & ~1) * 8u;
-  if (total)
-    mbar_expect_tx(&S.bar, total);
-  else
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&S.bar)) : "memory");
-  int off = 0;
-  for (int k = 0; k < n; ++k) {
-    if (doubles[k] <= 0) {
-      out[k] = src[k];
-      continue;
-    }
-    const int padded = (doubles[k] + 1) & ~1;
-    bulk_g2s(S.mat + off, src[k], uint32_t(padded) * 8u, &S.bar);
-    out[k] = S.mat + off;
-    off += padded;
-  }
-}
-
-__device__ __forceinline__ void wait_blocks(const FusedArgs& F, Smem& S, uint32_t& phase) {
-  if (!F.stage_smem) return;
-  while (!mbar_try_wait(&S.bar, phase)) {
-  }
-  phase ^= 1u;
-}
-
-__device__ void item_back(const FusedArgs& F, int i, Smem& S, uint32_t& phase) {
+__device__ void item_back(const FusedArgs& F, const Plan& P, const Slot& S, double* sc_, double* red) {
   const Dev& D = F.D;
+  const int i = P.node;
   const int t = threadIdx.x, nx = D.nx, nu = D.nu, m = nx + nu;
   const bool leaf = D.cc[i] == 0, root = i == 0;
   const double al = F.alpha;
-  const double* z = F.z;
-  const double* eta = F.eta;
-  int px = 0, pu = 0, pN = 0;
+  const double* V = S.vec;
+  auto sp = [&](int id) { return V + S.voff[id]; };
+  double* gx = sc_;           // L* (x, u) of this node without the children
+  double* q = gx + kSlot;     // q (nx)
+  double* tv = q + kSlot;     // scratch (m)
+  double* rhs = tv + kSlot;   // scratch (m)
+  int px = 0, pu = 0;
   if (!root) px = D.px[i - 1], pu = D.pu[i - 1];
-  if (leaf) pN = D.pN[i - D.nnl];
-  // ---- 1. prefetch this node's blocks: H_x', H_u' (own stage SOC), M1' (own
-  // sweep block), K', Rt^-1 (non-leaf) or H_N' (leaf)
-  __shared__ const double* sp[6];
-  {
-    const double* src[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
-    int dbl[6] = {0, 0, 0, 0, 0, 0};
-    if (!root) {
-      src[0] = D.HxT + D.hx_off[i - 1], dbl[0] = px * nx;
-      src[1] = D.HuT + D.hu_off[i - 1], dbl[1] = pu * nu;
-      src[2] = D.M1T + size_t(i - 1) * D.m1_stride, dbl[2] = m * nx;
-    }
-    if (!leaf) {
-      src[3] = D.KT + size_t(i) * D.k_stride, dbl[3] = nx * nu;
-      src[4] = D.Rinv + size_t(i) * D.r_stride, dbl[4] = nu * nu;
-    } else {
-      src[5] = D.HNT + D.hn_off[i - D.nnl], dbl[5] = pN * nx;
-    }
-    stage_blocks(F, S, src, dbl, 6, sp);
-  }
-  double* V = S.vec;
-  double* head = V;          // own stage-SOC head (p), later the leaf head (pN)
-  double* gx = head + kSlot; // G' ec (+ leaf terms): L* (x, u) without the children
-  double* xb = gx + kSlot;   // z (x, u) of this node
-  double* q = xb + kSlot;    // q (nx)
-  double* tv = q + kSlot;    // scratch (m)
-  double* rhs = tv + kSlot;  // scratch (m)
-  double* red = S.red;
-  // ---- 2. everything that does not depend on the children
-  double rsum = 0.0, rsumN = 0.0;
-  if (!root) {
-    const int o2 = D.s2_off[i - 1], p = px + pu;
-    for (int r = t; r < p; r += kFT) head[r] = eta[o2 + r];
-    rsum = eta[o2 + p] + eta[o2 + p + 1];
-  }
-  for (int r = t; r < (leaf ? nx : m); r += kFT)
-    xb[r] = r < nx ? z[1 + size_t(i) * nx + r] : z[D.u_base + size_t(i) * nu + (r - nx)];
+  int mk = 0;
+  const double* HxT = root ? nullptr : S.mp[mk++];
+  const double* HuT = root ? nullptr : S.mp[mk++];
+  const double* M1T = root ? nullptr : S.mp[mk++];
+  const double* KT = leaf ? nullptr : S.mp[mk++];
+  const double* Ri = leaf ? nullptr : S.mp[mk++];
+  const double* HNT = leaf ? S.mp[mk++] : nullptr;
+  // ---- own G' ec (+ terminal SOC term for leaves); independent of children
   if (!leaf) {
-    const int ny = D.y_dim[i], nc = D.s1_nc[i];
-    const double* ec = eta + D.s1_off[i] + ny + 1;
+    const int nc = D.s1_nc[i];
+    const double* ec = sp(B_EC);
     if (D.g_diag) {
-      const double* gd = D.gd + size_t(i) * m;
+      const double* gd = sp(B_GD);
       for (int r = t; r < m; r += kFT) gx[r] = gd[r] * ec[r];
-    } else {
-      for (int r = t; r < nc; r += kFT) rhs[r] = ec[r];
       __syncthreads();
-      cta_gemv(D.GxT + D.g_off[i] * nx, nx, nc, nx, rhs, gx, false, red);
-      cta_gemv(D.GuT + D.g_off[i] * nu, nu, nc, nu, rhs, gx + nx, false, red);
+    } else {
+      cta_gemv(D.GxT + D.g_off[i] * nx, nx, nc, nx, ec, gx, false, red);
+      cta_gemv(D.GuT + D.g_off[i] * nu, nu, nc, nu, ec, gx + nx, false, red);
     }
   } else {
-    const int j = i - D.nnl, nc = D.s3_nc[j];
-    const double* ec = eta + D.s3_off[j];
+    const int j = i - D.nnl, nc = D.s3_nc[j], pN = D.pN[j];
+    const double* ec = sp(B_EC);
     if (D.gN_diag) {
-      const double* gd = D.gNd + size_t(j) * nx;
+      const double* gd = sp(B_GD);
       for (int r = t; r < nx; r += kFT) gx[r] = gd[r] * ec[r];
-    } else {
-      for (int r = t; r < nc; r += kFT) rhs[r] = ec[r];
       __syncthreads();
-      cta_gemv(D.GNT + D.gN_off[j] * nx, nx, nc, nx, rhs, gx, false, red);
+    } else {
+      cta_gemv(D.GNT + D.gN_off[j] * nx, nx, nc, nx, ec, gx, false, red);
     }
+    const double* hd = sp(B_HEADN);
+    cta_gemv(HNT, nx, pN, nx, hd, gx, true, red);
+    const double rsumN = hd[pN] + hd[pN + 1];
+    const double* qk = sp(B_QKN);
+    const double* zx = sp(B_ZX);
+    for (int r = t; r < nx; r += kFT) q[r] = -(zx[r] - al * (gx[r] - 0.5 * rsumN * qk[r]));  // q = -xbar
   }
-  __syncthreads();
-  const double *HxT = sp[0], *HuT = sp[1], *M1T = sp[2], *KT = sp[3], *Ri = sp[4], *HNT = sp[5];
-  wait_blocks(F, S, phase);
   if (!root) {  // own stage-SOC adjoint term for the parent: adj_i = H' head - rsum/2 qk
-    const double* qkv = D.qk + size_t(i - 1) * m;
+    const double* head = sp(B_HEAD);
+    const double rsum = head[px + pu] + head[px + pu + 1];
+    const double* qkv = sp(B_QK);
     for (int r = t; r < m; r += kFT) tv[r] = -0.5 * rsum * qkv[r];
     __syncthreads();
     cta_gemv(HxT, nx, px, nx, head, tv, true, red);
@@ -366,28 +488,16 @@ __device__ void item_back(const FusedArgs& F, int i, Smem& S, uint32_t& phase) {
     double* adj = D.adj + size_t(i - 1) * m;
     for (int r = t; r < m; r += kFT) adj[r] = tv[r];
   }
-  if (leaf) {  // terminal SOC term of L* (x part): + H_N' head_N - rsum_N/2 qk_N
-    const int j = i - D.nnl;
-    const double* hd = eta + D.s3_off[j] + D.s3_nc[j];
-    __syncthreads();
-    for (int r = t; r < pN; r += kFT) head[r] = hd[r];
-    rsumN = hd[pN] + hd[pN + 1];
-    __syncthreads();
-    cta_gemv(HNT, nx, pN, nx, head, gx, true, red);
-    const double* qk = D.qkN + size_t(j) * nx;
-    for (int r = t; r < nx; r += kFT) {
-      gx[r] -= 0.5 * rsumN * qk[r];
-      q[r] = -(xb[r] - al * gx[r]);  // leaf: q = -xbar
-    }
-    __syncthreads();
-  } else {
-    // ---- 3. children (flags), then q, d
+  if (!leaf) {
+    // ---- children (flags), then q and d
     const int c0 = D.cf[i], nch = D.cc[i];
     if (t == 0)
-      for (int c = 0; c < nch; ++c) wait_flag(F.flagB + c0 + c, 1);
+      for (int c = 0; c < nch; ++c) wait_flag(F.flagB + c0 + c);
     __syncthreads();
-    const double* h = D.h + size_t(i) * nx;
-    const double* gv = D.g + size_t(i) * nu;
+    const double* zx = sp(B_ZX);
+    const double* zu = sp(B_ZU);
+    const double* h = sp(B_H);
+    const double* gv = sp(B_G);
     for (int r = t; r < m; r += kFT) {
       double lt = gx[r], tq = 0.0;
       for (int c = 0; c < nch; ++c) {
@@ -395,35 +505,36 @@ __device__ void item_back(const FusedArgs& F, int i, Smem& S, uint32_t& phase) {
         lt += ldcg(D.adj + o);
         tq += ldcg(D.T12 + o);
       }
-      const double w = xb[r] - al * lt;  // (xbar, ubar)
       if (r < nx) {
-        q[r] = h[r] - w + tq;
+        q[r] = h[r] - (zx[r] - al * lt) + tq;
       } else {
-        xb[r] = w;  // ubar
-        rhs[r - nx] = w - gv[r - nx] - tq;
+        const double ub = zu[r - nx] - al * lt;  // ubar
+        tv[r] = ub;
+        rhs[r - nx] = ub - gv[r - nx] - tq;
       }
     }
     __syncthreads();
-    cta_gemv(KT, nx, nu, nx, xb + nx, tv, false, red);  // K' ubar
-    for (int r = t; r < nx; r += kFT) q[r] -= tv[r];
-    cta_gemv(Ri, nu, nu, nu, rhs, tv + nx, false, red);  // d
+    cta_gemv(KT, nx, nu, nx, tv + nx, gx, false, red);  // K' ubar (gx reused)
+    for (int r = t; r < nx; r += kFT) q[r] -= gx[r];
+    cta_gemv(Ri, nu, nu, nu, rhs, tv, false, red);  // d
     double* dv = D.dvec + size_t(i) * nu;
-    for (int r = t; r < nu; r += kFT) dv[r] = tv[nx + r];
-    __syncthreads();
+    for (int r = t; r < nu; r += kFT) dv[r] = tv[r];
   }
+  __syncthreads();
   if (!root) {
     cta_gemv(M1T, m, nx, m, q, tv, false, red);
     double* T12 = D.T12 + size_t(i - 1) * m;
     for (int r = t; r < m; r += kFT) T12[r] = tv[r];
   } else if (t == 0) {
-    const double sc = eta[D.s1_off[0] + D.y_dim[0]];
-    F.zo[0] = z[0] - al * sc - al;  // CP primal step on s0 (solver.cpp:153-154)
+    const double sc = F.eta[D.s1_off[0] + D.y_dim[0]];
+    F.zo[0] = F.z[0] - al * sc - al;  // CP primal step on s0 (solver.cpp:153-154)
   }
   cta_release(F.flagB + i);
 }
 
-__device__ void item_fwd(const FusedArgs& F, int c, Smem& S, uint32_t& phase) {
+__device__ void item_fwd(const FusedArgs& F, const Plan& P, const Slot& S, double* sc_, double* red) {
   const Dev& D = F.D;
+  const int c = P.node;
   const int t = threadIdx.x, nx = D.nx, nu = D.nu, m = nx + nu;
   const bool leaf = D.cc[c] == 0, root = c == 0;
   const double al = F.alpha;
@@ -431,61 +542,43 @@ __device__ void item_fwd(const FusedArgs& F, int c, Smem& S, uint32_t& phase) {
   const double* eta = F.eta;
   double* zo = F.zo;
   double* eo = F.eo;
-  int px = 0, pu = 0, pN = 0;
-  if (!root) px = D.px[c - 1], pu = D.pu[c - 1];
-  if (leaf) pN = D.pN[c - D.nnl];
-  __shared__ const double* sp[5];
-  {
-    const double* src[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
-    int dbl[5] = {0, 0, 0, 0, 0};
-    if (!root) {
-      src[0] = D.M1 + size_t(c - 1) * D.m1_stride, dbl[0] = nx * m;
-      src[1] = D.Hx + D.hx_off[c - 1], dbl[1] = px * nx;
-      src[2] = D.Hu + D.hu_off[c - 1], dbl[2] = pu * nu;
-    }
-    if (!leaf)
-      src[3] = D.K + size_t(c) * D.k_stride, dbl[3] = nu * nx;
-    else
-      src[4] = D.HN + D.hn_off[c - D.nnl], dbl[4] = pN * nx;
-    stage_blocks(F, S, src, dbl, 5, sp);
-  }
-  double* V = S.vec;
-  double* xd = V;              // [x_anc+; d_anc]
-  double* xn = xd + kSlot;     // own (x+, u+)
-  double* zown = xn + kSlot;   // own (x, u) of z
-  double* ahat = zown + kSlot; // anc (x^, u^)
+  const double* V = S.vec;
+  auto sp = [&](int id) { return V + S.voff[id]; };
+  double* xd = sc_;            // [x_anc+; d_anc]
+  double* xn = xd + kSlot;     // own (x+, u+), then (x^, u^)
+  double* ahat = xn + kSlot;   // anc (x^, u^)
   double* val = ahat + kSlot;  // segment values
   double* pv = val + kSlot;    // p / alpha
-  double* red = S.red;
-  // independent of the parent
-  for (int r = t; r < (leaf ? nx : m); r += kFT)
-    zown[r] = r < nx ? z[1 + size_t(c) * nx + r] : z[D.u_base + size_t(c) * nu + (r - nx)];
+  int px = 0, pu = 0;
+  if (!root) px = D.px[c - 1], pu = D.pu[c - 1];
+  int mk = 0;
+  const double* M1 = root ? nullptr : S.mp[mk++];
+  const double* Hx = root ? nullptr : S.mp[mk++];
+  const double* Hu = root ? nullptr : S.mp[mk++];
+  const double* K = leaf ? nullptr : S.mp[mk++];
+  const double* HN = leaf ? S.mp[mk++] : nullptr;
   const int an = root ? 0 : D.anc[c];
-  if (!root)
-    for (int r = t; r < m; r += kFT)
-      ahat[r] = -(r < nx ? z[1 + size_t(an) * nx + r] : z[D.u_base + size_t(an) * nu + (r - nx)]);
-  double dself = 0.0;  // own d entry for thread t < nu
-  __syncthreads();
-  const double *M1 = sp[0], *Hx = sp[1], *Hu = sp[2], *K = sp[3], *HN = sp[4];
-  wait_blocks(F, S, phase);
   // ---- parent forward (root: own backward)
-  if (t == 0) wait_flag(root ? F.flagB : F.flagF + an, 1);
+  if (t == 0) wait_flag(root ? F.flagB : F.flagF + an);
   __syncthreads();
+  double dself = 0.0;
   if (!leaf && t < nu) dself = ldcg(D.dvec + size_t(c) * nu + t);
   if (!root) {
+    const double* zax = sp(F_AX);
+    const double* zau = sp(F_AU);
     for (int r = t; r < m; r += kFT) {
       if (r < nx) {
         const double xp = ldcg(zo + 1 + size_t(an) * nx + r);
         xd[r] = xp;
-        ahat[r] += 2.0 * xp;
+        ahat[r] = 2.0 * xp - zax[r];
       } else {
         xd[r] = ldcg(D.dvec + size_t(an) * nu + (r - nx));
-        ahat[r] += 2.0 * ldcg(zo + D.u_base + size_t(an) * nu + (r - nx));
+        ahat[r] = 2.0 * ldcg(zo + D.u_base + size_t(an) * nu + (r - nx)) - zau[r - nx];
       }
     }
     __syncthreads();
     cta_gemv(M1, nx, m, nx, xd, xn, false, red);
-    const double* cv = D.cvec + size_t(c - 1) * nx;
+    const double* cv = sp(F_CV);
     for (int r = t; r < nx; r += kFT) xn[r] += cv[r];
   } else {
     for (int r = t; r < nx; r += kFT) xn[r] = D.xinit[r];
@@ -502,27 +595,23 @@ __device__ void item_fwd(const FusedArgs& F, int c, Smem& S, uint32_t& phase) {
     else
       zo[D.u_base + size_t(c) * nu + (r - nx)] = xn[r];
   }
-  // children need only (x+, u+) and d: release before the dual work
+  // children need only (x+, u+) and d: publish before the dual work
   cta_release(F.flagF + c);
-  for (int r = t; r < (leaf ? nx : m); r += kFT) zown[r] = 2.0 * xn[r] - zown[r];  // own (x^, u^)
+  {
+    const double* zx = sp(F_ZX);
+    const double* zu = sp(F_ZU);
+    for (int r = t; r < (leaf ? nx : m); r += kFT) xn[r] = 2.0 * xn[r] - (r < nx ? zx[r] : zu[r - nx]);
+  }
+  const double* hat = xn;
   if (t == 0) {
-    if (!leaf) wait_flag(F.flagS2 + c, 1);
-    if (!root) wait_flag(F.flagS2 + an, 1);
+    if (!leaf) wait_flag(F.flagS2 + c);
+    if (!root) wait_flag(F.flagS2 + an);
   }
   __syncthreads();
-  const double* hat = zown;
-  auto dual = [&](int off, int d) {
-    for (int r = t; r < d; r += kFT) {
-      const double p = eta[off + r] + al * val[r];
-      val[r] = p;
-      pv[r] = p / al;
-    }
-    __syncthreads();
-  };
   auto hatv = [&](int idx) { return 2.0 * ldcg(zo + idx) - z[idx]; };
   if (!root) {  // stage-cost SOC block of (x_anc, u_anc, tau_c)
     const int k = c - 1, p = px + pu, o2 = D.s2_off[k];
-    const double* qk = D.qk + size_t(k) * m;
+    const double* qk = sp(F_QK);
     double part = 0.0;
     for (int r = t; r < m; r += kFT) part += qk[r] * ahat[r];
     const double qd = cta_sum(part, red);
@@ -534,24 +623,32 @@ __device__ void item_fwd(const FusedArgs& F, int c, Smem& S, uint32_t& phase) {
       val[p + 1] = row;
     }
     __syncthreads();
-    dual(o2, p + 2);
-    cta_soc_project(pv, D.a + D.a_off[k], p + 2, red);
+    const double* seg = sp(F_SEG2);
+    for (int r = t; r < p + 2; r += kFT) {
+      const double pp = seg[r] + al * val[r];
+      val[r] = pp;
+      pv[r] = pp / al;
+    }
+    __syncthreads();
+    cta_soc_project(pv, sp(F_A), p + 2, red);
     for (int r = t; r < p + 2; r += kFT) eo[o2 + r] = val[r] - al * pv[r];
     __syncthreads();
   }
   if (!leaf) {  // y-copy rows (dual cone), risk scalar (R+), constraint rows (box)
     const int ny = D.y_dim[c], yo = D.y_off[c], so = D.s1_off[c], nc = D.s1_nc[c];
-    const double* rb = D.rb + (yo - D.y_base);
+    const bool pre = P.vn[F_SEG1] > 0;
+    const double* seg1 = pre ? sp(F_SEG1) : eta + so;
+    const double* rb = pre ? sp(F_RB) : D.rb + (yo - D.y_base);
     const int nn0 = D.yc_nonneg[c];
     double part = 0.0;
     for (int r = t; r < ny; r += kFT) {
       const double yh = hatv(yo + r);
       part += rb[r] * yh;
-      const double p = eta[so + r] + al * yh;
-      double tp = p / al;
+      const double pp = seg1[r] + al * yh;
+      double tp = pp / al;
       if (nn0 >= 0) {
         if (r < nn0) tp = fmax(tp, 0.0);
-        eo[so + r] = p - al * tp;
+        eo[so + r] = pp - al * tp;
       } else {
         eo[so + r] = tp;  // staged, general cone projected below
       }
@@ -585,50 +682,50 @@ __device__ void item_fwd(const FusedArgs& F, int c, Smem& S, uint32_t& phase) {
         off += dim;
       }
       for (int r = t; r < ny; r += kFT) {
-        const double p = eta[so + r] + al * hatv(yo + r);
-        eo[so + r] = p - al * eo[so + r];
+        const double pp = seg1[r] + al * hatv(yo + r);
+        eo[so + r] = pp - al * eo[so + r];
       }
     }
     if (t == 0) {
       const double sv = hatv(c == 0 ? 0 : D.s_base + c - 1) - by;
-      const double p = eta[so + ny] + al * sv;
-      eo[so + ny] = p - al * fmax(0.0, p / al);
+      const double pp = seg1[ny] + al * sv;
+      eo[so + ny] = pp - al * fmax(0.0, pp / al);
     }
-    __syncthreads();
     // constraint rows G [x^; u^] with box projection
     if (D.g_diag) {
-      const double* gd = D.gd + size_t(c) * m;
+      const double* gd = sp(F_GD);
       for (int r = t; r < nc; r += kFT) val[r] = gd[r] * hat[r];
+      __syncthreads();
     } else {
       cta_gemv(D.Gx + D.g_off[c] * nx, nc, nx, nc, hat, val, false, red);
       cta_gemv(D.Gu + D.g_off[c] * nu, nc, nu, nc, hat + nx, val, true, red);
     }
-    __syncthreads();
-    const int co = so + ny + 1;
-    const double* lo = D.lo + D.g_off[c];
-    const double* hi = D.hi + D.g_off[c];
+    const double* lo = sp(F_LO);
+    const double* hi = sp(F_HI);
+    const double* ec = seg1 + ny + 1;
     for (int r = t; r < nc; r += kFT) {
-      const double p = eta[co + r] + al * val[r];
-      eo[co + r] = p - al * fmin(fmax(p / al, lo[r]), hi[r]);
+      const double pp = ec[r] + al * val[r];
+      eo[so + ny + 1 + r] = pp - al * fmin(fmax(pp / al, lo[r]), hi[r]);
     }
     __syncthreads();
   } else {  // leaf: G_N x^ (box) and the terminal SOC block of (x, s)
-    const int j = c - D.nnl, nc = D.s3_nc[j], eo3 = D.s3_off[j], p = pN;
+    const int j = c - D.nnl, nc = D.s3_nc[j], eo3 = D.s3_off[j], p = D.pN[j];
+    const double* seg3 = sp(F_SEG3);
     if (D.gN_diag) {
-      const double* gd = D.gNd + size_t(j) * nx;
+      const double* gd = sp(F_GND);
       for (int r = t; r < nc; r += kFT) val[r] = gd[r] * hat[r];
+      __syncthreads();
     } else {
       cta_gemv(D.GN + D.gN_off[j] * nx, nc, nx, nc, hat, val, false, red);
     }
-    __syncthreads();
-    const double* lo = D.loN + D.gN_off[j];
-    const double* hi = D.hiN + D.gN_off[j];
+    const double* lo = sp(F_LON);
+    const double* hi = sp(F_HIN);
     for (int r = t; r < nc; r += kFT) {
-      const double pp = eta[eo3 + r] + al * val[r];
+      const double pp = seg3[r] + al * val[r];
       eo[eo3 + r] = pp - al * fmin(fmax(pp / al, lo[r]), hi[r]);
     }
     __syncthreads();
-    const double* qk = D.qkN + size_t(j) * nx;
+    const double* qk = sp(F_QKN);
     double part = 0.0;
     for (int r = t; r < nx; r += kFT) part += qk[r] * hat[r];
     const double qd = cta_sum(part, red);
@@ -639,52 +736,92 @@ __device__ void item_fwd(const FusedArgs& F, int c, Smem& S, uint32_t& phase) {
       val[p + 1] = row;
     }
     __syncthreads();
-    const int so = eo3 + nc;
-    dual(so, p + 2);
-    cta_soc_project(pv, D.aN + D.aN_off[j], p + 2, red);
-    for (int r = t; r < p + 2; r += kFT) eo[so + r] = val[r] - al * pv[r];
+    const double* hs = seg3 + nc;
+    for (int r = t; r < p + 2; r += kFT) {
+      const double pp = hs[r] + al * val[r];
+      val[r] = pp;
+      pv[r] = pp / al;
+    }
+    __syncthreads();
+    cta_soc_project(pv, sp(F_AN), p + 2, red);
+    for (int r = t; r < p + 2; r += kFT) eo[eo3 + nc + r] = val[r] - al * pv[r];
     __syncthreads();
   }
 }
 
 __global__ void __launch_bounds__(kFT, 1) k_T_fused(FusedArgs F) {
   extern __shared__ __align__(1024) double dsm[];
-  __shared__ Smem S;
-  __shared__ int ticket;
+  __shared__ uint64_t bars[2];
+  __shared__ Slot slots[2];
+  __shared__ int tk[2];
+  __shared__ Plan plans[2];
   const int t = threadIdx.x;
+  double* scratch = dsm + 2 * (size_t(F.mat_doubles) + F.vec_doubles);
+  double* red = scratch + kScratch * kSlot;
   if (t == 0) {
-    mbar_init(&S.bar, 1);
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    S.mat = dsm;
-    S.vec = dsm + F.mat_doubles;
-    S.red = S.vec + kSlots * kSlot;
-  }
-  __syncthreads();
-  uint32_t phase = 0;
-  const int nnl = F.D.nnl, nn = F.D.nn, total = nnl + 2 * nn;
-  for (;;) {
-    if (t == 0) ticket = int(atomicAdd(F.ticket, 1ull));
-    __syncthreads();
-    const int it = ticket;
-    __syncthreads();
-    if (it >= total) break;
-    if (it < nnl) {
-      item_s2(F, it, S.red, S.vec);
-      __threadfence();
-      __syncthreads();
-      if (t == 0) st_release(F.flagS2 + it, 1);
-    } else if (it < nnl + nn) {
-      item_back(F, nn - 1 - (it - nnl), S, phase);
-    } else {
-      item_fwd(F, it - nnl - nn, S, phase);
+    for (int s = 0; s < 2; ++s) {
+      slots[s].mat = dsm + s * (size_t(F.mat_doubles) + F.vec_doubles);
+      slots[s].vec = slots[s].mat + F.mat_doubles;
+      slots[s].bar = &bars[s];
     }
   }
+  uint32_t phase[2] = {0u, 0u};
+  const int nnl = F.D.nnl, nn = F.D.nn, total = nnl + 2 * nn;
+  // first item
+  if (t == 0) tk[0] = int(atomicAdd(F.ticket, 1ull));
+  __syncthreads();
+  int cur = 0;
+  if (tk[0] < total) {
+    if (t == 0) make_plan(F, tk[0], plans[0]);
+    __syncthreads();
+    issue(F, plans[0], slots[0]);
+  } else {
+    cp_async_commit();
+  }
+  for (;;) {
+    const int it = tk[cur];
+    if (it >= total) break;
+    const int nxt = cur ^ 1;
+    // take and prefetch the next item into the other slot
+    if (t == 0) tk[nxt] = int(atomicAdd(F.ticket, 1ull));
+    __syncthreads();
+    if (tk[nxt] < total) {
+      if (t == 0) make_plan(F, tk[nxt], plans[nxt]);
+      __syncthreads();
+      issue(F, plans[nxt], slots[nxt]);
+    } else {
+      cp_async_commit();  // keep one group per item in flight
+    }
+    // wait for the current item's operands (all but the newest cp.async group)
+    cp_async_wait<1>();
+    const Plan& P = plans[cur];
+    if (P.kind != 0 && F.stage_smem && P.nmat > 0) {
+      while (!mbar_try_wait(slots[cur].bar, phase[cur])) {
+      }
+      phase[cur] ^= 1u;
+    }
+    __syncthreads();
+    if (P.kind == 0) {
+      item_s2(F, P.node, red, scratch);
+      cta_release(F.flagS2 + P.node);
+    } else if (P.kind == 1) {
+      item_back(F, P, slots[cur], scratch, red);
+    } else {
+      item_fwd(F, P, slots[cur], scratch, red);
+    }
+    __syncthreads();
+    cur = nxt;
+  }
+  cp_async_wait<0>();
 }
 
 }  // namespace
 
 int fused_smem_bytes(const FusedArgs& F) {
-  return int(sizeof(double) * (F.mat_doubles + kSlots * kSlot + 2 * kFT));
+  return int(sizeof(double) * (2 * (size_t(F.mat_doubles) + F.vec_doubles) + kScratch * kSlot + 2 * kFT));
 }
 
 cudaError_t fused_configure(int smem_bytes) {

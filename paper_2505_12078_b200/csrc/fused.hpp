@@ -18,7 +18,8 @@ struct FusedArgs {
   int* flagS2;                 // [nnl], reset to 0 before each launch
   int* flagB;                  // [nn]
   int* flagF;                  // [nn]
-  int mat_doubles;             // shared-memory matrix staging area (doubles)
+  int mat_doubles;             // shared-memory matrix staging area per ring slot (doubles)
+  int vec_doubles;             // prefetched vector operands per ring slot (doubles)
   int stage_smem;              // 1: TMA bulk staging of node blocks into shared memory
 };
 
