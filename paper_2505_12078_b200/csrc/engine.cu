@@ -166,6 +166,149 @@ void Engine::setup_fused() {
   F.flagS2 = reinterpret_cast<int*>(buf + 8);
   F.flagB = F.flagS2 + nnl;
   F.flagF = F.flagB + nn;
+  // per-item records (prefetch plans + metadata), mirroring the span ids of fused.cu
+  enum { B_HEAD = 0, B_QK, B_ZX, B_ZU, B_EC, B_GD, B_H, B_G, B_HEADN, B_QKN };
+  enum { F_ZX = 0, F_ZU, F_AX, F_AU, F_CV, F_SEG2, F_A, F_QK, F_GD, F_LO, F_HI, F_SEG3, F_AN, F_QKN, F_GND,
+         F_LON, F_HIN, F_SEG1, F_RB };
+  std::vector<ItemRec> recs(size_t(nnl) + 2 * size_t(nn));
+  std::vector<int64_t> hx_off(nn - 1), hu_off(nn - 1), a_off(nn - 1), hn_off(tr.nl()), aN_off(tr.nl());
+  {
+    int64_t sx = 0, su = 0, sa = 0;
+    for (int k = 0; k < nn - 1; ++k) {
+      hx_off[k] = sx, hu_off[k] = su, a_off[k] = sa;
+      sx += pad2(int64_t(soc_.stage[k].px) * nx);
+      su += pad2(int64_t(soc_.stage[k].pu) * nu);
+      sa += soc_.stage[k].px + soc_.stage[k].pu + 2;
+    }
+    int64_t sh = 0, sb = 0;
+    for (int j = 0; j < tr.nl(); ++j) {
+      hn_off[j] = sh, aN_off[j] = sb;
+      sh += pad2(int64_t(soc_.leaf[j].px) * nx);
+      sb += soc_.leaf[j].px + 2;
+    }
+  }
+  auto fill_meta = [&](ItemRec& R, int i) {
+    R.node = i;
+    R.nch = tr.child_count[i];
+    R.c0 = tr.child_first[i];
+    R.anc = tr.anc[i];
+    R.px = i > 0 ? soc_.stage[i - 1].px : 0;
+    R.pu = i > 0 ? soc_.stage[i - 1].pu : 0;
+    R.s2o = i > 0 ? lay_.seg2_off[i - 1] : 0;
+    if (i < nnl) {
+      R.nc = p_.nc[i], R.ny = lay_.y_dim[i], R.s1o = lay_.seg1_off[i], R.yo = lay_.y_off[i];
+    } else {
+      const int j = i - nnl;
+      R.nc = p_.ncN[j], R.pN = soc_.leaf[j].px, R.s3o = lay_.seg3_off[j];
+    }
+  };
+  auto mat = [&](ItemRec& R, int base, int64_t off, int64_t cnt) {
+    R.mbase[R.nmat] = uint8_t(base);
+    R.moff[R.nmat] = off;
+    R.mcnt[R.nmat] = int32_t(cnt);
+    ++R.nmat;
+  };
+  auto vec = [&](ItemRec& R, int id, int base, int64_t off, int64_t cnt) {
+    R.vbase[id] = uint8_t(base);
+    R.voff[id] = off;
+    R.vcnt[id] = int32_t(cnt);
+    R.nspan = std::max(R.nspan, id + 1);
+  };
+  for (int it = 0; it < nnl; ++it) {
+    ItemRec& R = recs[it];
+    std::memset(&R, 0, sizeof(R));
+    R.kind = 0;
+    fill_meta(R, it);
+  }
+  for (int k = 0; k < nn; ++k) {  // backward items: node nn-1 ... 0
+    const int i = nn - 1 - k;
+    ItemRec& R = recs[size_t(nnl) + k];
+    std::memset(&R, 0, sizeof(R));
+    R.kind = 1;
+    fill_meta(R, i);
+    const bool leaf = tr.leaf(i), root = i == 0;
+    if (!root) {
+      const int px = R.px, pu = R.pu;
+      mat(R, FB_HXT, hx_off[i - 1], int64_t(px) * nx);
+      mat(R, FB_HUT, hu_off[i - 1], int64_t(pu) * nu);
+      mat(R, FB_M1T, int64_t(i - 1) * D_.m1_stride, int64_t(m) * nx);
+      vec(R, B_HEAD, FB_ETA, lay_.seg2_off[i - 1], px + pu + 2);
+      vec(R, B_QK, FB_QK, int64_t(i - 1) * m, m);
+    }
+    vec(R, B_ZX, FB_Z, 1 + int64_t(i) * nx, nx);
+    if (!leaf) {
+      mat(R, FB_KT, int64_t(i) * D_.k_stride, int64_t(nx) * nu);
+      mat(R, FB_RINV, int64_t(i) * D_.r_stride, int64_t(nu) * nu);
+      vec(R, B_ZU, FB_Z, lay_.u_base + int64_t(i) * nu, nu);
+      vec(R, B_EC, FB_ETA, lay_.seg1_off[i] + lay_.y_dim[i] + 1, p_.nc[i]);
+      if (D_.g_diag) vec(R, B_GD, FB_GD, int64_t(i) * m, m);
+      vec(R, B_H, FB_H, int64_t(i) * nx, nx);
+      vec(R, B_G, FB_G, int64_t(i) * nu, nu);
+    } else {
+      const int j = i - nnl, pN = R.pN, nc = R.nc;
+      mat(R, FB_HNT, hn_off[j], int64_t(pN) * nx);
+      vec(R, B_EC, FB_ETA, lay_.seg3_off[j], nc);
+      if (D_.gN_diag) vec(R, B_GD, FB_GND, int64_t(j) * nx, nx);
+      vec(R, B_HEADN, FB_ETA, lay_.seg3_off[j] + nc, pN + 2);
+      vec(R, B_QKN, FB_QKN, int64_t(j) * nx, nx);
+    }
+  }
+  for (int c = 0; c < nn; ++c) {  // forward items: node 0 ... nn-1
+    ItemRec& R = recs[size_t(nnl) + nn + c];
+    std::memset(&R, 0, sizeof(R));
+    R.kind = 2;
+    fill_meta(R, c);
+    const bool leaf = tr.leaf(c), root = c == 0;
+    vec(R, F_ZX, FB_Z, 1 + int64_t(c) * nx, nx);
+    if (!leaf) vec(R, F_ZU, FB_Z, lay_.u_base + int64_t(c) * nu, nu);
+    if (!root) {
+      const int px = R.px, pu = R.pu, an = R.anc, p = px + pu;
+      mat(R, FB_M1, int64_t(c - 1) * D_.m1_stride, int64_t(nx) * m);
+      mat(R, FB_HX, hx_off[c - 1], int64_t(px) * nx);
+      mat(R, FB_HU, hu_off[c - 1], int64_t(pu) * nu);
+      vec(R, F_AX, FB_Z, 1 + int64_t(an) * nx, nx);
+      vec(R, F_AU, FB_Z, lay_.u_base + int64_t(an) * nu, nu);
+      vec(R, F_CV, FB_CVEC, int64_t(c - 1) * nx, nx);
+      vec(R, F_SEG2, FB_ETA, lay_.seg2_off[c - 1], p + 2);
+      vec(R, F_A, FB_A, a_off[c - 1], p + 2);
+      vec(R, F_QK, FB_QK, int64_t(c - 1) * m, m);
+    }
+    if (!leaf) {
+      mat(R, FB_K, int64_t(c) * D_.k_stride, int64_t(nu) * nx);
+      const int nc = p_.nc[c], ny = lay_.y_dim[c];
+      const int64_t go = p_.g_off[c];
+      if (D_.g_diag) vec(R, F_GD, FB_GD, int64_t(c) * m, m);
+      vec(R, F_LO, FB_LO, go, nc);
+      vec(R, F_HI, FB_HI, go, nc);
+      if (ny + 1 + nc <= kMaxD) {
+        vec(R, F_SEG1, FB_ETA, lay_.seg1_off[c], ny + 1 + nc);
+        vec(R, F_RB, FB_RB, lay_.y_off[c] - D_.y_base, ny);
+      }
+    } else {
+      const int j = c - nnl, pN = R.pN, nc = R.nc;
+      const int64_t go = p_.gN_off[j];
+      mat(R, FB_HN, hn_off[j], int64_t(pN) * nx);
+      vec(R, F_SEG3, FB_ETA, lay_.seg3_off[j], nc + pN + 2);
+      vec(R, F_AN, FB_AN, aN_off[j], pN + 2);
+      vec(R, F_QKN, FB_QKN, int64_t(j) * nx, nx);
+      if (D_.gN_diag) vec(R, F_GND, FB_GND, int64_t(j) * nx, nx);
+      vec(R, F_LON, FB_LON, go, nc);
+      vec(R, F_HIN, FB_HIN, go, nc);
+    }
+  }
+  ItemRec* drec = nullptr;
+  CK(cudaMalloc(&drec, sizeof(ItemRec) * recs.size()));
+  allocs_.push_back(drec);
+  CK(cudaMemcpyAsync(drec, recs.data(), sizeof(ItemRec) * recs.size(), cudaMemcpyHostToDevice, st_));
+  F.items = drec;
+  const double* bases[FB_COUNT] = {};
+  bases[FB_HXT] = D_.HxT, bases[FB_HUT] = D_.HuT, bases[FB_M1T] = D_.M1T, bases[FB_KT] = D_.KT;
+  bases[FB_RINV] = D_.Rinv, bases[FB_HNT] = D_.HNT, bases[FB_QK] = D_.qk, bases[FB_GD] = D_.gd;
+  bases[FB_H] = D_.h, bases[FB_G] = D_.g, bases[FB_QKN] = D_.qkN, bases[FB_GND] = D_.gNd;
+  bases[FB_M1] = D_.M1, bases[FB_HX] = D_.Hx, bases[FB_HU] = D_.Hu, bases[FB_K] = D_.K, bases[FB_HN] = D_.HN;
+  bases[FB_CVEC] = D_.cvec, bases[FB_A] = D_.a, bases[FB_LO] = D_.lo, bases[FB_HI] = D_.hi, bases[FB_RB] = D_.rb;
+  bases[FB_AN] = D_.aN, bases[FB_LON] = D_.loN, bases[FB_HIN] = D_.hiN;
+  for (int k = 0; k < FB_COUNT; ++k) F.base[k] = bases[k];
 }
 
 Engine::~Engine() {
@@ -750,6 +893,8 @@ void Engine::T(const double* z, const double* eta, double* zo, double* eo) {
     F.eta = eta;
     F.zo = zo;
     F.eo = eo;
+    F.base[FB_Z] = z;
+    F.base[FB_ETA] = eta;
     F.alpha = alpha_;
     CK(cudaMemsetAsync(F.ticket, 0, fused_sync_bytes_, st_));
     launch_T_fused(F, fused_grid_, st_);

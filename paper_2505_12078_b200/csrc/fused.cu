@@ -41,7 +41,6 @@ namespace spock {
 namespace {
 
 constexpr int kFT = 256;   // threads per CTA
-constexpr int kMaxSpans = 24;
 constexpr int kSlot = kMaxD + 8;  // doubles per scratch vector slot
 constexpr int kScratch = 6;       // scratch slots per CTA
 
@@ -172,7 +171,7 @@ __device__ void cta_soc_project(double* v, const double* a, int d, double* red) 
 }
 
 // ---------------------------------------------------------------------------
-// Prefetch plan of one item: matrices (bulk) and independent vector spans.
+// Span ids of the per-item records (host: Engine::setup_fused).
 enum Span : int {
   // backward
   B_HEAD = 0, B_QK, B_ZX, B_ZU, B_EC, B_GD, B_H, B_G, B_HEADN, B_QKN,
@@ -181,163 +180,68 @@ enum Span : int {
   F_HIN, F_SEG1, F_RB
 };
 
-struct Plan {
-  int kind;  // 0 S2, 1 backward, 2 forward
-  int node;
-  int nmat;
-  const double* msrc[6];
-  int mdbl[6];
-  int nspan;
-  const double* vsrc[kMaxSpans];
-  int vn[kMaxSpans];
-};
-
-__device__ void make_plan(const FusedArgs& F, int it, Plan& P) {
-  const Dev& D = F.D;
-  const int nnl = D.nnl, nn = D.nn, nx = D.nx, nu = D.nu, m = nx + nu;
-  P.nmat = 0;
-  P.nspan = 0;
-  for (int k = 0; k < kMaxSpans; ++k) P.vsrc[k] = nullptr, P.vn[k] = 0;
-  auto mat = [&](const double* s, int n) {
-    P.msrc[P.nmat] = s;
-    P.mdbl[P.nmat] = n;
-    ++P.nmat;
-  };
-  auto vec = [&](int id, const double* s, int n) {
-    P.vsrc[id] = s;
-    P.vn[id] = n;
-    P.nspan = max(P.nspan, id + 1);
-  };
-  if (it < nnl) {
-    P.kind = 0;
-    P.node = it;
-    return;
-  }
-  const double* z = F.z;
-  const double* eta = F.eta;
-  if (it < nnl + nn) {
-    const int i = nn - 1 - (it - nnl);
-    P.kind = 1;
-    P.node = i;
-    const bool leaf = D.cc[i] == 0, root = i == 0;
-    if (!root) {
-      const int px = D.px[i - 1], pu = D.pu[i - 1];
-      mat(D.HxT + D.hx_off[i - 1], px * nx);
-      mat(D.HuT + D.hu_off[i - 1], pu * nu);
-      mat(D.M1T + size_t(i - 1) * D.m1_stride, m * nx);
-      vec(B_HEAD, eta + D.s2_off[i - 1], px + pu + 2);
-      vec(B_QK, D.qk + size_t(i - 1) * m, m);
-    }
-    vec(B_ZX, z + 1 + size_t(i) * nx, nx);
-    if (!leaf) {
-      mat(D.KT + size_t(i) * D.k_stride, nx * nu);
-      mat(D.Rinv + size_t(i) * D.r_stride, nu * nu);
-      vec(B_ZU, z + D.u_base + size_t(i) * nu, nu);
-      const int nc = D.s1_nc[i];
-      vec(B_EC, eta + D.s1_off[i] + D.y_dim[i] + 1, nc);
-      if (D.g_diag) vec(B_GD, D.gd + size_t(i) * m, m);
-      vec(B_H, D.h + size_t(i) * nx, nx);
-      vec(B_G, D.g + size_t(i) * nu, nu);
-    } else {
-      const int j = i - nnl, pN = D.pN[j], nc = D.s3_nc[j];
-      mat(D.HNT + D.hn_off[j], pN * nx);
-      vec(B_EC, eta + D.s3_off[j], nc);
-      if (D.gN_diag) vec(B_GD, D.gNd + size_t(j) * nx, nx);
-      vec(B_HEADN, eta + D.s3_off[j] + nc, pN + 2);
-      vec(B_QKN, D.qkN + size_t(j) * nx, nx);
-    }
-    return;
-  }
-  const int c = it - nnl - nn;
-  P.kind = 2;
-  P.node = c;
-  const bool leaf = D.cc[c] == 0, root = c == 0;
-  vec(F_ZX, z + 1 + size_t(c) * nx, nx);
-  if (!leaf) vec(F_ZU, z + D.u_base + size_t(c) * nu, nu);
-  if (!root) {
-    const int px = D.px[c - 1], pu = D.pu[c - 1], an = D.anc[c], p = px + pu;
-    mat(D.M1 + size_t(c - 1) * D.m1_stride, nx * m);
-    mat(D.Hx + D.hx_off[c - 1], px * nx);
-    mat(D.Hu + D.hu_off[c - 1], pu * nu);
-    vec(F_AX, z + 1 + size_t(an) * nx, nx);
-    vec(F_AU, z + D.u_base + size_t(an) * nu, nu);
-    vec(F_CV, D.cvec + size_t(c - 1) * nx, nx);
-    vec(F_SEG2, eta + D.s2_off[c - 1], p + 2);
-    vec(F_A, D.a + D.a_off[c - 1], p + 2);
-    vec(F_QK, D.qk + size_t(c - 1) * m, m);
-  }
-  if (!leaf) {
-    mat(D.K + size_t(c) * D.k_stride, nu * nx);
-    const int nc = D.s1_nc[c], ny = D.y_dim[c];
-    if (D.g_diag) vec(F_GD, D.gd + size_t(c) * m, m);
-    vec(F_LO, D.lo + D.g_off[c], nc);
-    vec(F_HI, D.hi + D.g_off[c], nc);
-    if (ny + 1 + nc <= kMaxD) {
-      vec(F_SEG1, eta + D.s1_off[c], ny + 1 + nc);
-      vec(F_RB, D.rb + (D.y_off[c] - D.y_base), ny);
-    }
-  } else {
-    const int j = c - nnl, pN = D.pN[j], nc = D.s3_nc[j];
-    mat(D.HN + D.hn_off[j], pN * nx);
-    vec(F_SEG3, eta + D.s3_off[j], nc + pN + 2);
-    vec(F_AN, D.aN + D.aN_off[j], pN + 2);
-    vec(F_QKN, D.qkN + size_t(j) * nx, nx);
-    if (D.gN_diag) vec(F_GND, D.gNd + size_t(j) * nx, nx);
-    vec(F_LON, D.loN + D.gN_off[j], nc);
-    vec(F_HIN, D.hiN + D.gN_off[j], nc);
-  }
-}
-
 struct Slot {
   double* mat;
   double* vec;
   uint64_t* bar;
-  int voff[kMaxSpans];  // span offsets in vec
-  const double* mp[6];  // staged (or global) matrix pointers
+  int voff[kRecSpans];      // span offsets in vec
+  const double* mp[kRecMats];  // staged (or global) matrix pointers
 };
 
-// issue the prefetch of an item into a slot; every thread takes part (vector
-// spans by cp.async), thread 0 issues the bulk copies; commits one cp.async
-// group per item
-__device__ void issue(const FusedArgs& F, const Plan& P, Slot& S) {
+// cooperative load of one 512-byte item record into shared memory
+__device__ __forceinline__ void load_rec(const FusedArgs& F, int it, ItemRec* dst) {
+  const int t = threadIdx.x;
+  constexpr int W = int(sizeof(ItemRec) / 16);
+  if (t < W) reinterpret_cast<int4*>(dst)[t] = __ldg(reinterpret_cast<const int4*>(F.items + it) + t);
+}
+
+// issue the prefetch of an item into a slot: vector spans by cp.async (all
+// threads, one commit group per item), matrices by TMA bulk copies (thread 0)
+__device__ void issue(const FusedArgs& F, const ItemRec& R, Slot& S) {
   const int t = threadIdx.x;
   int off = 0;
-  for (int k = 0; k < P.nspan; ++k) {
+  for (int k = 0; k < R.nspan; ++k) {
+    const int n = R.vcnt[k];
+    if (n > 0) {
+      const double* src = F.base[R.vbase[k]] + R.voff[k];
+      double* dst = S.vec + off;
+      for (int e = t; e < n; e += kFT) cp_async8(dst + e, src + e);
+    }
     if (t == 0) S.voff[k] = off;
-    off += (P.vn[k] + 1) & ~1;
-  }
-  off = 0;
-  for (int k = 0; k < P.nspan; ++k) {
-    const double* src = P.vsrc[k];
-    double* dst = S.vec + off;
-    for (int e = t; e < P.vn[k]; e += kFT) cp_async8(dst + e, src + e);
-    off += (P.vn[k] + 1) & ~1;
+    off += (n + 1) & ~1;
   }
   cp_async_commit();
   if (t == 0) {
-    if (F.stage_smem && P.nmat > 0) {
+    const bool stage = F.stage_smem && R.nmat > 0;
+    if (stage) {
       fence_proxy_async();
       uint32_t total = 0;
-      for (int k = 0; k < P.nmat; ++k) total += uint32_t((P.mdbl[k] + 1) & ~1) * 8u;
+      for (int k = 0; k < R.nmat; ++k) total += uint32_t((R.mcnt[k] + 1) & ~1) * 8u;
       if (total)
         mbar_expect_tx(S.bar, total);
       else
         mbar_arrive(S.bar);
-      int mo = 0;
-      for (int k = 0; k < P.nmat; ++k) {
-        if (P.mdbl[k] <= 0) {
-          S.mp[k] = P.msrc[k];
-          continue;
-        }
-        const int padded = (P.mdbl[k] + 1) & ~1;
-        bulk_g2s(S.mat + mo, P.msrc[k], uint32_t(padded) * 8u, S.bar);
-        S.mp[k] = S.mat + mo;
-        mo += padded;
+    }
+    int mo = 0;
+    for (int k = 0; k < R.nmat; ++k) {
+      const double* src = F.base[R.mbase[k]] + R.moff[k];
+      if (!stage || R.mcnt[k] <= 0) {
+        S.mp[k] = src;
+        continue;
       }
-    } else {
-      for (int k = 0; k < P.nmat; ++k) S.mp[k] = P.msrc[k];
+      const int padded = (R.mcnt[k] + 1) & ~1;
+      bulk_g2s(S.mat + mo, src, uint32_t(padded) * 8u, S.bar);
+      S.mp[k] = S.mat + mo;
+      mo += padded;
     }
   }
+}
+
+// wait on up to kFT flags in parallel (one thread each), then CTA barrier
+__device__ __forceinline__ void wait_flags_par(const int* f, int n) {
+  const int t = threadIdx.x;
+  for (int k = t; k < n; k += kFT) wait_flag(f + k);
+  __syncthreads();
 }
 
 // ---------------------------------------------------------------------------
@@ -427,11 +331,11 @@ __device__ void item_s2(const FusedArgs& F, int i, double* red, double* vec) {
   __syncthreads();
 }
 
-__device__ void item_back(const FusedArgs& F, const Plan& P, const Slot& S, double* sc_, double* red) {
+__device__ void item_back(const FusedArgs& F, const ItemRec& P, const Slot& S, double* sc_, double* red) {
   const Dev& D = F.D;
   const int i = P.node;
   const int t = threadIdx.x, nx = D.nx, nu = D.nu, m = nx + nu;
-  const bool leaf = D.cc[i] == 0, root = i == 0;
+  const bool leaf = P.nch == 0, root = i == 0;
   const double al = F.alpha;
   const double* V = S.vec;
   auto sp = [&](int id) { return V + S.voff[id]; };
@@ -439,8 +343,7 @@ __device__ void item_back(const FusedArgs& F, const Plan& P, const Slot& S, doub
   double* q = gx + kSlot;     // q (nx)
   double* tv = q + kSlot;     // scratch (m)
   double* rhs = tv + kSlot;   // scratch (m)
-  int px = 0, pu = 0;
-  if (!root) px = D.px[i - 1], pu = D.pu[i - 1];
+  const int px = P.px, pu = P.pu;
   int mk = 0;
   const double* HxT = root ? nullptr : S.mp[mk++];
   const double* HuT = root ? nullptr : S.mp[mk++];
@@ -450,7 +353,7 @@ __device__ void item_back(const FusedArgs& F, const Plan& P, const Slot& S, doub
   const double* HNT = leaf ? S.mp[mk++] : nullptr;
   // ---- own G' ec (+ terminal SOC term for leaves); independent of children
   if (!leaf) {
-    const int nc = D.s1_nc[i];
+    const int nc = P.nc;
     const double* ec = sp(B_EC);
     if (D.g_diag) {
       const double* gd = sp(B_GD);
@@ -461,7 +364,7 @@ __device__ void item_back(const FusedArgs& F, const Plan& P, const Slot& S, doub
       cta_gemv(D.GuT + D.g_off[i] * nu, nu, nc, nu, ec, gx + nx, false, red);
     }
   } else {
-    const int j = i - D.nnl, nc = D.s3_nc[j], pN = D.pN[j];
+    const int j = i - D.nnl, nc = P.nc, pN = P.pN;
     const double* ec = sp(B_EC);
     if (D.gN_diag) {
       const double* gd = sp(B_GD);
@@ -490,10 +393,8 @@ __device__ void item_back(const FusedArgs& F, const Plan& P, const Slot& S, doub
   }
   if (!leaf) {
     // ---- children (flags), then q and d
-    const int c0 = D.cf[i], nch = D.cc[i];
-    if (t == 0)
-      for (int c = 0; c < nch; ++c) wait_flag(F.flagB + c0 + c);
-    __syncthreads();
+    const int c0 = P.c0, nch = P.nch;
+    wait_flags_par(F.flagB + c0, nch);
     const double* zx = sp(B_ZX);
     const double* zu = sp(B_ZU);
     const double* h = sp(B_H);
@@ -526,17 +427,17 @@ __device__ void item_back(const FusedArgs& F, const Plan& P, const Slot& S, doub
     double* T12 = D.T12 + size_t(i - 1) * m;
     for (int r = t; r < m; r += kFT) T12[r] = tv[r];
   } else if (t == 0) {
-    const double sc = F.eta[D.s1_off[0] + D.y_dim[0]];
+    const double sc = F.eta[P.s1o + P.ny];
     F.zo[0] = F.z[0] - al * sc - al;  // CP primal step on s0 (solver.cpp:153-154)
   }
   cta_release(F.flagB + i);
 }
 
-__device__ void item_fwd(const FusedArgs& F, const Plan& P, const Slot& S, double* sc_, double* red) {
+__device__ void item_fwd(const FusedArgs& F, const ItemRec& P, const Slot& S, double* sc_, double* red) {
   const Dev& D = F.D;
   const int c = P.node;
   const int t = threadIdx.x, nx = D.nx, nu = D.nu, m = nx + nu;
-  const bool leaf = D.cc[c] == 0, root = c == 0;
+  const bool leaf = P.nch == 0, root = c == 0;
   const double al = F.alpha;
   const double* z = F.z;
   const double* eta = F.eta;
@@ -549,17 +450,18 @@ __device__ void item_fwd(const FusedArgs& F, const Plan& P, const Slot& S, doubl
   double* ahat = xn + kSlot;   // anc (x^, u^)
   double* val = ahat + kSlot;  // segment values
   double* pv = val + kSlot;    // p / alpha
-  int px = 0, pu = 0;
-  if (!root) px = D.px[c - 1], pu = D.pu[c - 1];
+  const int px = P.px, pu = P.pu;
   int mk = 0;
   const double* M1 = root ? nullptr : S.mp[mk++];
   const double* Hx = root ? nullptr : S.mp[mk++];
   const double* Hu = root ? nullptr : S.mp[mk++];
   const double* K = leaf ? nullptr : S.mp[mk++];
   const double* HN = leaf ? S.mp[mk++] : nullptr;
-  const int an = root ? 0 : D.anc[c];
+  const int an = root ? 0 : P.anc;
   // ---- parent forward (root: own backward)
   if (t == 0) wait_flag(root ? F.flagB : F.flagF + an);
+  else if (t == 32 && !leaf) wait_flag(F.flagS2 + c);
+  else if (t == 64 && !root) wait_flag(F.flagS2 + an);
   __syncthreads();
   double dself = 0.0;
   if (!leaf && t < nu) dself = ldcg(D.dvec + size_t(c) * nu + t);
@@ -603,14 +505,10 @@ __device__ void item_fwd(const FusedArgs& F, const Plan& P, const Slot& S, doubl
     for (int r = t; r < (leaf ? nx : m); r += kFT) xn[r] = 2.0 * xn[r] - (r < nx ? zx[r] : zu[r - nx]);
   }
   const double* hat = xn;
-  if (t == 0) {
-    if (!leaf) wait_flag(F.flagS2 + c);
-    if (!root) wait_flag(F.flagS2 + an);
-  }
   __syncthreads();
   auto hatv = [&](int idx) { return 2.0 * ldcg(zo + idx) - z[idx]; };
   if (!root) {  // stage-cost SOC block of (x_anc, u_anc, tau_c)
-    const int k = c - 1, p = px + pu, o2 = D.s2_off[k];
+    const int k = c - 1, p = px + pu, o2 = P.s2o;
     const double* qk = sp(F_QK);
     double part = 0.0;
     for (int r = t; r < m; r += kFT) part += qk[r] * ahat[r];
@@ -635,8 +533,8 @@ __device__ void item_fwd(const FusedArgs& F, const Plan& P, const Slot& S, doubl
     __syncthreads();
   }
   if (!leaf) {  // y-copy rows (dual cone), risk scalar (R+), constraint rows (box)
-    const int ny = D.y_dim[c], yo = D.y_off[c], so = D.s1_off[c], nc = D.s1_nc[c];
-    const bool pre = P.vn[F_SEG1] > 0;
+    const int ny = P.ny, yo = P.yo, so = P.s1o, nc = P.nc;
+    const bool pre = P.vcnt[F_SEG1] > 0;
     const double* seg1 = pre ? sp(F_SEG1) : eta + so;
     const double* rb = pre ? sp(F_RB) : D.rb + (yo - D.y_base);
     const int nn0 = D.yc_nonneg[c];
@@ -709,7 +607,7 @@ __device__ void item_fwd(const FusedArgs& F, const Plan& P, const Slot& S, doubl
     }
     __syncthreads();
   } else {  // leaf: G_N x^ (box) and the terminal SOC block of (x, s)
-    const int j = c - D.nnl, nc = D.s3_nc[j], eo3 = D.s3_off[j], p = D.pN[j];
+    const int j = c - D.nnl, nc = P.nc, eo3 = P.s3o, p = P.pN;
     const double* seg3 = sp(F_SEG3);
     if (D.gN_diag) {
       const double* gd = sp(F_GND);
@@ -754,7 +652,7 @@ __global__ void __launch_bounds__(kFT, 1) k_T_fused(FusedArgs F) {
   __shared__ uint64_t bars[2];
   __shared__ Slot slots[2];
   __shared__ int tk[2];
-  __shared__ Plan plans[2];
+  __shared__ ItemRec recs[2];
   const int t = threadIdx.x;
   double* scratch = dsm + 2 * (size_t(F.mat_doubles) + F.vec_doubles);
   double* red = scratch + kScratch * kSlot;
@@ -767,17 +665,16 @@ __global__ void __launch_bounds__(kFT, 1) k_T_fused(FusedArgs F) {
       slots[s].vec = slots[s].mat + F.mat_doubles;
       slots[s].bar = &bars[s];
     }
+    tk[0] = int(atomicAdd(F.ticket, 1ull));
   }
   uint32_t phase[2] = {0u, 0u};
-  const int nnl = F.D.nnl, nn = F.D.nn, total = nnl + 2 * nn;
-  // first item
-  if (t == 0) tk[0] = int(atomicAdd(F.ticket, 1ull));
+  const int total = F.D.nnl + 2 * F.D.nn;
   __syncthreads();
   int cur = 0;
   if (tk[0] < total) {
-    if (t == 0) make_plan(F, tk[0], plans[0]);
+    load_rec(F, tk[0], &recs[0]);
     __syncthreads();
-    issue(F, plans[0], slots[0]);
+    issue(F, recs[0], slots[0]);
   } else {
     cp_async_commit();
   }
@@ -788,16 +685,17 @@ __global__ void __launch_bounds__(kFT, 1) k_T_fused(FusedArgs F) {
     // take and prefetch the next item into the other slot
     if (t == 0) tk[nxt] = int(atomicAdd(F.ticket, 1ull));
     __syncthreads();
-    if (tk[nxt] < total) {
-      if (t == 0) make_plan(F, tk[nxt], plans[nxt]);
+    const int itn = tk[nxt];
+    if (itn < total) {
+      load_rec(F, itn, &recs[nxt]);
       __syncthreads();
-      issue(F, plans[nxt], slots[nxt]);
+      issue(F, recs[nxt], slots[nxt]);
     } else {
       cp_async_commit();  // keep one group per item in flight
     }
     // wait for the current item's operands (all but the newest cp.async group)
     cp_async_wait<1>();
-    const Plan& P = plans[cur];
+    const ItemRec& P = recs[cur];
     if (P.kind != 0 && F.stage_smem && P.nmat > 0) {
       while (!mbar_try_wait(slots[cur].bar, phase[cur])) {
       }

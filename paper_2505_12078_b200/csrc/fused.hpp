@@ -7,6 +7,30 @@
 
 namespace spock {
 
+// Operand base arrays of the per-item records (offsets are relative to these).
+enum FusedBase : int {
+  FB_Z = 0, FB_ETA, FB_HXT, FB_HUT, FB_M1T, FB_KT, FB_RINV, FB_HNT, FB_QK, FB_GD, FB_H, FB_G, FB_QKN, FB_GND,
+  FB_M1, FB_HX, FB_HU, FB_K, FB_HN, FB_CVEC, FB_A, FB_LO, FB_HI, FB_RB, FB_AN, FB_LON, FB_HIN, FB_COUNT
+};
+constexpr int kRecMats = 6;
+constexpr int kRecSpans = 20;
+
+// Precomputed per-item prefetch plan and metadata (built once on the host;
+// one cooperative 512-byte load per item on the device).
+struct alignas(16) ItemRec {
+  int32_t kind, node, nmat, nspan;
+  int32_t px, pu, pN, nc, ny, nch, c0, anc;
+  int32_t s1o, s2o, s3o, yo;
+  int64_t moff[kRecMats];
+  int32_t mcnt[kRecMats];
+  int64_t voff[kRecSpans];
+  int32_t vcnt[kRecSpans];
+  uint8_t mbase[kRecMats];
+  uint8_t vbase[kRecSpans];
+  uint8_t pad_[6];
+};
+static_assert(sizeof(ItemRec) <= 512, "ItemRec must fit the 512-byte cooperative load");
+
 struct FusedArgs {
   Dev D;
   const double* z;
@@ -21,6 +45,8 @@ struct FusedArgs {
   int mat_doubles;             // shared-memory matrix staging area per ring slot (doubles)
   int vec_doubles;             // prefetched vector operands per ring slot (doubles)
   int stage_smem;              // 1: TMA bulk staging of node blocks into shared memory
+  const ItemRec* items;        // [nnl + 2 nn]
+  const double* base[FB_COUNT];
 };
 
 int fused_smem_bytes(const FusedArgs& F);
