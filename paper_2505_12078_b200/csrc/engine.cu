@@ -143,7 +143,8 @@ void Engine::setup_fused() {
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   CK(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  if (fused_smem_bytes(F) + 8192 > smem_optin) {  // blocks too large to stage: stream from L2/HBM
+  const char* ns = std::getenv("SPOCK_FUSED_NOSTAGE");
+  if ((ns && ns[0] == '1') || fused_smem_bytes(F) + 8192 > smem_optin) {  // stream blocks from L2/HBM
     F.stage_smem = 0;
     F.mat_doubles = 0;
   }
@@ -156,7 +157,9 @@ void Engine::setup_fused() {
   int occ = 0;
   F.D = D_;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fused_kernel_ptr(), 256, bytes));
-  fused_grid_ = std::max(1, std::min(occ, 2)) * sms;
+  int occ_cap = 2;
+  if (const char* oc = std::getenv("SPOCK_FUSED_OCC")) occ_cap = std::max(1, std::atoi(oc));
+  fused_grid_ = std::max(1, std::min(occ, occ_cap)) * sms;
   const int total = nnl + 2 * nn;
   fused_grid_ = std::min(fused_grid_, total);
   const size_t fb = 8 + sizeof(int) * size_t(nnl + 2 * nn);
