@@ -106,14 +106,24 @@ void Engine::setup_fused() {
   if (!fused_ok_) return;
   // largest per-item set of staged blocks and prefetched vector spans (even
   // doubles each), mirroring make_plan in fused.cu
+  auto knob = [](const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return (v && v[0]) ? std::atoi(v) : dflt;
+  };
+  // defaults: wide trees stream more bytes per SM with 128-thread CTAs and
+  // critical-only staging; narrow trees favour a 256-thread ring
+  const bool wide = nn >= 4096;
+  const int sall = knob("SPOCK_FUSED_STAGEALL", wide ? 0 : 1);
+  const int nslots = knob("SPOCK_FUSED_SLOTS", wide ? 1 : 2);
+  const int threads = knob("SPOCK_FUSED_FT", wide ? 128 : 256) == 128 ? 128 : 256;
   int64_t mx = 0, vx = 0;
   for (int i = 0; i < nn; ++i) {
     const bool leaf = tr.leaf(i), root = i == 0;
     int64_t b = 0, f = 0, vb = pad2(nx), vf = pad2(nx);
     if (!root) {
       const int px = soc_.stage[i - 1].px, pu = soc_.stage[i - 1].pu, p = px + pu;
-      b += pad2(int64_t(px) * nx) + pad2(int64_t(pu) * nu) + pad2(int64_t(m) * nx);
-      f += pad2(int64_t(nx) * m) + pad2(int64_t(px) * nx) + pad2(int64_t(pu) * nu);
+      b += (sall ? pad2(int64_t(px) * nx) + pad2(int64_t(pu) * nu) : 0) + pad2(int64_t(m) * nx);
+      f += pad2(int64_t(nx) * m) + (sall ? pad2(int64_t(px) * nx) + pad2(int64_t(pu) * nu) : 0);
       vb += pad2(p + 2) + pad2(m);
       vf += pad2(nx) + pad2(nu) + pad2(nx) + 2 * pad2(p + 2) + pad2(m);
     }
@@ -126,8 +136,8 @@ void Engine::setup_fused() {
       if (ny + 1 + nc <= kMaxD) vf += pad2(ny + 1 + nc) + pad2(ny);
     } else {
       const int j = i - tr.nnl(), pN = soc_.leaf[j].px, nc = p_.ncN[j];
-      b += pad2(int64_t(pN) * nx);
-      f += pad2(int64_t(pN) * nx);
+      b += sall ? pad2(int64_t(pN) * nx) : 0;
+      f += sall ? pad2(int64_t(pN) * nx) : 0;
       vb += pad2(nc) + (D_.gN_diag ? pad2(nx) : 0) + pad2(pN + 2) + pad2(nx);
       vf += pad2(nc + pN + 2) + pad2(pN + 2) + pad2(nx) + (D_.gN_diag ? pad2(nx) : 0) + 2 * pad2(nc);
     }
@@ -137,6 +147,9 @@ void Engine::setup_fused() {
   FusedArgs& F = fargs_;
   F = FusedArgs{};
   F.stage_smem = 1;
+  F.stage_all = sall;
+  F.nslots = nslots > 1 ? 2 : 1;
+  F.threads = threads;
   F.mat_doubles = int(mx);
   F.vec_doubles = int(vx);
   int dev = 0, sms = 148, smem_optin = 0;
@@ -153,12 +166,11 @@ void Engine::setup_fused() {
     return;
   }
   const int bytes = fused_smem_bytes(F);
-  CK(fused_configure(bytes));
+  CK(fused_configure(bytes, F.threads));
   int occ = 0;
   F.D = D_;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fused_kernel_ptr(), 256, bytes));
-  int occ_cap = 2;
-  if (const char* oc = std::getenv("SPOCK_FUSED_OCC")) occ_cap = std::max(1, std::atoi(oc));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fused_kernel_ptr(F.threads), F.threads, bytes));
+  const int occ_cap = std::max(1, knob("SPOCK_FUSED_OCC", 4));
   fused_grid_ = std::max(1, std::min(occ, occ_cap)) * sms;
   const int total = nnl + 2 * nn;
   fused_grid_ = std::min(fused_grid_, total);
@@ -205,7 +217,8 @@ void Engine::setup_fused() {
       R.nc = p_.ncN[j], R.pN = soc_.leaf[j].px, R.s3o = lay_.seg3_off[j];
     }
   };
-  auto mat = [&](ItemRec& R, int base, int64_t off, int64_t cnt) {
+  auto mat = [&](ItemRec& R, int base, int64_t off, int64_t cnt, bool crit) {
+    if (crit) R.mcrit |= uint8_t(1u << R.nmat);
     R.mbase[R.nmat] = uint8_t(base);
     R.moff[R.nmat] = off;
     R.mcnt[R.nmat] = int32_t(cnt);
@@ -232,16 +245,16 @@ void Engine::setup_fused() {
     const bool leaf = tr.leaf(i), root = i == 0;
     if (!root) {
       const int px = R.px, pu = R.pu;
-      mat(R, FB_HXT, hx_off[i - 1], int64_t(px) * nx);
-      mat(R, FB_HUT, hu_off[i - 1], int64_t(pu) * nu);
-      mat(R, FB_M1T, int64_t(i - 1) * D_.m1_stride, int64_t(m) * nx);
+      mat(R, FB_HXT, hx_off[i - 1], int64_t(px) * nx, false);
+      mat(R, FB_HUT, hu_off[i - 1], int64_t(pu) * nu, false);
+      mat(R, FB_M1T, int64_t(i - 1) * D_.m1_stride, int64_t(m) * nx, true);
       vec(R, B_HEAD, FB_ETA, lay_.seg2_off[i - 1], px + pu + 2);
       vec(R, B_QK, FB_QK, int64_t(i - 1) * m, m);
     }
     vec(R, B_ZX, FB_Z, 1 + int64_t(i) * nx, nx);
     if (!leaf) {
-      mat(R, FB_KT, int64_t(i) * D_.k_stride, int64_t(nx) * nu);
-      mat(R, FB_RINV, int64_t(i) * D_.r_stride, int64_t(nu) * nu);
+      mat(R, FB_KT, int64_t(i) * D_.k_stride, int64_t(nx) * nu, true);
+      mat(R, FB_RINV, int64_t(i) * D_.r_stride, int64_t(nu) * nu, true);
       vec(R, B_ZU, FB_Z, lay_.u_base + int64_t(i) * nu, nu);
       vec(R, B_EC, FB_ETA, lay_.seg1_off[i] + lay_.y_dim[i] + 1, p_.nc[i]);
       if (D_.g_diag) vec(R, B_GD, FB_GD, int64_t(i) * m, m);
@@ -249,7 +262,7 @@ void Engine::setup_fused() {
       vec(R, B_G, FB_G, int64_t(i) * nu, nu);
     } else {
       const int j = i - nnl, pN = R.pN, nc = R.nc;
-      mat(R, FB_HNT, hn_off[j], int64_t(pN) * nx);
+      mat(R, FB_HNT, hn_off[j], int64_t(pN) * nx, false);
       vec(R, B_EC, FB_ETA, lay_.seg3_off[j], nc);
       if (D_.gN_diag) vec(R, B_GD, FB_GND, int64_t(j) * nx, nx);
       vec(R, B_HEADN, FB_ETA, lay_.seg3_off[j] + nc, pN + 2);
@@ -266,9 +279,9 @@ void Engine::setup_fused() {
     if (!leaf) vec(R, F_ZU, FB_Z, lay_.u_base + int64_t(c) * nu, nu);
     if (!root) {
       const int px = R.px, pu = R.pu, an = R.anc, p = px + pu;
-      mat(R, FB_M1, int64_t(c - 1) * D_.m1_stride, int64_t(nx) * m);
-      mat(R, FB_HX, hx_off[c - 1], int64_t(px) * nx);
-      mat(R, FB_HU, hu_off[c - 1], int64_t(pu) * nu);
+      mat(R, FB_M1, int64_t(c - 1) * D_.m1_stride, int64_t(nx) * m, true);
+      mat(R, FB_HX, hx_off[c - 1], int64_t(px) * nx, false);
+      mat(R, FB_HU, hu_off[c - 1], int64_t(pu) * nu, false);
       vec(R, F_AX, FB_Z, 1 + int64_t(an) * nx, nx);
       vec(R, F_AU, FB_Z, lay_.u_base + int64_t(an) * nu, nu);
       vec(R, F_CV, FB_CVEC, int64_t(c - 1) * nx, nx);
@@ -277,7 +290,7 @@ void Engine::setup_fused() {
       vec(R, F_QK, FB_QK, int64_t(c - 1) * m, m);
     }
     if (!leaf) {
-      mat(R, FB_K, int64_t(c) * D_.k_stride, int64_t(nu) * nx);
+      mat(R, FB_K, int64_t(c) * D_.k_stride, int64_t(nu) * nx, true);
       const int nc = p_.nc[c], ny = lay_.y_dim[c];
       const int64_t go = p_.g_off[c];
       if (D_.g_diag) vec(R, F_GD, FB_GD, int64_t(c) * m, m);
@@ -290,7 +303,7 @@ void Engine::setup_fused() {
     } else {
       const int j = c - nnl, pN = R.pN, nc = R.nc;
       const int64_t go = p_.gN_off[j];
-      mat(R, FB_HN, hn_off[j], int64_t(pN) * nx);
+      mat(R, FB_HN, hn_off[j], int64_t(pN) * nx, false);
       vec(R, F_SEG3, FB_ETA, lay_.seg3_off[j], nc + pN + 2);
       vec(R, F_AN, FB_AN, aN_off[j], pN + 2);
       vec(R, F_QKN, FB_QKN, int64_t(j) * nx, nx);

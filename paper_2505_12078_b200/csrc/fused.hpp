@@ -27,7 +27,8 @@ struct alignas(16) ItemRec {
   int32_t vcnt[kRecSpans];
   uint8_t mbase[kRecMats];
   uint8_t vbase[kRecSpans];
-  uint8_t pad_[6];
+  uint8_t mcrit;  // bit k: matrix k is on the critical path (staged in critical-only mode)
+  uint8_t pad_[5];
 };
 static_assert(sizeof(ItemRec) <= 512, "ItemRec must fit the 512-byte cooperative load");
 
@@ -45,13 +46,16 @@ struct FusedArgs {
   int mat_doubles;             // shared-memory matrix staging area per ring slot (doubles)
   int vec_doubles;             // prefetched vector operands per ring slot (doubles)
   int stage_smem;              // 1: TMA bulk staging of node blocks into shared memory
+  int stage_all;               // 1: stage every block; 0: only the critical-path blocks
+  int nslots;                  // 1 or 2 (prefetch ring depth)
+  int threads;                 // 128 or 256 threads per CTA
   const ItemRec* items;        // [nnl + 2 nn]
   const double* base[FB_COUNT];
 };
 
 int fused_smem_bytes(const FusedArgs& F);
-cudaError_t fused_configure(int smem_bytes);
+cudaError_t fused_configure(int smem_bytes, int threads);
 void launch_T_fused(const FusedArgs& F, int grid, cudaStream_t st);
-const void* fused_kernel_ptr();
+const void* fused_kernel_ptr(int threads);
 
 }  // namespace spock

@@ -1,0 +1,701 @@
+// Device code of the fused T kernel, instantiated per CTA size by fused.cu
+// (FUSED_FT threads per CTA).  See fused.cu for the design notes.
+
+constexpr int kFT = FUSED_FT;  // threads per CTA
+constexpr int kSlot = kMaxD + 8;  // doubles per scratch vector slot
+constexpr int kScratch = 6;       // scratch slots per CTA
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// loads of data produced by other CTAs in this launch: L2 only (no stale L1)
+__device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
+
+__device__ void wait_flag(const int* f) {
+  while (ld_acquire(f) < 1) __nanosleep(20);
+}
+// CTA barrier, then one fenced release store (CUTLASS GenericBarrier pattern)
+__device__ __forceinline__ void cta_release(int* flag) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    st_release(flag, 1);
+  }
+}
+
+// y[r] = (acc ? y[r] : 0) + sum_c A[r + c*lda] x[c], r < m <= kFT; all threads
+// participate (column slices reduced in fixed order => deterministic).
+__device__ void cta_gemv(const double* A, int m, int n, int lda, const double* x, double* y, bool acc,
+                         double* red) {
+  const int t = threadIdx.x;
+  if (m <= 0) return;
+  if (m > kFT) {  // tall: one thread per row, rows strided by the CTA size
+    for (int r = t; r < m; r += kFT) {
+      double v = acc ? y[r] : 0.0;
+      for (int c = 0; c < n; ++c) v = fma(A[r + size_t(c) * lda], x[c], v);
+      y[r] = v;
+    }
+    __syncthreads();
+    return;
+  }
+  const int slices = max(1, kFT / m);
+  const int r = t % m, s = t / m;
+  double v = 0.0;
+  if (s < slices && n > 0) {
+    int c = s;
+    for (; c + 3 * slices < n; c += 4 * slices) {
+      v = fma(A[r + size_t(c) * lda], x[c], v);
+      v = fma(A[r + size_t(c + slices) * lda], x[c + slices], v);
+      v = fma(A[r + size_t(c + 2 * slices) * lda], x[c + 2 * slices], v);
+      v = fma(A[r + size_t(c + 3 * slices) * lda], x[c + 3 * slices], v);
+    }
+    for (; c < n; c += slices) v = fma(A[r + size_t(c) * lda], x[c], v);
+  }
+  if (t < m * slices) red[t] = v;
+  __syncthreads();
+  if (t < m) {
+    double o = acc ? y[t] : 0.0;
+    for (int j = 0; j < slices; ++j) o += red[t + j * m];
+    y[t] = o;
+  }
+  __syncthreads();
+}
+
+__device__ double cta_sum(double v, double* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < kFT / 32; ++k) s += red[k];
+  __syncthreads();
+  return s;
+}
+
+// v <- a + Pi_SOC(v - a), axis last, in place (projections.cpp:11-37)
+__device__ void cta_soc_project(double* v, const double* a, int d, double* red) {
+  const int t = threadIdx.x;
+  double s = 0.0;
+  for (int r = t; r < d; r += kFT) {
+    v[r] -= a[r];
+    if (r < d - 1) s += v[r] * v[r];
+  }
+  const double hn = sqrt(cta_sum(s, red));
+  const double tt = v[d - 1];
+  if (hn <= tt) {
+  } else if (hn <= -tt) {
+    for (int r = t; r < d; r += kFT) v[r] = 0.0;
+  } else {
+    const double f = (hn + tt) / (2.0 * hn);
+    for (int r = t; r < d - 1; r += kFT) v[r] *= f;
+    if (t == 0) v[d - 1] = 0.5 * (hn + tt);
+  }
+  __syncthreads();
+  for (int r = t; r < d; r += kFT) v[r] += a[r];
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// Span ids of the per-item records (host: Engine::setup_fused).
+enum Span : int {
+  // backward
+  B_HEAD = 0, B_QK, B_ZX, B_ZU, B_EC, B_GD, B_H, B_G, B_HEADN, B_QKN,
+  // forward
+  F_ZX = 0, F_ZU, F_AX, F_AU, F_CV, F_SEG2, F_A, F_QK, F_GD, F_LO, F_HI, F_SEG3, F_AN, F_QKN, F_GND, F_LON,
+  F_HIN, F_SEG1, F_RB
+};
+
+struct Slot {
+  double* mat;
+  double* vec;
+  uint64_t* bar;
+  int voff[kRecSpans];      // span offsets in vec
+  const double* mp[kRecMats];  // staged (or global) matrix pointers
+};
+
+// cooperative load of one 512-byte item record into shared memory
+__device__ __forceinline__ void load_rec(const FusedArgs& F, int it, ItemRec* dst) {
+  const int t = threadIdx.x;
+  constexpr int W = int(sizeof(ItemRec) / 16);
+  if (t < W) reinterpret_cast<int4*>(dst)[t] = __ldg(reinterpret_cast<const int4*>(F.items + it) + t);
+}
+
+// issue the prefetch of an item into a slot: vector spans by cp.async (all
+// threads, one commit group per item), matrices by TMA bulk copies (thread 0)
+__device__ void issue(const FusedArgs& F, const ItemRec& R, Slot& S) {
+  const int t = threadIdx.x;
+  int off = 0;
+  for (int k = 0; k < R.nspan; ++k) {
+    const int n = R.vcnt[k];
+    if (n > 0) {
+      const double* src = F.base[R.vbase[k]] + R.voff[k];
+      double* dst = S.vec + off;
+      for (int e = t; e < n; e += kFT) cp_async8(dst + e, src + e);
+    }
+    if (t == 0) S.voff[k] = off;
+    off += (n + 1) & ~1;
+  }
+  cp_async_commit();
+  if (t == 0) {
+    const bool stage = F.stage_smem && R.nmat > 0;
+    if (stage) {
+      fence_proxy_async();
+      uint32_t total = 0;
+      for (int k = 0; k < R.nmat; ++k)
+        if (F.stage_all || (R.mcrit & (1 << k))) total += uint32_t((R.mcnt[k] + 1) & ~1) * 8u;
+      if (total)
+        mbar_expect_tx(S.bar, total);
+      else
+        mbar_arrive(S.bar);
+    }
+    int mo = 0;
+    for (int k = 0; k < R.nmat; ++k) {
+      const double* src = F.base[R.mbase[k]] + R.moff[k];
+      if (!stage || R.mcnt[k] <= 0 || !(F.stage_all || (R.mcrit & (1 << k)))) {
+        S.mp[k] = src;
+        continue;
+      }
+      const int padded = (R.mcnt[k] + 1) & ~1;
+      bulk_g2s(S.mat + mo, src, uint32_t(padded) * 8u, S.bar);
+      S.mp[k] = S.mat + mo;
+      mo += padded;
+    }
+  }
+}
+
+// wait on up to kFT flags in parallel (one thread each), then CTA barrier
+__device__ __forceinline__ void wait_flags_par(const int* f, int n) {
+  const int t = threadIdx.x;
+  for (int k = t; k < n; k += kFT) wait_flag(f + k);
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+__device__ void item_s2(const FusedArgs& F, int i, double* red, double* vec) {
+  const Dev& D = F.D;
+  const int t = threadIdx.x;
+  const int n = D.cc[i], c0 = D.cf[i], ny = D.y_dim[i], yo = D.y_off[i], so = D.s1_off[i];
+  const double al = F.alpha;
+  const double* z = F.z;
+  const double* eta = F.eta;
+  double* zo = F.zo;
+  const double* rb = D.rb + (yo - D.y_base);
+  const double sc = eta[so + ny];
+  // w = z - alpha L* eta on (y_i, tau_c, s_c)
+  auto wy = [&](int r) { return z[yo + r] - al * (eta[so + r] - sc * rb[r]); };
+  auto wtau = [&](int k) {
+    const int c = c0 + k;
+    const int o2 = D.s2_off[c - 1], p = D.px[c - 1] + D.pu[c - 1];
+    return z[D.tau_base + c - 1] - al * (0.5 * (eta[o2 + p] + eta[o2 + p + 1]));
+  };
+  auto ws = [&](int k) {
+    const int c = c0 + k;
+    double lt;
+    if (D.cc[c] > 0) {
+      lt = eta[D.s1_off[c] + D.y_dim[c]];
+    } else {
+      const int j = c - D.nnl, p = D.pN[j], o3 = D.s3_off[j] + D.s3_nc[j];
+      lt = 0.5 * (eta[o3 + p] + eta[o3 + p + 1]);
+    }
+    return z[D.s_base + c - 1] - al * lt;
+  };
+  const int kind = D.s2_kind[i];
+  if (kind == S2_DENSE) {
+    const int dim = ny + 2 * n;
+    double* w = vec;
+    for (int r = t; r < dim; r += kFT) w[r] = r < ny ? wy(r) : (r < ny + n ? wtau(r - ny) : ws(r - ny - n));
+    __syncthreads();
+    double* o = w + kSlot;
+    cta_gemv(D.s2P + D.s2p_off[i], dim, dim, dim, w, o, false, red);
+    for (int r = t; r < dim; r += kFT) {
+      if (r < ny)
+        zo[yo + r] = o[r];
+      else if (r < ny + n)
+        zo[D.tau_base + c0 + (r - ny) - 1] = o[r];
+      else
+        zo[D.s_base + c0 + (r - ny - n) - 1] = o[r];
+    }
+    __syncthreads();
+    return;
+  }
+  const double gam = D.s2_gamma[i];
+  const double A = kind == S2_AVAR ? gam * gam + 3.0 : 3.0;
+  const double Bc = kind == S2_EQ ? 0.0 : 1.0;
+  const double ylast = kind == S2_AVAR ? wy(2 * n) : (kind == S2_MAX ? wy(n) : 0.0);
+  auto ety = [&](int k) -> double {
+    if (kind == S2_AVAR) return gam * wy(k) - wy(n + k) + ylast;
+    if (kind == S2_MAX) return -wy(k) + ylast;
+    return wy(k);
+  };
+  double part = 0.0;
+  for (int k = t; k < n; k += kFT) part += ety(k) - wtau(k) - ws(k);
+  const double S = cta_sum(part, red);
+  const double den = A + Bc * n;
+  const double shift = Bc * S / den;
+  for (int k = t; k < n; k += kFT) {
+    const double yk = wy(k), tk = wtau(k), sk = ws(k);
+    const double v = ety(k) - tk - sk;
+    const double lam = (v - shift) / A;
+    if (kind == S2_AVAR) {
+      zo[yo + k] = yk - gam * lam;
+      zo[yo + n + k] = wy(n + k) + lam;
+    } else if (kind == S2_MAX) {
+      zo[yo + k] = yk + lam;
+    } else {
+      zo[yo + k] = yk - lam;
+    }
+    zo[D.tau_base + c0 + k - 1] = tk + lam;
+    zo[D.s_base + c0 + k - 1] = sk + lam;
+  }
+  if (t == 0 && kind != S2_EQ) {
+    const double lsum = S / den;
+    if (kind == S2_AVAR)
+      zo[yo + 2 * n] = ylast - lsum;
+    else
+      zo[yo + n] = ylast - lsum;
+  }
+  __syncthreads();
+}
+
+__device__ void item_back(const FusedArgs& F, const ItemRec& P, const Slot& S, double* sc_, double* red) {
+  const Dev& D = F.D;
+  const int i = P.node;
+  const int t = threadIdx.x, nx = D.nx, nu = D.nu, m = nx + nu;
+  const bool leaf = P.nch == 0, root = i == 0;
+  const double al = F.alpha;
+  const double* V = S.vec;
+  auto sp = [&](int id) { return V + S.voff[id]; };
+  double* gx = sc_;           // L* (x, u) of this node without the children
+  double* q = gx + kSlot;     // q (nx)
+  double* tv = q + kSlot;     // scratch (m)
+  double* rhs = tv + kSlot;   // scratch (m)
+  const int px = P.px, pu = P.pu;
+  int mk = 0;
+  const double* HxT = root ? nullptr : S.mp[mk++];
+  const double* HuT = root ? nullptr : S.mp[mk++];
+  const double* M1T = root ? nullptr : S.mp[mk++];
+  const double* KT = leaf ? nullptr : S.mp[mk++];
+  const double* Ri = leaf ? nullptr : S.mp[mk++];
+  const double* HNT = leaf ? S.mp[mk++] : nullptr;
+  // ---- own G' ec (+ terminal SOC term for leaves); independent of children
+  if (!leaf) {
+    const int nc = P.nc;
+    const double* ec = sp(B_EC);
+    if (D.g_diag) {
+      const double* gd = sp(B_GD);
+      for (int r = t; r < m; r += kFT) gx[r] = gd[r] * ec[r];
+      __syncthreads();
+    } else {
+      cta_gemv(D.GxT + D.g_off[i] * nx, nx, nc, nx, ec, gx, false, red);
+      cta_gemv(D.GuT + D.g_off[i] * nu, nu, nc, nu, ec, gx + nx, false, red);
+    }
+  } else {
+    const int j = i - D.nnl, nc = P.nc, pN = P.pN;
+    const double* ec = sp(B_EC);
+    if (D.gN_diag) {
+      const double* gd = sp(B_GD);
+      for (int r = t; r < nx; r += kFT) gx[r] = gd[r] * ec[r];
+      __syncthreads();
+    } else {
+      cta_gemv(D.GNT + D.gN_off[j] * nx, nx, nc, nx, ec, gx, false, red);
+    }
+    const double* hd = sp(B_HEADN);
+    cta_gemv(HNT, nx, pN, nx, hd, gx, true, red);
+    const double rsumN = hd[pN] + hd[pN + 1];
+    const double* qk = sp(B_QKN);
+    const double* zx = sp(B_ZX);
+    for (int r = t; r < nx; r += kFT) q[r] = -(zx[r] - al * (gx[r] - 0.5 * rsumN * qk[r]));  // q = -xbar
+  }
+  if (!root) {  // own stage-SOC adjoint term for the parent: adj_i = H' head - rsum/2 qk
+    const double* head = sp(B_HEAD);
+    const double rsum = head[px + pu] + head[px + pu + 1];
+    const double* qkv = sp(B_QK);
+    for (int r = t; r < m; r += kFT) tv[r] = -0.5 * rsum * qkv[r];
+    __syncthreads();
+    cta_gemv(HxT, nx, px, nx, head, tv, true, red);
+    cta_gemv(HuT, nu, pu, nu, head + px, tv + nx, true, red);
+    double* adj = D.adj + size_t(i - 1) * m;
+    for (int r = t; r < m; r += kFT) adj[r] = tv[r];
+  }
+  if (!leaf) {
+    // ---- children (flags), then q and d
+    const int c0 = P.c0, nch = P.nch;
+    wait_flags_par(F.flagB + c0, nch);
+    const double* zx = sp(B_ZX);
+    const double* zu = sp(B_ZU);
+    const double* h = sp(B_H);
+    const double* gv = sp(B_G);
+    for (int r = t; r < m; r += kFT) {
+      double lt = gx[r], tq = 0.0;
+      for (int c = 0; c < nch; ++c) {
+        const size_t o = size_t(c0 + c - 1) * m + r;
+        lt += ldcg(D.adj + o);
+        tq += ldcg(D.T12 + o);
+      }
+      if (r < nx) {
+        q[r] = h[r] - (zx[r] - al * lt) + tq;
+      } else {
+        const double ub = zu[r - nx] - al * lt;  // ubar
+        tv[r] = ub;
+        rhs[r - nx] = ub - gv[r - nx] - tq;
+      }
+    }
+    __syncthreads();
+    cta_gemv(KT, nx, nu, nx, tv + nx, gx, false, red);  // K' ubar (gx reused)
+    for (int r = t; r < nx; r += kFT) q[r] -= gx[r];
+    cta_gemv(Ri, nu, nu, nu, rhs, tv, false, red);  // d
+    double* dv = D.dvec + size_t(i) * nu;
+    for (int r = t; r < nu; r += kFT) dv[r] = tv[r];
+  }
+  __syncthreads();
+  if (!root) {
+    cta_gemv(M1T, m, nx, m, q, tv, false, red);
+    double* T12 = D.T12 + size_t(i - 1) * m;
+    for (int r = t; r < m; r += kFT) T12[r] = tv[r];
+  } else if (t == 0) {
+    const double sc = F.eta[P.s1o + P.ny];
+    F.zo[0] = F.z[0] - al * sc - al;  // CP primal step on s0 (solver.cpp:153-154)
+  }
+  cta_release(F.flagB + i);
+}
+
+__device__ void item_fwd(const FusedArgs& F, const ItemRec& P, const Slot& S, double* sc_, double* red) {
+  const Dev& D = F.D;
+  const int c = P.node;
+  const int t = threadIdx.x, nx = D.nx, nu = D.nu, m = nx + nu;
+  const bool leaf = P.nch == 0, root = c == 0;
+  const double al = F.alpha;
+  const double* z = F.z;
+  const double* eta = F.eta;
+  double* zo = F.zo;
+  double* eo = F.eo;
+  const double* V = S.vec;
+  auto sp = [&](int id) { return V + S.voff[id]; };
+  double* xd = sc_;            // [x_anc+; d_anc]
+  double* xn = xd + kSlot;     // own (x+, u+), then (x^, u^)
+  double* ahat = xn + kSlot;   // anc (x^, u^)
+  double* val = ahat + kSlot;  // segment values
+  double* pv = val + kSlot;    // p / alpha
+  const int px = P.px, pu = P.pu;
+  int mk = 0;
+  const double* M1 = root ? nullptr : S.mp[mk++];
+  const double* Hx = root ? nullptr : S.mp[mk++];
+  const double* Hu = root ? nullptr : S.mp[mk++];
+  const double* K = leaf ? nullptr : S.mp[mk++];
+  const double* HN = leaf ? S.mp[mk++] : nullptr;
+  const int an = root ? 0 : P.anc;
+  // ---- parent forward (root: own backward)
+  if (t == 0) wait_flag(root ? F.flagB : F.flagF + an);
+  else if (t == 32 && !leaf) wait_flag(F.flagS2 + c);
+  else if (t == 64 && !root) wait_flag(F.flagS2 + an);
+  __syncthreads();
+  if (!root) {
+    const double* zax = sp(F_AX);
+    const double* zau = sp(F_AU);
+    for (int r = t; r < m; r += kFT) {
+      if (r < nx) {
+        const double xp = ldcg(zo + 1 + size_t(an) * nx + r);
+        xd[r] = xp;
+        ahat[r] = 2.0 * xp - zax[r];
+      } else {
+        xd[r] = ldcg(D.dvec + size_t(an) * nu + (r - nx));
+        ahat[r] = 2.0 * ldcg(zo + D.u_base + size_t(an) * nu + (r - nx)) - zau[r - nx];
+      }
+    }
+    __syncthreads();
+    cta_gemv(M1, nx, m, nx, xd, xn, false, red);
+    const double* cv = sp(F_CV);
+    for (int r = t; r < nx; r += kFT) xn[r] += cv[r];
+  } else {
+    for (int r = t; r < nx; r += kFT) xn[r] = D.xinit[r];
+  }
+  __syncthreads();
+  if (!leaf) {
+    cta_gemv(K, nu, nx, nu, xn, xn + nx, false, red);
+    for (int r = t; r < nu; r += kFT) xn[nx + r] += ldcg(D.dvec + size_t(c) * nu + r);
+    __syncthreads();
+  }
+  for (int r = t; r < (leaf ? nx : m); r += kFT) {
+    if (r < nx)
+      zo[1 + size_t(c) * nx + r] = xn[r];
+    else
+      zo[D.u_base + size_t(c) * nu + (r - nx)] = xn[r];
+  }
+  // children need only (x+, u+) and d: publish before the dual work
+  cta_release(F.flagF + c);
+  {
+    const double* zx = sp(F_ZX);
+    const double* zu = sp(F_ZU);
+    for (int r = t; r < (leaf ? nx : m); r += kFT) xn[r] = 2.0 * xn[r] - (r < nx ? zx[r] : zu[r - nx]);
+  }
+  const double* hat = xn;
+  __syncthreads();
+  auto hatv = [&](int idx) { return 2.0 * ldcg(zo + idx) - z[idx]; };
+  if (!root) {  // stage-cost SOC block of (x_anc, u_anc, tau_c)
+    const int k = c - 1, p = px + pu, o2 = P.s2o;
+    const double* qk = sp(F_QK);
+    double part = 0.0;
+    for (int r = t; r < m; r += kFT) part += qk[r] * ahat[r];
+    const double qd = cta_sum(part, red);
+    cta_gemv(Hx, px, nx, px, ahat, val, false, red);
+    cta_gemv(Hu, pu, nu, pu, ahat + nx, val + px, false, red);
+    if (t == 0) {
+      const double row = 0.5 * hatv(D.tau_base + k) - 0.5 * qd;
+      val[p] = row;
+      val[p + 1] = row;
+    }
+    __syncthreads();
+    const double* seg = sp(F_SEG2);
+    for (int r = t; r < p + 2; r += kFT) {
+      const double pp = seg[r] + al * val[r];
+      val[r] = pp;
+      pv[r] = pp / al;
+    }
+    __syncthreads();
+    cta_soc_project(pv, sp(F_A), p + 2, red);
+    for (int r = t; r < p + 2; r += kFT) eo[o2 + r] = val[r] - al * pv[r];
+    __syncthreads();
+  }
+  if (!leaf) {  // y-copy rows (dual cone), risk scalar (R+), constraint rows (box)
+    const int ny = P.ny, yo = P.yo, so = P.s1o, nc = P.nc;
+    const bool pre = P.vcnt[F_SEG1] > 0;
+    const double* seg1 = pre ? sp(F_SEG1) : eta + so;
+    const double* rb = pre ? sp(F_RB) : D.rb + (yo - D.y_base);
+    const int nn0 = D.yc_nonneg[c];
+    double part = 0.0;
+    for (int r = t; r < ny; r += kFT) {
+      const double yh = hatv(yo + r);
+      part += rb[r] * yh;
+      const double pp = seg1[r] + al * yh;
+      double tp = pp / al;
+      if (nn0 >= 0) {
+        if (r < nn0) tp = fmax(tp, 0.0);
+        eo[so + r] = pp - al * tp;
+      } else {
+        eo[so + r] = tp;  // staged, general cone projected below
+      }
+    }
+    const double by = cta_sum(part, red);
+    if (nn0 < 0) {
+      int off = 0;
+      for (int pi = D.yc_poff[c]; pi < D.yc_poff[c + 1]; ++pi) {
+        const int kind = D.yc_kind[pi], dim = D.yc_dim[pi];
+        double* pvg = eo + so + off;
+        if (kind == 0) {
+          for (int r = t; r < dim; r += kFT) pvg[r] = 0.0;
+        } else if (kind == 1) {
+          for (int r = t; r < dim; r += kFT) pvg[r] = fmax(pvg[r], 0.0);
+        } else if (kind == 2) {
+          double ss = 0.0;
+          for (int r = t; r < dim - 1; r += kFT) ss += pvg[r] * pvg[r];
+          const double hn = sqrt(cta_sum(ss, red));
+          const double tt = pvg[dim - 1];
+          __syncthreads();
+          if (hn <= tt) {
+          } else if (hn <= -tt) {
+            for (int r = t; r < dim; r += kFT) pvg[r] = 0.0;
+          } else {
+            const double f = (hn + tt) / (2.0 * hn);
+            for (int r = t; r < dim - 1; r += kFT) pvg[r] *= f;
+            if (t == 0) pvg[dim - 1] = 0.5 * (hn + tt);
+          }
+        }
+        __syncthreads();
+        off += dim;
+      }
+      for (int r = t; r < ny; r += kFT) {
+        const double pp = seg1[r] + al * hatv(yo + r);
+        eo[so + r] = pp - al * eo[so + r];
+      }
+    }
+    if (t == 0) {
+      const double sv = hatv(c == 0 ? 0 : D.s_base + c - 1) - by;
+      const double pp = seg1[ny] + al * sv;
+      eo[so + ny] = pp - al * fmax(0.0, pp / al);
+    }
+    // constraint rows G [x^; u^] with box projection
+    if (D.g_diag) {
+      const double* gd = sp(F_GD);
+      for (int r = t; r < nc; r += kFT) val[r] = gd[r] * hat[r];
+      __syncthreads();
+    } else {
+      cta_gemv(D.Gx + D.g_off[c] * nx, nc, nx, nc, hat, val, false, red);
+      cta_gemv(D.Gu + D.g_off[c] * nu, nc, nu, nc, hat + nx, val, true, red);
+    }
+    const double* lo = sp(F_LO);
+    const double* hi = sp(F_HI);
+    const double* ec = seg1 + ny + 1;
+    for (int r = t; r < nc; r += kFT) {
+      const double pp = ec[r] + al * val[r];
+      eo[so + ny + 1 + r] = pp - al * fmin(fmax(pp / al, lo[r]), hi[r]);
+    }
+    __syncthreads();
+  } else {  // leaf: G_N x^ (box) and the terminal SOC block of (x, s)
+    const int j = c - D.nnl, nc = P.nc, eo3 = P.s3o, p = P.pN;
+    const double* seg3 = sp(F_SEG3);
+    if (D.gN_diag) {
+      const double* gd = sp(F_GND);
+      for (int r = t; r < nc; r += kFT) val[r] = gd[r] * hat[r];
+      __syncthreads();
+    } else {
+      cta_gemv(D.GN + D.gN_off[j] * nx, nc, nx, nc, hat, val, false, red);
+    }
+    const double* lo = sp(F_LON);
+    const double* hi = sp(F_HIN);
+    for (int r = t; r < nc; r += kFT) {
+      const double pp = seg3[r] + al * val[r];
+      eo[eo3 + r] = pp - al * fmin(fmax(pp / al, lo[r]), hi[r]);
+    }
+    __syncthreads();
+    const double* qk = sp(F_QKN);
+    double part = 0.0;
+    for (int r = t; r < nx; r += kFT) part += qk[r] * hat[r];
+    const double qd = cta_sum(part, red);
+    cta_gemv(HN, p, nx, p, hat, val, false, red);
+    if (t == 0) {
+      const double row = 0.5 * hatv(D.s_base + c - 1) - 0.5 * qd;
+      val[p] = row;
+      val[p + 1] = row;
+    }
+    __syncthreads();
+    const double* hs = seg3 + nc;
+    for (int r = t; r < p + 2; r += kFT) {
+      const double pp = hs[r] + al * val[r];
+      val[r] = pp;
+      pv[r] = pp / al;
+    }
+    __syncthreads();
+    cta_soc_project(pv, sp(F_AN), p + 2, red);
+    for (int r = t; r < p + 2; r += kFT) eo[eo3 + nc + r] = val[r] - al * pv[r];
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kFT, 1) k_T_fused(FusedArgs F) {
+  extern __shared__ __align__(1024) double dsm[];
+  __shared__ uint64_t bars[2];
+  __shared__ Slot slots[2];
+  __shared__ int tk[2];
+  __shared__ ItemRec recs[2];
+  const int t = threadIdx.x;
+  double* scratch = dsm + F.nslots * (size_t(F.mat_doubles) + F.vec_doubles);
+  double* red = scratch + kScratch * kSlot;
+  if (t == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int s = 0; s < 2; ++s) {
+      slots[s].mat = dsm + (F.nslots > 1 ? s : 0) * (size_t(F.mat_doubles) + F.vec_doubles);
+      slots[s].vec = slots[s].mat + F.mat_doubles;
+      slots[s].bar = &bars[s];
+    }
+    tk[0] = int(atomicAdd(F.ticket, 1ull));
+  }
+  uint32_t phase[2] = {0u, 0u};
+  const int total = F.D.nnl + 2 * F.D.nn;
+  __syncthreads();
+  int cur = 0;
+  if (tk[0] < total) {
+    load_rec(F, tk[0], &recs[0]);
+    __syncthreads();
+    issue(F, recs[0], slots[0]);
+  } else {
+    cp_async_commit();
+  }
+  const bool ring = F.nslots > 1;
+  for (;;) {
+    const int it = tk[cur];
+    if (it >= total) break;
+    const int nxt = ring ? cur ^ 1 : cur;
+    // take and prefetch the next item into the other slot (two-slot ring)
+    if (ring) {
+      if (t == 0) tk[nxt] = int(atomicAdd(F.ticket, 1ull));
+      __syncthreads();
+      const int itn = tk[nxt];
+      if (itn < total) {
+        load_rec(F, itn, &recs[nxt]);
+        __syncthreads();
+        issue(F, recs[nxt], slots[nxt]);
+      } else {
+        cp_async_commit();  // keep one group per item in flight
+      }
+    } else {
+      cp_async_commit();
+    }
+    // wait for the current item's operands (all but the newest cp.async group)
+    cp_async_wait<1>();
+    const ItemRec& P = recs[cur];
+    if (P.kind != 0 && F.stage_smem && P.nmat > 0) {
+      while (!mbar_try_wait(slots[cur].bar, phase[cur])) {
+      }
+      phase[cur] ^= 1u;
+    }
+    __syncthreads();
+    if (P.kind == 0) {
+      item_s2(F, P.node, red, scratch);
+      cta_release(F.flagS2 + P.node);
+    } else if (P.kind == 1) {
+      item_back(F, P, slots[cur], scratch, red);
+    } else {
+      item_fwd(F, P, slots[cur], scratch, red);
+    }
+    __syncthreads();
+    if (!ring) {  // single slot: take and prefetch the next item now
+      if (t == 0) tk[cur] = int(atomicAdd(F.ticket, 1ull));
+      __syncthreads();
+      if (tk[cur] < total) {
+        load_rec(F, tk[cur], &recs[cur]);
+        __syncthreads();
+        issue(F, recs[cur], slots[cur]);
+      }
+    }
+    cur = nxt;
+  }
+  cp_async_wait<0>();
+}
+
