@@ -101,8 +101,13 @@ void Engine::setup_fused() {
     if (p_.nc[i] > kMaxD) fused_ok_ = false;
   for (int j = 0; j < tr.nl(); ++j)
     if (p_.ncN[j] > kMaxD) fused_ok_ = false;
+  // Measured on B200 (profiles/r01_fused_configs.md): the dataflow kernel
+  // wins on narrow trees (c2, 223 nodes: 0.105 ms vs 1.21 ms per T), the
+  // stage-parallel kernels on wide ones (c3, 36085 nodes: 3.05 ms vs 3.30 ms).
   const char* env = std::getenv("SPOCK_T_UNFUSED");
+  const char* fenv = std::getenv("SPOCK_T_FUSED");
   if (env && env[0] == '1') fused_ok_ = false;
+  if (!(fenv && fenv[0] == '1') && nn >= 4096) fused_ok_ = false;
   if (!fused_ok_) return;
   // largest per-item set of staged blocks and prefetched vector spans (even
   // doubles each), mirroring make_plan in fused.cu
