@@ -81,6 +81,8 @@ Engine::Engine(const spock_problem_desc* desc, const Params& prm) : prm_(prm) {
   CK(cudaGetDevice(&dev));
   CK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
   upload();
+  narrow_ = p_.tree.nn() < 4096;
+  if (const char* nv = std::getenv("SPOCK_NARROW")) narrow_ = nv[0] == '1';
   factorize();
   norm_.analytic_bound = analytic_norm_bound(p_, soc_);
   setup_fused();
@@ -900,9 +902,21 @@ void Engine::factorize() {
 // ---------------------------------------------------------------------------
 void Engine::sync() { CK(cudaStreamSynchronize(st_)); }
 
-void Engine::L(const double* z, double* eta) { launch_L(D_, z, 1.0, nullptr, 0.0, nullptr, eta, 0.0, false, st_); }
+// standalone L / L*: CTA-per-node kernels on narrow trees (latency), warp-per-
+// node kernels on wide ones (throughput); same arithmetic
+void Engine::L(const double* z, double* eta) {
+  if (narrow_)
+    launch_L_narrow(D_, z, eta, st_);
+  else
+    launch_L(D_, z, 1.0, nullptr, 0.0, nullptr, eta, 0.0, false, st_);
+}
 
-void Engine::Lt(const double* eta, double* z) { launch_Lt(D_, eta, nullptr, z, 0.0, 1.0, 0.0, st_); }
+void Engine::Lt(const double* eta, double* z) {
+  if (narrow_)
+    launch_Lt_narrow(D_, eta, z, st_);
+  else
+    launch_Lt(D_, eta, nullptr, z, 0.0, 1.0, 0.0, st_);
+}
 
 // one CP application (solver.cpp:148-164), internal layout; zo/eo must not
 // alias z/eta
@@ -1469,7 +1483,8 @@ double Engine::bench_T(int k, bool graph, bool flush) {
 }
 
 // average device ms per launch class over k repetitions:
-// ms[0] L* (child+node), ms[1] S1 (all stages), ms[2] S2, ms[3] L+S3 dual, ms[4] whole T
+// ms[0] L* (standalone), ms[1] S1 sweeps (per-stage path only), ms[2] S2,
+// ms[3] L (standalone), ms[4] whole T (fused kernel or per-stage sequence)
 void Engine::bench_kernels(int k, bool flush, double* ms) {
   double *z0 = scratch_z_[0], *e0 = scratch_e_[0], *z1 = scratch_z_[1], *e1 = scratch_e_[1];
   cudaEvent_t a, b;
@@ -1478,13 +1493,14 @@ void Engine::bench_kernels(int k, bool flush, double* ms) {
   for (int c = 0; c < 5; ++c) ms[c] = 0.0;
   for (int i = 0; i < k; ++i) {
     for (int c = 0; c < 5; ++c) {
+      if (c == 1 && fused_ok_) continue;
       if (flush) flush_l2();
       CK(cudaEventRecord(a, st_));
       switch (c) {
-        case 0: launch_Lt(D_, e0, z0, z1, 1.0, -alpha_, -alpha_, st_); break;
+        case 0: Lt(e0, z1); break;
         case 1: launch_s1(D_, stage_start_.data(), z1, st_); break;
         case 2: launch_s2(D_, z1, st_); break;
-        case 3: launch_L(D_, z1, 2.0, z0, -1.0, e0, e1, alpha_, true, st_); break;
+        case 3: L(z0, e1); break;
         case 4: T(z0, e0, z1, e1); break;
       }
       CK(cudaEventRecord(b, st_));
@@ -1501,39 +1517,44 @@ void Engine::bench_kernels(int k, bool flush, double* ms) {
 }
 
 // Algorithmic bytes per launch class (each operand read or written once per
-// launch): [L*, S1, S2, L+S3, T]
+// launch): [L*, S1 sweeps, S2, L, T].  T is the sum
+// of the fused phases: L* matrices + S1 blocks + L matrices + every vector
+// segment once (the dual update reads eta and the a/box data, writes eta+).
 void Engine::traffic(double* out) const {
   const Tree& tr = p_.tree;
   const int nn = tr.nn(), nnl = tr.nnl(), nx = p_.nx, nu = p_.nu, m = nx + nu;
-  double lt = 0, s1 = 0, s2 = 0, ld = 0;
+  double lt = 0, s1 = 0, s2 = 0, l = 0, dual = 0;
   for (int k = 0; k < nn - 1; ++k) {
     const int px = soc_.stage[k].px, pu = soc_.stage[k].pu, p = px + pu;
-    lt += double(px) * nx + double(pu) * nu + m + (p + 2) + m + 2;        // H', qk, eta seg, adj, tau in/out
-    ld += double(px) * nx + double(pu) * nu + m + 2.0 * (p + 2) + (p + 2)  // H, qk, a, eta in, eta out
-          + 2.0 * m + 2;                                                    // (x,u)_anc of z+ and z, tau
-    s1 += double(m) * nx + (nx + m)   // backward: M1', q in (xbar), T12 out
-          + double(nx) * m + m + 2 * nx;  // forward: M1, (x,d)_anc, c, x out
+    const double H = double(px) * nx + double(pu) * nu;
+    lt += H + m + (p + 2) + m + 1;            // H', qk, eta seg, adj out, tau out
+    l += H + m + 2.0 * m + 1 + (p + 2);       // H, qk, (x,u)_anc, tau, eta seg out
+    dual += 2.0 * (p + 2);                    // eta in (p+2) and translation a (p+2) of the dual update
+    s1 += double(m) * nx + (nx + m)           // backward: M1', q in, T12 out
+          + double(nx) * m + m + 2 * nx;      // forward: M1, (x,d)_anc, c, x out
   }
   for (int i = 0; i < nnl; ++i) {
     const int ny = lay_.y_dim[i], nc = p_.nc[i], nch = tr.child_count[i];
     const double g = D_.g_diag ? m : double(nc) * m;
-    lt += 2.0 * ny + 1 + nc + g + double(nch) * m + 2.0 * (m + ny + 1);  // eta, b, G, adj sums, z in/out
-    ld += 2.0 * ny + ny + 1 + (ny + 1 + nc) * 2.0 + g + 2.0 * m + 2.0 * nc + 2;  // y of z+,z, b, eta in/out, G, xu, box
-    s1 += double(nx) * nu + nx + nu + double(nu) * nu + double(nch) * m + nu  // KT, h, g, Rinv, T12 of children, d
-          + double(nu) * nx + nu + nu + nu;                                    // forward K, d, u out
-    s2 += 2.0 * (ny + 2 * nch) + (D_.s2_kind ? 0.0 : 0.0);
+    lt += (ny + 1 + nc) + ny + g + double(nch) * m + (m + ny + 1);  // eta seg, b, G, adj sums, z out
+    l += ny + ny + g + m + 1 + (ny + 1 + nc);                          // y, b, G, (x,u), s, eta out
+    dual += 2.0 * nc;                                                  // box lo/hi
+    s1 += double(nx) * nu + nx + nu + double(nu) * nu + double(nch) * m + nu  // KT, h, g, Rinv, T12 sums, d
+          + double(nu) * nx + nu + nu + nu;                                  // forward K, d, u out
+    s2 += 2.0 * (ny + 2 * nch);
   }
   for (int j = 0; j < nn - nnl; ++j) {
     const int pN = soc_.leaf[j].px, nc = p_.ncN[j];
     const double g = D_.gN_diag ? nx : double(nc) * nx;
-    lt += nc + g + double(pN) * nx + (pN + 2) + nx + 2.0 * (nx + 1);
-    ld += g + double(pN) * nx + nx + 2.0 * (pN + 2) + (pN + 2) + 2.0 * (nc) + nc * 2.0 + 2.0 * (nx + 1);
+    lt += nc + g + double(pN) * nx + (pN + 2) + nx + (nx + 1);
+    l += g + double(pN) * nx + nx + nx + 1 + (nc + pN + 2);
+    dual += 2.0 * (pN + 2) + 2.0 * nc;
   }
   out[0] = 8.0 * lt;
   out[1] = 8.0 * s1;
   out[2] = 8.0 * s2;
-  out[3] = 8.0 * ld;
-  out[4] = out[0] + out[1] + out[2] + out[3];
+  out[3] = 8.0 * l;
+  out[4] = out[0] + out[1] + out[2] + out[3] + 8.0 * dual;
 }
 
 }  // namespace spock

@@ -122,6 +122,7 @@ class Engine {
   double* scratch_e_[3] = {};
   cudaGraphExec_t bench_graph_ = nullptr;
   bool fused_ok_ = false;
+  bool narrow_ = true;
   FusedArgs fargs_{};
   int fused_grid_ = 0;
   size_t fused_sync_bytes_ = 0;
