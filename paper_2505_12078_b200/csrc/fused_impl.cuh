@@ -55,15 +55,18 @@ __device__ __forceinline__ void st_release(int* p, int v) {
 __device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
 
 __device__ void wait_flag(const int* f) {
-  while (ld_acquire(f) < 1) __nanosleep(20);
+  // tight spin first (the producer is usually one hop away), then back off
+  for (int k = 0; k < 64; ++k)
+    if (ld_acquire(f) >= 1) return;
+  while (ld_acquire(f) < 1) __nanosleep(32);
 }
-// CTA barrier, then one fenced release store (CUTLASS GenericBarrier pattern)
+// CTA barrier, then one release store.  bar.sync makes every thread's prior
+// writes performed with respect to thread 0, and st.release.gpu is cumulative,
+// so a consumer that acquires the flag sees all of them (PTX memory model;
+// the extra fence.sc of __threadfence() is not needed).
 __device__ __forceinline__ void cta_release(int* flag) {
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    st_release(flag, 1);
-  }
+  if (threadIdx.x == 0) st_release(flag, 1);
 }
 
 // y[r] = (acc ? y[r] : 0) + sum_c A[r + c*lda] x[c], r < m <= kFT; all threads
