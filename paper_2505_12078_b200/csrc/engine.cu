@@ -8,6 +8,7 @@
 //   Engine::solve_b      <- SpockSolver::run           proj/src/solver.cpp:189-350
 #include "engine.hpp"
 
+#include <cstdio>
 #include <cstdlib>
 
 #include <algorithm>
@@ -1431,10 +1432,41 @@ void Engine::flush_l2() {
   CK(cudaMemsetAsync(flush_buf_, int(0x5a), n, st_));
 }
 
+// SPOCK_FUSED_TRACE=<file>: one traced fused T (4 globaltimer stamps per item,
+// int64 little endian) written to <file>; used by tools/trace_fused.py
+static void dump_trace_if_requested(const FusedArgs& F0, int grid, cudaStream_t st, int nitems) {
+  const char* path = std::getenv("SPOCK_FUSED_TRACE");
+  if (!path || !path[0]) return;
+  FusedArgs F = F0;
+  unsigned long long* d = nullptr;
+  CK(cudaMalloc(&d, sizeof(unsigned long long) * 4 * size_t(nitems)));
+  CK(cudaMemsetAsync(d, 0, sizeof(unsigned long long) * 4 * size_t(nitems), st));
+  F.trace = d;
+  launch_T_fused(F, grid, st);
+  std::vector<unsigned long long> h(4 * size_t(nitems));
+  CK(cudaMemcpyAsync(h.data(), d, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  cudaFree(d);
+  if (FILE* f = std::fopen(path, "wb")) {
+    std::fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
+    std::fclose(f);
+  }
+}
+
 double Engine::bench_T(int k, bool graph, bool flush) {
   double *z[2] = {scratch_z_[0], scratch_z_[1]}, *e[2] = {scratch_e_[0], scratch_e_[1]};
   CK(cudaMemsetAsync(z[0], 0, sizeof(double) * lay_.nz, st_));
   CK(cudaMemsetAsync(e[0], 0, sizeof(double) * lay_.neta, st_));
+  if (fused_ok_ && std::getenv("SPOCK_FUSED_TRACE")) {
+    FusedArgs F = fargs_;
+    F.D = D_;
+    F.z = z[0], F.eta = e[0], F.zo = z[1], F.eo = e[1], F.alpha = alpha_;
+    F.base[FB_Z] = z[0];
+    F.base[FB_ETA] = e[0];
+    flush_l2();
+    CK(cudaMemsetAsync(F.ticket, 0, fused_sync_bytes_, st_));
+    dump_trace_if_requested(F, fused_grid_, st_, D_.nnl + 2 * D_.nn);
+  }
   if (graph && !bench_graph_) {
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));

@@ -50,6 +50,7 @@ struct FusedArgs {
   int nslots;                  // 1 or 2 (prefetch ring depth)
   int threads;                 // 128 or 256 threads per CTA
   const ItemRec* items;        // [nnl + 2 nn]
+  unsigned long long* trace;   // optional: 4 globaltimer stamps per item (debug/profiling)
   const double* base[FB_COUNT];
 };
 

@@ -54,6 +54,15 @@ __device__ __forceinline__ void st_release(int* p, int v) {
 // loads of data produced by other CTAs in this launch: L2 only (no stale L1)
 __device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void stamp(const FusedArgs& F, int item, int k) {
+  if (F.trace && threadIdx.x == 0) F.trace[size_t(item) * 4 + k] = gtimer();
+}
+
 __device__ void wait_flag(const int* f) {
   // tight spin first (the producer is usually one hop away), then back off
   for (int k = 0; k < 64; ++k)
@@ -369,6 +378,7 @@ __device__ void item_back(const FusedArgs& F, const ItemRec& P, const Slot& S, d
     // ---- children (flags), then q and d
     const int c0 = P.c0, nch = P.nch;
     wait_flags_par(F.flagB + c0, nch);
+    stamp(F, F.D.nnl + (F.D.nn - 1 - i), 1);
     const double* zx = sp(B_ZX);
     const double* zu = sp(B_ZU);
     const double* h = sp(B_H);
@@ -405,6 +415,7 @@ __device__ void item_back(const FusedArgs& F, const ItemRec& P, const Slot& S, d
     F.zo[0] = F.z[0] - al * sc - al;  // CP primal step on s0 (solver.cpp:153-154)
   }
   cta_release(F.flagB + i);
+  stamp(F, F.D.nnl + (F.D.nn - 1 - i), 2);
 }
 
 __device__ void item_fwd(const FusedArgs& F, const ItemRec& P, const Slot& S, double* sc_, double* red) {
@@ -437,6 +448,7 @@ __device__ void item_fwd(const FusedArgs& F, const ItemRec& P, const Slot& S, do
   else if (t == 32 && !leaf) wait_flag(F.flagS2 + c);
   else if (t == 64 && !root) wait_flag(F.flagS2 + an);
   __syncthreads();
+  stamp(F, F.D.nnl + F.D.nn + c, 1);
   if (!root) {
     const double* zax = sp(F_AX);
     const double* zau = sp(F_AU);
@@ -471,6 +483,7 @@ __device__ void item_fwd(const FusedArgs& F, const ItemRec& P, const Slot& S, do
   }
   // children need only (x+, u+) and d: publish before the dual work
   cta_release(F.flagF + c);
+  stamp(F, F.D.nnl + F.D.nn + c, 2);
   {
     const double* zx = sp(F_ZX);
     const double* zu = sp(F_ZU);
@@ -679,6 +692,7 @@ __global__ void __launch_bounds__(kFT, 1) k_T_fused(FusedArgs F) {
       phase[cur] ^= 1u;
     }
     __syncthreads();
+    stamp(F, it, 0);
     if (P.kind == 0) {
       item_s2(F, P.node, red, scratch);
       cta_release(F.flagS2 + P.node);
@@ -688,6 +702,7 @@ __global__ void __launch_bounds__(kFT, 1) k_T_fused(FusedArgs F) {
       item_fwd(F, P, slots[cur], scratch, red);
     }
     __syncthreads();
+    stamp(F, it, 3);
     if (!ring) {  // single slot: take and prefetch the next item now
       if (t == 0) tk[cur] = int(atomicAdd(F.ticket, 1ull));
       __syncthreads();
