@@ -130,15 +130,17 @@ void Engine::setup_fused() {
     int64_t b = 0, f = 0, vb = pad2(nx), vf = pad2(nx);
     if (!root) {
       const int px = soc_.stage[i - 1].px, pu = soc_.stage[i - 1].pu, p = px + pu;
-      b += (sall ? pad2(int64_t(px) * nx) + pad2(int64_t(pu) * nu) : 0) + pad2(int64_t(m) * nx);
-      f += pad2(int64_t(nx) * m) + (sall ? pad2(int64_t(px) * nx) + pad2(int64_t(pu) * nu) : 0);
+      const int64_t mb = leaf ? int64_t(m) * nx : int64_t(m) * m;  // M1' or [M1' | M1'K']
+      const int64_t mf = leaf ? int64_t(nx) * m : int64_t(m) * m;  // M1 or [M1; K M1]
+      b += (sall ? pad2(int64_t(px) * nx) + pad2(int64_t(pu) * nu) : 0) + pad2(mb);
+      f += pad2(mf) + (sall ? pad2(int64_t(px) * nx) + pad2(int64_t(pu) * nu) : 0);
       vb += pad2(p + 2) + pad2(m);
-      vf += pad2(nx) + pad2(nu) + pad2(nx) + 2 * pad2(p + 2) + pad2(m);
+      vf += pad2(nx) + pad2(nu) + pad2(m) + 2 * pad2(p + 2) + pad2(m);
     }
     if (!leaf) {
       const int nc = p_.nc[i], ny = lay_.y_dim[i];
       b += pad2(int64_t(nx) * nu) + pad2(int64_t(nu) * nu);
-      f += pad2(int64_t(nu) * nx);
+      if (root) f += pad2(int64_t(nu) * nx);
       vb += pad2(nu) + pad2(nc) + (D_.g_diag ? pad2(m) : 0) + pad2(nx) + pad2(nu);
       vf += pad2(nu) + (D_.g_diag ? pad2(m) : 0) + 2 * pad2(nc);
       if (ny + 1 + nc <= kMaxD) vf += pad2(ny + 1 + nc) + pad2(ny);
@@ -189,10 +191,18 @@ void Engine::setup_fused() {
   F.flagS2 = reinterpret_cast<int*>(buf + 8);
   F.flagB = F.flagS2 + nnl;
   F.flagF = F.flagB + nn;
+  // offline combined blocks B = [M1' | M1'K'], F = [M1; K M1], f = [c; K c]
+  const int64_t cs = pad2(int64_t(m) * m);
+  double* dBm = dalloc<double>(size_t(std::max(nn - 1, 1)) * cs);
+  double* dFm = dalloc<double>(size_t(std::max(nn - 1, 1)) * cs);
+  double* dfc = dalloc<double>(size_t(std::max(nn - 1, 1)) * m);
+  launch_build_combined(D_, dBm, dFm, dfc, cs, st_);
+  CK(cudaGetLastError());
   // per-item records (prefetch plans + metadata), mirroring the span ids of fused.cu
   enum { B_HEAD = 0, B_QK, B_ZX, B_ZU, B_EC, B_GD, B_H, B_G, B_HEADN, B_QKN };
-  enum { F_ZX = 0, F_ZU, F_AX, F_AU, F_CV, F_SEG2, F_A, F_QK, F_GD, F_LO, F_HI, F_SEG3, F_AN, F_QKN, F_GND,
+  enum { F_ZX = 0, F_ZU, F_AX, F_AU, F_FC, F_SEG2, F_A, F_QK, F_GD, F_LO, F_HI, F_SEG3, F_AN, F_QKN, F_GND,
          F_LON, F_HIN, F_SEG1, F_RB };
+  // ticket order: [backward nn-1..0][S2 of each parent][forward 0..nn-1]
   std::vector<ItemRec> recs(size_t(nnl) + 2 * size_t(nn));
   std::vector<int64_t> hx_off(nn - 1), hu_off(nn - 1), a_off(nn - 1), hn_off(tr.nl()), aN_off(tr.nl());
   {
@@ -239,14 +249,14 @@ void Engine::setup_fused() {
     R.nspan = std::max(R.nspan, id + 1);
   };
   for (int it = 0; it < nnl; ++it) {
-    ItemRec& R = recs[it];
+    ItemRec& R = recs[size_t(nn) + it];
     std::memset(&R, 0, sizeof(R));
     R.kind = 0;
     fill_meta(R, it);
   }
   for (int k = 0; k < nn; ++k) {  // backward items: node nn-1 ... 0
     const int i = nn - 1 - k;
-    ItemRec& R = recs[size_t(nnl) + k];
+    ItemRec& R = recs[size_t(k)];
     std::memset(&R, 0, sizeof(R));
     R.kind = 1;
     fill_meta(R, i);
@@ -255,7 +265,10 @@ void Engine::setup_fused() {
       const int px = R.px, pu = R.pu;
       mat(R, FB_HXT, hx_off[i - 1], int64_t(px) * nx, false);
       mat(R, FB_HUT, hu_off[i - 1], int64_t(pu) * nu, false);
-      mat(R, FB_M1T, int64_t(i - 1) * D_.m1_stride, int64_t(m) * nx, true);
+      if (leaf)
+        mat(R, FB_M1T, int64_t(i - 1) * D_.m1_stride, int64_t(m) * nx, true);
+      else
+        mat(R, FB_BM, int64_t(i - 1) * cs, int64_t(m) * m, true);
       vec(R, B_HEAD, FB_ETA, lay_.seg2_off[i - 1], px + pu + 2);
       vec(R, B_QK, FB_QK, int64_t(i - 1) * m, m);
     }
@@ -278,7 +291,7 @@ void Engine::setup_fused() {
     }
   }
   for (int c = 0; c < nn; ++c) {  // forward items: node 0 ... nn-1
-    ItemRec& R = recs[size_t(nnl) + nn + c];
+    ItemRec& R = recs[size_t(nn) + nnl + c];
     std::memset(&R, 0, sizeof(R));
     R.kind = 2;
     fill_meta(R, c);
@@ -287,18 +300,21 @@ void Engine::setup_fused() {
     if (!leaf) vec(R, F_ZU, FB_Z, lay_.u_base + int64_t(c) * nu, nu);
     if (!root) {
       const int px = R.px, pu = R.pu, an = R.anc, p = px + pu;
-      mat(R, FB_M1, int64_t(c - 1) * D_.m1_stride, int64_t(nx) * m, true);
+      if (leaf)
+        mat(R, FB_M1, int64_t(c - 1) * D_.m1_stride, int64_t(nx) * m, true);
+      else
+        mat(R, FB_FM, int64_t(c - 1) * cs, int64_t(m) * m, true);
       mat(R, FB_HX, hx_off[c - 1], int64_t(px) * nx, false);
       mat(R, FB_HU, hu_off[c - 1], int64_t(pu) * nu, false);
       vec(R, F_AX, FB_Z, 1 + int64_t(an) * nx, nx);
       vec(R, F_AU, FB_Z, lay_.u_base + int64_t(an) * nu, nu);
-      vec(R, F_CV, FB_CVEC, int64_t(c - 1) * nx, nx);
+      vec(R, F_FC, FB_FC, int64_t(c - 1) * m, leaf ? nx : m);
       vec(R, F_SEG2, FB_ETA, lay_.seg2_off[c - 1], p + 2);
       vec(R, F_A, FB_A, a_off[c - 1], p + 2);
       vec(R, F_QK, FB_QK, int64_t(c - 1) * m, m);
     }
+    if (root) mat(R, FB_K, int64_t(c) * D_.k_stride, int64_t(nu) * nx, true);
     if (!leaf) {
-      mat(R, FB_K, int64_t(c) * D_.k_stride, int64_t(nu) * nx, true);
       const int nc = p_.nc[c], ny = lay_.y_dim[c];
       const int64_t go = p_.g_off[c];
       if (D_.g_diag) vec(R, F_GD, FB_GD, int64_t(c) * m, m);
@@ -332,6 +348,7 @@ void Engine::setup_fused() {
   bases[FB_M1] = D_.M1, bases[FB_HX] = D_.Hx, bases[FB_HU] = D_.Hu, bases[FB_K] = D_.K, bases[FB_HN] = D_.HN;
   bases[FB_CVEC] = D_.cvec, bases[FB_A] = D_.a, bases[FB_LO] = D_.lo, bases[FB_HI] = D_.hi, bases[FB_RB] = D_.rb;
   bases[FB_AN] = D_.aN, bases[FB_LON] = D_.loN, bases[FB_HIN] = D_.hiN;
+  bases[FB_BM] = dBm, bases[FB_FM] = dFm, bases[FB_FC] = dfc;
   for (int k = 0; k < FB_COUNT; ++k) F.base[k] = bases[k];
 }
 
@@ -1439,11 +1456,11 @@ static void dump_trace_if_requested(const FusedArgs& F0, int grid, cudaStream_t 
   if (!path || !path[0]) return;
   FusedArgs F = F0;
   unsigned long long* d = nullptr;
-  CK(cudaMalloc(&d, sizeof(unsigned long long) * 4 * size_t(nitems)));
-  CK(cudaMemsetAsync(d, 0, sizeof(unsigned long long) * 4 * size_t(nitems), st));
+  CK(cudaMalloc(&d, sizeof(unsigned long long) * 8 * size_t(nitems)));
+  CK(cudaMemsetAsync(d, 0, sizeof(unsigned long long) * 8 * size_t(nitems), st));
   F.trace = d;
   launch_T_fused(F, grid, st);
-  std::vector<unsigned long long> h(4 * size_t(nitems));
+  std::vector<unsigned long long> h(8 * size_t(nitems));
   CK(cudaMemcpyAsync(h.data(), d, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   cudaFree(d);

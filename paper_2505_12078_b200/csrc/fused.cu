@@ -6,9 +6,9 @@
 // the Moreau step (projections.cpp:212-244, solver.cpp:159-163).
 //
 // Work items, handed out in this order by a global ticket counter:
-//   [0, nnl)            S2 of parent i (no dependencies)
-//   [nnl, nnl+nn)       backward item of node nn-1 ... 0 (children first)
-//   [nnl+nn, nnl+2nn)   forward item of node 0 ... nn-1 (parents first)
+//   [0, nn)             backward item of node nn-1 ... 0 (children first)
+//   [nn, nn+nnl)        S2 of parent i (no dependencies; needed by forward items)
+//   [nn+nnl, 2nn+nnl)   forward item of node 0 ... nn-1 (parents first)
 // An item only waits on items with smaller tickets.  A CTA holds at most two
 // items: the one it computes and the next one, whose operands are already in
 // flight into the other half of a two-slot shared-memory ring: the node's
@@ -25,8 +25,10 @@
 //   q_i = sum_c [Abar_c' q_c] - xbar_i - K_i' ubar_i + h_i ;  leaf: q_i = -xbar_i
 //   d_i = Rt_i^{-1}(ubar_i - sum_c [B_c' q_c] - g_i)
 //   [Abar_i' q_i; B_i' q_i] -> T12_i for the parent
-// Forward item (node c):
-//   x_c = [Abar_c B_c][x_anc; d_anc] + c_c,  u_c = K_c x_c + d_c  (flag released here)
+// with every child-independent term computed before the flag wait and the
+// rest as one parallel GEMV round: T12_i = [M1_i' | M1_i'K_i'] v, d_i = dc - Rt^-1 w.
+// Forward item (node c), one GEMV with F_c = [M1_c; K_c M1_c]:
+//   [x_c; u_c - d_c] = F_c [x_anc; d_anc] + [c_c; K_c c_c]  (flag released here)
 //   then every dual segment owned by c: eta+ = p - a Pi_S3(p / a),
 //   p = eta + a L(2 z+ - z).
 #include <cuda_runtime.h>
@@ -51,6 +53,47 @@ namespace fused128 {
 }  // namespace fused128
 
 namespace {
+// Offline combined blocks of the fused sweeps (one CTA per non-root node):
+//   Bm = [M1' | M1' K'] (m x m), Fm = [M1; K M1] (m x m), fc = [c; K c]
+// (leaves: only the M1 part; K is the node's own feedback gain).
+__global__ void k_build_combined(Dev D, double* Bm, double* Fm, double* fc, int64_t cs) {
+  const int c = blockIdx.x + 1;
+  const int nx = D.nx, nu = D.nu, m = nx + nu;
+  const bool leaf = D.cc[c] == 0;
+  const double* M1 = D.M1 + size_t(c - 1) * D.m1_stride;   // nx x m
+  const double* M1T = D.M1T + size_t(c - 1) * D.m1_stride; // m x nx
+  const double* K = leaf ? nullptr : D.K + size_t(c) * D.k_stride;   // nu x nx
+  const double* KT = leaf ? nullptr : D.KT + size_t(c) * D.k_stride; // nx x nu
+  double* B = Bm + size_t(c - 1) * cs;
+  double* Fo = Fm + size_t(c - 1) * cs;
+  const double* cv = D.cvec + size_t(c - 1) * nx;
+  double* f = fc + size_t(c - 1) * m;
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+    const int r = e % m, col = e / m;
+    double b = 0.0, fo = 0.0;
+    if (col < nx) {
+      b = M1T[r + size_t(col) * m];
+    } else if (!leaf) {
+      for (int k = 0; k < nx; ++k) b += M1T[r + size_t(k) * m] * KT[k + size_t(col - nx) * nx];
+    }
+    if (r < nx) {
+      fo = M1[r + size_t(col) * nx];
+    } else if (!leaf) {
+      for (int k = 0; k < nx; ++k) fo += K[(r - nx) + size_t(k) * nu] * M1[k + size_t(col) * nx];
+    }
+    B[e] = b;
+    Fo[e] = fo;
+  }
+  for (int r = threadIdx.x; r < m; r += blockDim.x) {
+    double v = 0.0;
+    if (r < nx) {
+      v = cv[r];
+    } else if (!leaf) {
+      for (int k = 0; k < nx; ++k) v += K[(r - nx) + size_t(k) * nu] * cv[k];
+    }
+    f[r] = v;
+  }
+}
 constexpr int kSlotD = kMaxD + 8;
 constexpr int kScratchSlots = 6;
 }  // namespace
@@ -69,6 +112,10 @@ cudaError_t fused_configure(int smem_bytes, int threads) {
 const void* fused_kernel_ptr(int threads) {
   return threads == 128 ? reinterpret_cast<const void*>(&fused128::k_T_fused)
                         : reinterpret_cast<const void*>(&fused256::k_T_fused);
+}
+
+void launch_build_combined(const Dev& D, double* Bm, double* Fm, double* fc, int64_t stride, cudaStream_t st) {
+  if (D.nr > 0) k_build_combined<<<D.nr, 256, 0, st>>>(D, Bm, Fm, fc, stride);
 }
 
 void launch_T_fused(const FusedArgs& F, int grid, cudaStream_t st) {

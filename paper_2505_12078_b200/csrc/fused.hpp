@@ -10,7 +10,8 @@ namespace spock {
 // Operand base arrays of the per-item records (offsets are relative to these).
 enum FusedBase : int {
   FB_Z = 0, FB_ETA, FB_HXT, FB_HUT, FB_M1T, FB_KT, FB_RINV, FB_HNT, FB_QK, FB_GD, FB_H, FB_G, FB_QKN, FB_GND,
-  FB_M1, FB_HX, FB_HU, FB_K, FB_HN, FB_CVEC, FB_A, FB_LO, FB_HI, FB_RB, FB_AN, FB_LON, FB_HIN, FB_COUNT
+  FB_M1, FB_HX, FB_HU, FB_K, FB_HN, FB_CVEC, FB_A, FB_LO, FB_HI, FB_RB, FB_AN, FB_LON, FB_HIN, FB_BM, FB_FM,
+  FB_FC, FB_COUNT
 };
 constexpr int kRecMats = 6;
 constexpr int kRecSpans = 20;
@@ -57,6 +58,7 @@ struct FusedArgs {
 int fused_smem_bytes(const FusedArgs& F);
 cudaError_t fused_configure(int smem_bytes, int threads);
 void launch_T_fused(const FusedArgs& F, int grid, cudaStream_t st);
+void launch_build_combined(const Dev& D, double* Bm, double* Fm, double* fc, int64_t stride, cudaStream_t st);
 const void* fused_kernel_ptr(int threads);
 
 }  // namespace spock

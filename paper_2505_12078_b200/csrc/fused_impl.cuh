@@ -60,7 +60,8 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 __device__ __forceinline__ void stamp(const FusedArgs& F, int item, int k) {
-  if (F.trace && threadIdx.x == 0) F.trace[size_t(item) * 4 + k] = gtimer();
+  // slots 0..3: %globaltimer (ns, cross-SM ordering); 4..7: clock64 (intra-item phases)
+  if (F.trace && threadIdx.x == 0) F.trace[size_t(item) * 8 + k] = k < 4 ? gtimer() : (unsigned long long)clock64();
 }
 
 __device__ void wait_flag(const int* f) {
@@ -116,6 +117,39 @@ __device__ void cta_gemv(const double* A, int m, int n, int lda, const double* x
   __syncthreads();
 }
 
+// y1 = A1 x1 (m1 rows) and y2 = A2 x2 (m2 rows) in one pass: rows of both are
+// spread over the CTA (column slices, fixed-order reduction)
+__device__ void cta_gemv2(const double* A1, int m1, int n1, int lda1, const double* x1, double* y1,
+                          const double* A2, int m2, int n2, int lda2, const double* x2, double* y2, double* red) {
+  const int t = threadIdx.x, m = m1 + m2;
+  if (m > kFT) {
+    cta_gemv(A1, m1, n1, lda1, x1, y1, false, red);
+    cta_gemv(A2, m2, n2, lda2, x2, y2, false, red);
+    return;
+  }
+  const int slices = max(1, kFT / m);
+  const int r = t % m, s = t / m;
+  double v = 0.0;
+  if (s < slices) {
+    const bool one = r < m1;
+    const double* A = one ? A1 : A2;
+    const double* x = one ? x1 : x2;
+    const int rr = one ? r : r - m1, n = one ? n1 : n2, lda = one ? lda1 : lda2;
+    for (int c = s; c < n; c += slices) v = fma(A[rr + size_t(c) * lda], x[c], v);
+  }
+  if (t < m * slices) red[t] = v;
+  __syncthreads();
+  if (t < m) {
+    double o = 0.0;
+    for (int j = 0; j < slices; ++j) o += red[t + j * m];
+    if (t < m1)
+      y1[t] = o;
+    else
+      y2[t - m1] = o;
+  }
+  __syncthreads();
+}
+
 __device__ double cta_sum(double v, double* red) {
   v = warp_sum(v);
   const int w = threadIdx.x >> 5;
@@ -158,7 +192,7 @@ enum Span : int {
   // backward
   B_HEAD = 0, B_QK, B_ZX, B_ZU, B_EC, B_GD, B_H, B_G, B_HEADN, B_QKN,
   // forward
-  F_ZX = 0, F_ZU, F_AX, F_AU, F_CV, F_SEG2, F_A, F_QK, F_GD, F_LO, F_HI, F_SEG3, F_AN, F_QKN, F_GND, F_LON,
+  F_ZX = 0, F_ZU, F_AX, F_AU, F_FC, F_SEG2, F_A, F_QK, F_GD, F_LO, F_HI, F_SEG3, F_AN, F_QKN, F_GND, F_LON,
   F_HIN, F_SEG1, F_RB
 };
 
@@ -314,6 +348,11 @@ __device__ void item_s2(const FusedArgs& F, int i, double* red, double* vec) {
   __syncthreads();
 }
 
+// Backward item.  Everything that does not depend on the children is done
+// before the flag wait (own adjoint term, G' ec, cst = h - z_x + a gx - K'(z_u - a gu),
+// dc = Rt^-1(z_u - a gu - g)); after it, one parallel GEMV round:
+//   T12_i = [M1_i' | M1_i' K_i'] [S_T1 + a S_adjx + cst ; a S_adju],  d_i = dc - Rt^-1 (a S_adju + S_T2)
+// (offline B_i = [M1_i' | M1_i' K_i'], Engine::build_combined).
 __device__ void item_back(const FusedArgs& F, const ItemRec& P, const Slot& S, double* sc_, double* red) {
   const Dev& D = F.D;
   const int i = P.node;
@@ -322,19 +361,21 @@ __device__ void item_back(const FusedArgs& F, const ItemRec& P, const Slot& S, d
   const double al = F.alpha;
   const double* V = S.vec;
   auto sp = [&](int id) { return V + S.voff[id]; };
-  double* gx = sc_;           // L* (x, u) of this node without the children
-  double* q = gx + kSlot;     // q (nx)
+  double* gx = sc_;           // G' ec (+ leaf terms)
+  double* q = gx + kSlot;     // leaf q / nonleaf v = [v_x; v_u]
   double* tv = q + kSlot;     // scratch (m)
-  double* rhs = tv + kSlot;   // scratch (m)
+  double* rhs = tv + kSlot;   // scratch: ubc, w
+  double* dc = rhs + kSlot;   // Rt^-1 (ubc - g)
+  double* rhs2 = dc + kSlot;  // ubc - g
   const int px = P.px, pu = P.pu;
   int mk = 0;
   const double* HxT = root ? nullptr : S.mp[mk++];
   const double* HuT = root ? nullptr : S.mp[mk++];
-  const double* M1T = root ? nullptr : S.mp[mk++];
+  const double* Mb = root ? nullptr : S.mp[mk++];  // M1' (leaf) or [M1' | M1'K'] (non-leaf)
   const double* KT = leaf ? nullptr : S.mp[mk++];
   const double* Ri = leaf ? nullptr : S.mp[mk++];
   const double* HNT = leaf ? S.mp[mk++] : nullptr;
-  // ---- own G' ec (+ terminal SOC term for leaves); independent of children
+  const int item = F.D.nn - 1 - i;  // ticket of this backward item
   if (!leaf) {
     const int nc = P.nc;
     const double* ec = sp(B_EC);
@@ -374,48 +415,69 @@ __device__ void item_back(const FusedArgs& F, const ItemRec& P, const Slot& S, d
     double* adj = D.adj + size_t(i - 1) * m;
     for (int r = t; r < m; r += kFT) adj[r] = tv[r];
   }
-  if (!leaf) {
-    // ---- children (flags), then q and d
-    const int c0 = P.c0, nch = P.nch;
-    wait_flags_par(F.flagB + c0, nch);
-    stamp(F, F.D.nnl + (F.D.nn - 1 - i), 1);
+  if (leaf) {
+    __syncthreads();
+    cta_gemv(Mb, m, nx, m, q, tv, false, red);  // T12 = M1' q
+    double* T12 = D.T12 + size_t(i - 1) * m;
+    for (int r = t; r < m; r += kFT) T12[r] = tv[r];
+    cta_release(F.flagB + i);
+    stamp(F, item, 2);
+    return;
+  }
+  // ---- non-leaf, before the children: ubc, cst, dc
+  {
     const double* zx = sp(B_ZX);
     const double* zu = sp(B_ZU);
     const double* h = sp(B_H);
     const double* gv = sp(B_G);
-    for (int r = t; r < m; r += kFT) {
-      double lt = gx[r], tq = 0.0;
-      for (int c = 0; c < nch; ++c) {
-        const size_t o = size_t(c0 + c - 1) * m + r;
-        lt += ldcg(D.adj + o);
-        tq += ldcg(D.T12 + o);
-      }
-      if (r < nx) {
-        q[r] = h[r] - (zx[r] - al * lt) + tq;
-      } else {
-        const double ub = zu[r - nx] - al * lt;  // ubar
-        tv[r] = ub;
-        rhs[r - nx] = ub - gv[r - nx] - tq;
-      }
+    for (int r = t; r < nu; r += kFT) {
+      const double ubc = zu[r] - al * gx[nx + r];
+      rhs[r] = ubc;
+      rhs2[r] = ubc - gv[r];
     }
     __syncthreads();
-    cta_gemv(KT, nx, nu, nx, tv + nx, gx, false, red);  // K' ubar (gx reused)
-    for (int r = t; r < nx; r += kFT) q[r] -= gx[r];
-    cta_gemv(Ri, nu, nu, nu, rhs, tv, false, red);  // d
-    double* dv = D.dvec + size_t(i) * nu;
-    for (int r = t; r < nu; r += kFT) dv[r] = tv[r];
+    cta_gemv2(KT, nx, nu, nx, rhs, tv, Ri, nu, nu, nu, rhs2, dc, red);  // K' ubc ; dc
+    for (int r = t; r < nx; r += kFT) q[r] = h[r] - zx[r] + al * gx[r] - tv[r];  // cst (into v_x)
+    __syncthreads();
+  }
+  // ---- children
+  const int c0 = P.c0, nch = P.nch;
+  wait_flags_par(F.flagB + c0, nch);
+  stamp(F, item, 1);
+  stamp(F, item, 4);
+  for (int r = t; r < m; r += kFT) {
+    double sa = 0.0, st = 0.0;
+    for (int c = 0; c < nch; ++c) {
+      const size_t o = size_t(c0 + c - 1) * m + r;
+      sa += ldcg(D.adj + o);
+      st += ldcg(D.T12 + o);
+    }
+    if (r < nx) {
+      q[r] += st + al * sa;  // v_x
+    } else {
+      q[r] = al * sa;               // v_u
+      rhs[r - nx] = al * sa + st;   // w
+    }
   }
   __syncthreads();
+  stamp(F, item, 5);
+  if (!root)
+    cta_gemv2(Mb, m, m, m, q, tv, Ri, nu, nu, nu, rhs, gx, red);  // T12 ; Rt^-1 w
+  else
+    cta_gemv(Ri, nu, nu, nu, rhs, gx, false, red);
+  stamp(F, item, 6);
+  double* dv = D.dvec + size_t(i) * nu;
+  for (int r = t; r < nu; r += kFT) dv[r] = dc[r] - gx[r];
   if (!root) {
-    cta_gemv(M1T, m, nx, m, q, tv, false, red);
     double* T12 = D.T12 + size_t(i - 1) * m;
     for (int r = t; r < m; r += kFT) T12[r] = tv[r];
   } else if (t == 0) {
     const double sc = F.eta[P.s1o + P.ny];
     F.zo[0] = F.z[0] - al * sc - al;  // CP primal step on s0 (solver.cpp:153-154)
   }
+  stamp(F, item, 7);
   cta_release(F.flagB + i);
-  stamp(F, F.D.nnl + (F.D.nn - 1 - i), 2);
+  stamp(F, item, 2);
 }
 
 __device__ void item_fwd(const FusedArgs& F, const ItemRec& P, const Slot& S, double* sc_, double* red) {
@@ -437,18 +499,23 @@ __device__ void item_fwd(const FusedArgs& F, const ItemRec& P, const Slot& S, do
   double* pv = val + kSlot;    // p / alpha
   const int px = P.px, pu = P.pu;
   int mk = 0;
-  const double* M1 = root ? nullptr : S.mp[mk++];
+  const double* Mf = root ? nullptr : S.mp[mk++];  // M1 (leaf) or [M1; K M1] (non-leaf)
   const double* Hx = root ? nullptr : S.mp[mk++];
   const double* Hu = root ? nullptr : S.mp[mk++];
-  const double* K = leaf ? nullptr : S.mp[mk++];
+  const double* K = root ? S.mp[mk++] : nullptr;   // root: u0 = K x_init + d0
   const double* HN = leaf ? S.mp[mk++] : nullptr;
   const int an = root ? 0 : P.anc;
-  // ---- parent forward (root: own backward)
+  if (root) {  // before the dependency: K x_init
+    for (int r = t; r < nx; r += kFT) xn[r] = D.xinit[r];
+    __syncthreads();
+    cta_gemv(K, nu, nx, nu, xn, xn + nx, false, red);
+  }
+  // ---- parent forward (root: own backward), S2 of self and parent
   if (t == 0) wait_flag(root ? F.flagB : F.flagF + an);
   else if (t == 32 && !leaf) wait_flag(F.flagS2 + c);
   else if (t == 64 && !root) wait_flag(F.flagS2 + an);
   __syncthreads();
-  stamp(F, F.D.nnl + F.D.nn + c, 1);
+  stamp(F, F.D.nn + F.D.nnl + c, 1);
   if (!root) {
     const double* zax = sp(F_AX);
     const double* zau = sp(F_AU);
@@ -463,18 +530,13 @@ __device__ void item_fwd(const FusedArgs& F, const ItemRec& P, const Slot& S, do
       }
     }
     __syncthreads();
-    cta_gemv(M1, nx, m, nx, xd, xn, false, red);
-    const double* cv = sp(F_CV);
-    for (int r = t; r < nx; r += kFT) xn[r] += cv[r];
-  } else {
-    for (int r = t; r < nx; r += kFT) xn[r] = D.xinit[r];
+    cta_gemv(Mf, leaf ? nx : m, m, leaf ? nx : m, xd, xn, false, red);  // [x; u - d] = Mf xd
+    const double* fc = sp(F_FC);
+    for (int r = t; r < (leaf ? nx : m); r += kFT) xn[r] += fc[r];
   }
-  __syncthreads();
-  if (!leaf) {
-    cta_gemv(K, nu, nx, nu, xn, xn + nx, false, red);
+  if (!leaf)
     for (int r = t; r < nu; r += kFT) xn[nx + r] += ldcg(D.dvec + size_t(c) * nu + r);
-    __syncthreads();
-  }
+  __syncthreads();
   for (int r = t; r < (leaf ? nx : m); r += kFT) {
     if (r < nx)
       zo[1 + size_t(c) * nx + r] = xn[r];
@@ -483,7 +545,7 @@ __device__ void item_fwd(const FusedArgs& F, const ItemRec& P, const Slot& S, do
   }
   // children need only (x+, u+) and d: publish before the dual work
   cta_release(F.flagF + c);
-  stamp(F, F.D.nnl + F.D.nn + c, 2);
+  stamp(F, F.D.nn + F.D.nnl + c, 2);
   {
     const double* zx = sp(F_ZX);
     const double* zu = sp(F_ZU);

@@ -22,13 +22,21 @@ def main(cfg="c2"):
     s.bench_T(2, use_graph=False, flush_l2=True)
     tr = p.tree
     nn, nnl = tr.num_nodes(), tr.num_nonleaf()
-    st = np.fromfile(path, dtype=np.uint64).reshape(-1, 4).astype(np.float64)
+    raw = np.fromfile(path, dtype=np.uint64).reshape(-1, 8).astype(np.float64)
+    cyc = raw[:, 4:8]
+    st = raw[:, :4]
     t0 = st[st > 0].min()
     st = np.where(st > 0, (st - t0) / 1000.0, np.nan)  # us
     print(f"{cfg}: nodes {nn}, items {len(st)}, T span {np.nanmax(st):.1f} us")
-    s2 = st[:nnl]
+    s2 = st[nn:nn + nnl]
     print(f"S2 items: start {np.nanmin(s2[:,0]):.1f}..{np.nanmax(s2[:,0]):.1f} end max {np.nanmax(s2[:,3]):.1f}")
-    for name, base, order in (("backward", nnl, lambda k: nn - 1 - k), ("forward", nnl + nn, lambda k: k)):
+    c = cyc[:nn]
+    ok = (c[:, 0] > 0) & (c[:, 1] > 0) & (c[:, 2] > 0) & (c[:, 3] > 0)
+    c = c[ok]
+    ph = np.array([c[:, 1] - c[:, 0], c[:, 2] - c[:, 1], c[:, 3] - c[:, 2]])
+    print("backward non-leaf phases (cycles, median): children loads %.0f  GEMV round %.0f  stores %.0f"
+          % tuple(np.median(ph, axis=1)))
+    for name, base, order in (("backward", 0, lambda k: nn - 1 - k), ("forward", nn + nnl, lambda k: k)):
         print(f"-- {name}: stage  nodes  start(min/max)  deps-ok(min/max)  released(min/max)  end(max)")
         for t in (range(tr.horizon, -1, -1) if name == "backward" else range(tr.horizon + 1)):
             nodes = range(tr.stage_begin(t), tr.stage_end(t))
