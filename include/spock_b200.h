@@ -191,10 +191,14 @@ int spock_solver_unscale_primal(spock_solver* s, const double* z_scaled, double*
  * outside the timed events.  Returns total device milliseconds.
  * spock_bench_kernels: average device ms of [L*, S1 sweeps, S2, L+S3, T].
  * spock_traffic_model: algorithmic bytes of the same five launch classes and
- * the number of kernel launches per T. */
+ * the number of kernel launches per T.
+ * spock_solver_t_path: which device schedule computes T -- "fused" (CTA-
+ * granular dataflow kernel, narrow trees), "wide" (warp-granular streaming
+ * dataflow kernel) or "stages" (one launch per tree stage). */
 int spock_bench_T(spock_solver* s, int32_t k, int32_t use_graph, int32_t flush_l2, double* ms_out);
 int spock_bench_kernels(spock_solver* s, int32_t k, int32_t flush_l2, double* ms5);
 int spock_traffic_model(spock_solver* s, double* bytes5, int32_t* launches_per_T);
+const char* spock_solver_t_path(const spock_solver* s);
 
 #ifdef __cplusplus
 }

@@ -208,4 +208,6 @@ int spock_traffic_model(spock_solver* s, double* bytes5, int32_t* launches_per_T
   });
 }
 
+const char* spock_solver_t_path(const spock_solver* s) { return (s && s->eng) ? s->eng->t_path() : ""; }
+
 }  // extern "C"

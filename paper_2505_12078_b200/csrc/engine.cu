@@ -87,6 +87,7 @@ Engine::Engine(const spock_problem_desc* desc, const Params& prm) : prm_(prm) {
   factorize();
   norm_.analytic_bound = analytic_norm_bound(p_, soc_);
   setup_fused();
+  setup_wide();
   power_iteration();
   alpha_ = prm_.alpha > 0.0 ? prm_.alpha : 0.99 / std::max(norm_.estimate, 1e-300);
   CK(cudaStreamSynchronize(st_));
@@ -352,7 +353,85 @@ void Engine::setup_fused() {
   for (int k = 0; k < FB_COUNT; ++k) F.base[k] = bases[k];
 }
 
+// Streaming dataflow T for wide trees (wide.cu): warp-granular items with
+// per-warp TMA rings.  Default for trees the CTA-granular kernel does not take
+// (>= 4096 nodes); SPOCK_T_WIDE=0 selects the per-stage kernels instead,
+// SPOCK_T_WIDE=1 forces it on any tree the fused kernel is not used for.
+void Engine::setup_wide() {
+  wide_ok_ = false;
+  if (fused_ok_) return;
+  const Tree& tr = p_.tree;
+  const int nn = tr.nn(), nnl = tr.nnl();
+  auto knob = [](const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return (v && v[0]) ? std::atoi(v) : dflt;
+  };
+  const int want = knob("SPOCK_T_WIDE", -1);
+  if (want == 0) return;
+  if (want < 0 && nn < 4096) return;
+  int max_nc = 0;
+  for (int i = 0; i < nnl; ++i) max_nc = std::max(max_nc, p_.nc[i]);
+  for (int j = 0; j < tr.nl(); ++j) max_nc = std::max(max_nc, p_.ncN[j]);
+  if (max_nc > kMaxD) return;
+  WideArgs& A = wargs_;
+  A = WideArgs{};
+  A.warps = std::max(1, std::min(8, knob("SPOCK_WIDE_WARPS", 8)));
+  // measured on B200 (profiles/r01_wide_configs.md): two 8-warp CTAs per SM
+  // with 2 x 6 KB slots per warp beat one CTA with deeper rings -- the items'
+  // dependent latency chains, not the bytes in flight, bound a warp
+  A.slots = std::max(1, std::min(8, knob("SPOCK_WIDE_SLOTS", 2)));
+  A.chunk = std::max(512, knob("SPOCK_WIDE_CHUNK", 768)) & ~1;
+  A.vecd = int((std::max({p_.nx + p_.nu, max_nc, max_dense_s2_}) + 2 + 7) & ~7);
+  wide_ctas_ = knob("SPOCK_WIDE_CTAS", 2) >= 2 ? 2 : 1;
+  wide_rows_ = wide_rows(D_, max_nc);
+  int dev = 0, sms = 148, smem_optin = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  CK(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  const int budget = smem_optin / wide_ctas_ - 2048;
+  while (wide_smem_bytes(A.warps, A.slots, A.chunk, A.vecd) > budget && A.chunk > 512) A.chunk = (A.chunk / 2) & ~1;
+  const int bytes = wide_smem_bytes(A.warps, A.slots, A.chunk, A.vecd);
+  if (bytes > smem_optin) return;
+  CK(wide_configure(wide_rows_, wide_ctas_, bytes));
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wide_kernel_ptr(wide_rows_, wide_ctas_), 32 * A.warps,
+                                                   bytes));
+  if (occ < 1) return;
+  // every CTA must be resident (items spin on flags of smaller tickets)
+  wide_grid_ = occ * sms;
+  const int total = nn + nnl + nn;
+  wide_grid_ = std::max(1, std::min(wide_grid_, (total + A.warps - 1) / A.warps));
+  wide_flag_bytes_ = sizeof(int) * size_t(nn + nnl + nn);
+  wide_flags_ = dalloc<int>(size_t(nn + nnl + nn));
+  A.flagB = wide_flags_;
+  A.flagS2 = wide_flags_ + nn;
+  A.flagF = wide_flags_ + nn + nnl;
+  if (knob("SPOCK_WIDE_PROF", 0)) A.prof = dalloc<unsigned long long>(16);
+  wide_ok_ = true;
+}
+
+void Engine::wide_profile(unsigned long long* out) {
+  for (int k = 0; k < 10; ++k) out[k] = 0;
+  if (!wargs_.prof) return;
+  CK(cudaStreamSynchronize(st_));
+  CK(cudaMemcpy(out, wargs_.prof, sizeof(unsigned long long) * 10, cudaMemcpyDeviceToHost));
+}
+
 Engine::~Engine() {
+  if (wargs_.prof) {  // SPOCK_WIDE_PROF=1: per-warp cycle shares of the wide kernel
+    unsigned long long p[10] = {};
+    try {
+      wide_profile(p);
+    } catch (...) {
+    }
+    const double tot = double(p[0] ? p[0] : 1);
+    std::fprintf(stderr,
+                 "[wide prof] warps*launches=%llu total=%.3g cyc  ring-wait %.1f%%  flag-wait %.1f%%  back %.1f%% "
+                 "(%llu, %.0f cyc/item)  s2 %.1f%% (%llu, %.0f)  fwd %.1f%% (%llu, %.0f)\n",
+                 p[9], tot, 100.0 * p[1] / tot, 100.0 * p[2] / tot, 100.0 * p[3] / tot, p[6],
+                 p[6] ? double(p[3]) / p[6] : 0.0, 100.0 * p[4] / tot, p[7], p[7] ? double(p[4]) / p[7] : 0.0,
+                 100.0 * p[5] / tot, p[8], p[8] ? double(p[5]) / p[8] : 0.0);
+  }
   if (bench_graph_) cudaGraphExecDestroy(bench_graph_);
   if (st_) cudaStreamSynchronize(st_);
   for (void* p : allocs_) cudaFree(p);
@@ -649,6 +728,7 @@ void Engine::upload() {
         // N = I - M'(MM')^+ M with a relative eigenvalue threshold on MM'
         const int dim = ny + 2 * n, mr = n + rs.nnu;
         require(dim <= kMaxD, "spock-b200: general risk spec with y+2*children above 256 is not supported");
+        max_dense_s2_ = std::max(max_dense_s2_, dim);
         Mat M(mr, dim);
         for (int c = 0; c < n; ++c) {
           for (int r = 0; r < ny; ++r) M(c, r) = E(r, c);
@@ -951,6 +1031,18 @@ void Engine::T(const double* z, const double* eta, double* zo, double* eo) {
     F.alpha = alpha_;
     CK(cudaMemsetAsync(F.ticket, 0, fused_sync_bytes_, st_));
     launch_T_fused(F, fused_grid_, st_);
+    return;
+  }
+  if (wide_ok_) {
+    WideArgs A = wargs_;
+    A.D = D_;
+    A.z = z;
+    A.eta = eta;
+    A.zo = zo;
+    A.eo = eo;
+    A.alpha = alpha_;
+    CK(cudaMemsetAsync(wide_flags_, 0, wide_flag_bytes_, st_));
+    launch_T_wide(A, wide_rows_, wide_ctas_, wide_grid_, st_);
     return;
   }
   launch_Lt(D_, eta, z, zo, 1.0, -alpha_, -alpha_, st_);

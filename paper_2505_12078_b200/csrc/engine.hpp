@@ -14,6 +14,7 @@
 #include "fused.hpp"
 #include "kernels.hpp"
 #include "model.hpp"
+#include "wide.hpp"
 
 namespace spock {
 
@@ -74,11 +75,15 @@ class Engine {
   double bench_T(int k, bool graph, bool flush);
   void bench_kernels(int k, bool flush, double* ms);
   void traffic(double* bytes) const;
-  int launches_per_T() const { return fused_ok_ ? 1 : 2 + 2 * (p_.tree.horizon + 1) + 1 + 1; }
+  int launches_per_T() const { return (fused_ok_ || wide_ok_) ? 1 : 2 + 2 * (p_.tree.horizon + 1) + 1 + 1; }
+  // SPOCK_WIDE_PROF=1: cycle counters of the wide kernel (summed over warps and launches)
+  void wide_profile(unsigned long long* out10);
+  const char* t_path() const { return fused_ok_ ? "fused" : (wide_ok_ ? "wide" : "stages"); }
 
  private:
   void upload();
   void setup_fused();
+  void setup_wide();
   void factorize();
   void power_iteration();
   void set_xinit(const double* x_orig_host);
@@ -126,6 +131,12 @@ class Engine {
   FusedArgs fargs_{};
   int fused_grid_ = 0;
   size_t fused_sync_bytes_ = 0;
+  bool wide_ok_ = false;
+  WideArgs wargs_{};
+  int wide_grid_ = 0, wide_rows_ = 0, wide_ctas_ = 1;
+  int max_dense_s2_ = 0;
+  int* wide_flags_ = nullptr;
+  size_t wide_flag_bytes_ = 0;
   double* flush_buf_ = nullptr;
   void flush_l2();
 };

@@ -188,6 +188,11 @@ class SpockSolver:
         _raise(self.lib, self.lib.spock_bench_kernels(self.h, int(k), int(flush_l2), out.ctypes.data))
         return out
 
+    @property
+    def t_path(self) -> str:
+        """Device schedule of T: 'fused', 'wide' or 'stages'."""
+        return self.lib.spock_solver_t_path(self.h).decode()
+
     def traffic_model(self):
         """Algorithmic bytes of [L*, S1, S2, L+S3, T] and kernel launches per T."""
         out = np.zeros(5)
