@@ -8,6 +8,8 @@
 //   Engine::solve_b      <- SpockSolver::run           proj/src/solver.cpp:189-350
 #include "engine.hpp"
 
+#include <climits>
+#include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 
@@ -57,8 +59,9 @@ void Params::validate() const {  // proj/src/solver.cpp:9-19
 template <class Ty>
 Ty* Engine::dalloc(size_t n) {
   void* p = nullptr;
-  CK(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(Ty)));
-  CK(cudaMemsetAsync(p, 0, std::max<size_t>(n, 1) * sizeof(Ty), st_));
+  // two spare elements: aligned 16-byte bulk copies of a trailing odd element stay in bounds
+  CK(cudaMalloc(&p, (std::max<size_t>(n, 1) + 2) * sizeof(Ty)));
+  CK(cudaMemsetAsync(p, 0, (std::max<size_t>(n, 1) + 2) * sizeof(Ty), st_));
   allocs_.push_back(p);
   return static_cast<Ty*>(p);
 }
@@ -361,7 +364,7 @@ void Engine::setup_wide() {
   wide_ok_ = false;
   if (fused_ok_) return;
   const Tree& tr = p_.tree;
-  const int nn = tr.nn(), nnl = tr.nnl();
+  const int nn = tr.nn(), nnl = tr.nnl(), nx = p_.nx, nu = p_.nu, m = nx + nu;
   auto knob = [](const char* name, int dflt) {
     const char* v = std::getenv(name);
     return (v && v[0]) ? std::atoi(v) : dflt;
@@ -369,29 +372,177 @@ void Engine::setup_wide() {
   const int want = knob("SPOCK_T_WIDE", -1);
   if (want == 0) return;
   if (want < 0 && nn < 4096) return;
-  int max_nc = 0;
+  int max_nc = 0, max_ny = 0;
   for (int i = 0; i < nnl; ++i) max_nc = std::max(max_nc, p_.nc[i]);
   for (int j = 0; j < tr.nl(); ++j) max_nc = std::max(max_nc, p_.ncN[j]);
+  for (int i = 0; i < nnl; ++i) max_ny = std::max(max_ny, lay_.y_dim[i]);
   if (max_nc > kMaxD) return;
   WideArgs& A = wargs_;
   A = WideArgs{};
   A.warps = std::max(1, std::min(8, knob("SPOCK_WIDE_WARPS", 8)));
-  // measured on B200 (profiles/r01_wide_configs.md): two 8-warp CTAs per SM
-  // with 2 x 6 KB slots per warp beat one CTA with deeper rings -- the items'
-  // dependent latency chains, not the bytes in flight, bound a warp
-  A.slots = std::max(1, std::min(8, knob("SPOCK_WIDE_SLOTS", 2)));
-  A.chunk = std::max(512, knob("SPOCK_WIDE_CHUNK", 768)) & ~1;
-  A.vecd = int((std::max({p_.nx + p_.nu, max_nc, max_dense_s2_}) + 2 + 7) & ~7);
+  {
+    const int sl = std::max(1, std::min(8, knob("SPOCK_WIDE_SLOTS", 2)));
+    A.slots = sl >= 8 ? 8 : (sl >= 4 ? 4 : (sl >= 2 ? 2 : 1));  // power of two
+  }
+  A.chunk = std::max(512, knob("SPOCK_WIDE_CHUNK", 512)) & ~1;
+  A.ycap = std::min(max_ny, 256);
+  A.vecd = int((std::max({m, max_nc, max_dense_s2_, 2 * nu + 2 + A.ycap}) + 2 + 7) & ~7);
   wide_ctas_ = knob("SPOCK_WIDE_CTAS", 2) >= 2 ? 2 : 1;
   wide_rows_ = wide_rows(D_, max_nc);
+  // ---- per-ticket records: [backward nn-1..0][S2 0..nnl-1][forward 0..nn-1]
+  std::vector<int64_t> hxo(std::max(nn - 1, 1)), huo(std::max(nn - 1, 1)), ao(std::max(nn - 1, 1));
+  std::vector<int64_t> hno(std::max(tr.nl(), 1)), aNo(std::max(tr.nl(), 1));
+  {
+    int64_t sx = 0, su = 0, sa = 0;
+    for (int k = 0; k < nn - 1; ++k) {
+      hxo[k] = sx, huo[k] = su, ao[k] = sa;
+      sx += pad2(int64_t(soc_.stage[k].px) * nx);
+      su += pad2(int64_t(soc_.stage[k].pu) * nu);
+      sa += soc_.stage[k].px + soc_.stage[k].pu + 2;
+    }
+    int64_t sh = 0, sb = 0;
+    for (int j = 0; j < tr.nl(); ++j) {
+      hno[j] = sh, aNo[j] = sb;
+      sh += pad2(int64_t(soc_.leaf[j].px) * nx);
+      sb += soc_.leaf[j].px + 2;
+    }
+  }
+  const int total = nn + nnl + nn;
+  std::vector<WRec> recs(static_cast<size_t>(total));
+  auto meta = [&](WRec& R, int kind, int i) {
+    std::memset(&R, 0, sizeof(R));
+    R.kind = kind;
+    R.node = i;
+    R.nch = tr.child_count[i];
+    R.c0 = tr.child_first[i];
+    R.anc = tr.anc[i];
+    if (i > 0) {
+      R.px = soc_.stage[i - 1].px;
+      R.pu = soc_.stage[i - 1].pu;
+      R.s2o = lay_.seg2_off[i - 1];
+    }
+    if (i < nnl) {
+      R.nc = p_.nc[i], R.ny = lay_.y_dim[i], R.so = lay_.seg1_off[i], R.yo = lay_.y_off[i];
+    } else {
+      const int j = i - nnl;
+      R.nc = p_.ncN[j], R.pN = soc_.leaf[j].px, R.so = lay_.seg3_off[j];
+    }
+  };
+  auto mat = [&](WRec& R, const double* p, int rows, int cols) {
+    R.mp[R.nmat] = p;
+    R.mrows[R.nmat] = int16_t(rows);
+    R.mcols[R.nmat] = int16_t(cols);
+    ++R.nmat;
+  };
+  auto span = [&](WRec& R, int id, int base, int64_t off, int64_t cnt) {
+    R.vbase[id] = uint8_t(base);
+    R.voff[id] = int32_t(off);
+    if (cnt > 1024 || off > INT32_MAX) {  // read in place (huge fan-out y blocks)
+      R.unstaged |= 1 << id;
+      R.vcnt[id] = 0;
+    } else {
+      R.vcnt[id] = uint16_t(cnt);
+    }
+    R.nspan = std::max(R.nspan, id + 1);
+  };
+  require(lay_.neta < INT32_MAX && lay_.nz < INT32_MAX, "spock-b200: wide T needs vectors below 2^31 entries");
+  enum { B_HEAD = 0, B_QK, B_ZX, B_ZU, B_EC, B_GD, B_H, B_G };
+  enum { B_SEG3 = B_ZU, B_GDN = B_GD, B_QKN = B_H };
+  enum { F_ZX = 0, F_ZU, F_AX, F_AU, F_CV, F_SEG2, F_A, F_QK, F_SEG1, F_RB, F_GD, F_LO, F_HI, F_ZY, F_ZT, F_ZS };
+  enum { F_SEG3 = F_SEG1, F_AN = F_RB, F_QKN = F_GD, F_GDN = F_LO, F_LON = F_HI, F_HIN = F_ZY };
+  for (int k = 0; k < nn; ++k) {  // backward items
+    const int i = nn - 1 - k;
+    WRec& R = recs[size_t(k)];
+    meta(R, 0, i);
+    const bool leaf = tr.leaf(i), root = i == 0;
+    if (!root) {
+      mat(R, D_.HxT + hxo[i - 1], nx, R.px);
+      mat(R, D_.HuT + huo[i - 1], nu, R.pu);
+      span(R, B_HEAD, WB_ETA, R.s2o, R.px + R.pu + 2);
+      span(R, B_QK, WB_QK, int64_t(i - 1) * m, m);
+    }
+    span(R, B_ZX, WB_Z, 1 + int64_t(i) * nx, nx);
+    if (leaf) {
+      const int j = i - nnl;
+      mat(R, D_.HNT + hno[j], nx, R.pN);
+      span(R, B_SEG3, WB_ETA, R.so, R.nc + R.pN + 2);
+      if (D_.gN_diag) span(R, B_GDN, WB_GDN, int64_t(j) * nx, nx);
+      span(R, B_QKN, WB_QKN, int64_t(j) * nx, nx);
+    } else {
+      mat(R, D_.KT + size_t(i) * D_.k_stride, nx, nu);
+      mat(R, D_.Rinv + size_t(i) * D_.r_stride, nu, nu);
+      span(R, B_ZU, WB_Z, lay_.u_base + int64_t(i) * nu, nu);
+      span(R, B_EC, WB_ETA, R.so + R.ny, 1 + R.nc);
+      if (D_.g_diag) span(R, B_GD, WB_GD, int64_t(i) * m, m);
+      span(R, B_H, WB_H, int64_t(i) * nx, nx);
+      span(R, B_G, WB_G, int64_t(i) * nu, nu);
+    }
+    if (!root) mat(R, D_.M1T + size_t(i - 1) * D_.m1_stride, m, nx);
+  }
+  for (int i = 0; i < nnl; ++i) meta(recs[size_t(nn) + i], 1, i);
+  for (int c = 0; c < nn; ++c) {  // forward items
+    WRec& R = recs[size_t(nn) + nnl + c];
+    meta(R, 2, c);
+    const bool leaf = tr.leaf(c), root = c == 0;
+    const int an = R.anc;
+    span(R, F_ZX, WB_Z, 1 + int64_t(c) * nx, nx);
+    if (!leaf) span(R, F_ZU, WB_Z, lay_.u_base + int64_t(c) * nu, nu);
+    if (!root) {
+      mat(R, D_.M1 + size_t(c - 1) * D_.m1_stride, nx, m);
+      span(R, F_AX, WB_Z, 1 + int64_t(an) * nx, nx);
+      span(R, F_AU, WB_Z, lay_.u_base + int64_t(an) * nu, nu);
+      span(R, F_CV, WB_CV, int64_t(c - 1) * nx, nx);
+      span(R, F_SEG2, WB_ETA, R.s2o, R.px + R.pu + 2);
+      span(R, F_A, WB_A, ao[c - 1], R.px + R.pu + 2);
+      span(R, F_QK, WB_QK, int64_t(c - 1) * m, m);
+      span(R, F_ZT, WB_Z, lay_.tau_base + c - 1, 1);
+    }
+    if (!leaf) mat(R, D_.K + size_t(c) * D_.k_stride, nu, nx);
+    if (!root) {
+      mat(R, D_.Hx + hxo[c - 1], R.px, nx);
+      mat(R, D_.Hu + huo[c - 1], R.pu, nu);
+    }
+    span(R, F_ZS, WB_Z, root ? 0 : lay_.s_base + c - 1, 1);
+    if (!leaf) {
+      const int64_t go = p_.g_off[c];
+      span(R, F_SEG1, WB_ETA, R.so, R.ny + 1 + R.nc);
+      span(R, F_RB, WB_RB, R.yo - D_.y_base, R.ny);
+      if (D_.g_diag) span(R, F_GD, WB_GD, int64_t(c) * m, m);
+      span(R, F_LO, WB_LO, go, R.nc);
+      span(R, F_HI, WB_HI, go, R.nc);
+      span(R, F_ZY, WB_Z, R.yo, R.ny);
+    } else {
+      const int j = c - nnl;
+      const int64_t go = p_.gN_off[j];
+      mat(R, D_.HN + hno[j], R.pN, nx);
+      span(R, F_SEG3, WB_ETA, R.so, R.nc + R.pN + 2);
+      span(R, F_AN, WB_AN, aNo[j], R.pN + 2);
+      span(R, F_QKN, WB_QKN, int64_t(j) * nx, nx);
+      if (D_.gN_diag) span(R, F_GDN, WB_GDN, int64_t(j) * nx, nx);
+      span(R, F_LON, WB_LON, go, R.nc);
+      span(R, F_HIN, WB_HIN, go, R.nc);
+    }
+  }
+  int64_t vmax = 2;
+  for (const WRec& R : recs) {
+    int64_t t = 0;
+    for (int k = 0; k < R.nspan; ++k)
+      if (R.vcnt[k]) t += pad2(R.vcnt[k] + 1);  // + alignment shift (taken from the address)
+    vmax = std::max(vmax, t);
+  }
+  A.vrec = int(pad2(vmax));
   int dev = 0, sms = 148, smem_optin = 0;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   CK(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   const int budget = smem_optin / wide_ctas_ - 2048;
-  while (wide_smem_bytes(A.warps, A.slots, A.chunk, A.vecd) > budget && A.chunk > 512) A.chunk = (A.chunk / 2) & ~1;
-  const int bytes = wide_smem_bytes(A.warps, A.slots, A.chunk, A.vecd);
+  while (wide_smem_bytes(A) > budget && A.chunk > 512) A.chunk = (A.chunk / 2) & ~1;
+  while (wide_smem_bytes(A) > budget && A.warps > 1) --A.warps;
+  const int bytes = wide_smem_bytes(A);
   if (bytes > smem_optin) return;
+  for (WRec& R : recs)  // columns per ring chunk (even; a chunk holds >= 2 columns)
+    for (int k = 0; k < R.nmat; ++k)
+      R.mcc[k] = int16_t(R.mrows[k] > 0 ? std::max(2, (A.chunk / R.mrows[k]) & ~1) : 2);
   CK(wide_configure(wide_rows_, wide_ctas_, bytes));
   int occ = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wide_kernel_ptr(wide_rows_, wide_ctas_), 32 * A.warps,
@@ -399,10 +550,18 @@ void Engine::setup_wide() {
   if (occ < 1) return;
   // every CTA must be resident (items spin on flags of smaller tickets)
   wide_grid_ = occ * sms;
-  const int total = nn + nnl + nn;
   wide_grid_ = std::max(1, std::min(wide_grid_, (total + A.warps - 1) / A.warps));
-  wide_flag_bytes_ = sizeof(int) * size_t(nn + nnl + nn);
-  wide_flags_ = dalloc<int>(size_t(nn + nnl + nn));
+  WRec* drec = nullptr;
+  CK(cudaMalloc(&drec, sizeof(WRec) * recs.size()));
+  allocs_.push_back(drec);
+  CK(cudaMemcpyAsync(drec, recs.data(), sizeof(WRec) * recs.size(), cudaMemcpyHostToDevice, st_));
+  CK(cudaStreamSynchronize(st_));
+  A.recs = drec;
+  A.vb[WB_QK] = D_.qk, A.vb[WB_GD] = D_.gd, A.vb[WB_H] = D_.h, A.vb[WB_G] = D_.g, A.vb[WB_QKN] = D_.qkN;
+  A.vb[WB_GDN] = D_.gNd, A.vb[WB_CV] = D_.cvec, A.vb[WB_A] = D_.a, A.vb[WB_LO] = D_.lo, A.vb[WB_HI] = D_.hi;
+  A.vb[WB_RB] = D_.rb, A.vb[WB_AN] = D_.aN, A.vb[WB_LON] = D_.loN, A.vb[WB_HIN] = D_.hiN;
+  wide_flag_bytes_ = sizeof(int) * size_t(total);
+  wide_flags_ = dalloc<int>(size_t(total));
   A.flagB = wide_flags_;
   A.flagS2 = wide_flags_ + nn;
   A.flagF = wide_flags_ + nn + nnl;
@@ -411,15 +570,15 @@ void Engine::setup_wide() {
 }
 
 void Engine::wide_profile(unsigned long long* out) {
-  for (int k = 0; k < 10; ++k) out[k] = 0;
+  for (int k = 0; k < 13; ++k) out[k] = 0;
   if (!wargs_.prof) return;
   CK(cudaStreamSynchronize(st_));
-  CK(cudaMemcpy(out, wargs_.prof, sizeof(unsigned long long) * 10, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(out, wargs_.prof, sizeof(unsigned long long) * 13, cudaMemcpyDeviceToHost));
 }
 
 Engine::~Engine() {
   if (wargs_.prof) {  // SPOCK_WIDE_PROF=1: per-warp cycle shares of the wide kernel
-    unsigned long long p[10] = {};
+    unsigned long long p[13] = {};
     try {
       wide_profile(p);
     } catch (...) {
@@ -427,10 +586,12 @@ Engine::~Engine() {
     const double tot = double(p[0] ? p[0] : 1);
     std::fprintf(stderr,
                  "[wide prof] warps*launches=%llu total=%.3g cyc  ring-wait %.1f%%  flag-wait %.1f%%  back %.1f%% "
-                 "(%llu, %.0f cyc/item)  s2 %.1f%% (%llu, %.0f)  fwd %.1f%% (%llu, %.0f)\n",
+                 "(%llu, %.0f cyc/item)  s2 %.1f%% (%llu, %.0f)  fwd %.1f%% (%llu, %.0f)  span-wait %.1f%%  "
+                 "refill %.1f%%  record-wait %.1f%%\n",
                  p[9], tot, 100.0 * p[1] / tot, 100.0 * p[2] / tot, 100.0 * p[3] / tot, p[6],
                  p[6] ? double(p[3]) / p[6] : 0.0, 100.0 * p[4] / tot, p[7], p[7] ? double(p[4]) / p[7] : 0.0,
-                 100.0 * p[5] / tot, p[8], p[8] ? double(p[5]) / p[8] : 0.0);
+                 100.0 * p[5] / tot, p[8], p[8] ? double(p[5]) / p[8] : 0.0, 100.0 * p[10] / tot,
+                 100.0 * p[11] / tot, 100.0 * p[12] / tot);
   }
   if (bench_graph_) cudaGraphExecDestroy(bench_graph_);
   if (st_) cudaStreamSynchronize(st_);

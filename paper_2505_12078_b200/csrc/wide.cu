@@ -6,14 +6,20 @@
 // on items with smaller tickets), but sized for trees whose matrices do not fit
 // on chip and whose per-T cost is streaming them once from HBM:
 //
-//  * one item per WARP, tickets assigned round-robin (ticket = warp + k*NW), so
+//  * one item per WARP, tickets assigned round-robin (ticket = warp + j*NW), so
 //    the whole schedule of a warp is known in advance and no CTA barrier sits
 //    on any path (a warp waits only on its own ring and on dependency flags);
+//  * per ticket a 256-byte host-built record (WRec) arrives by bulk copy three
+//    tickets ahead: node metadata, the matrices to stream, the vector spans;
 //  * every node matrix streams through a per-warp ring of S shared-memory
 //    slots, one cp.async.bulk (TMA bulk copy, mbarrier completion) per column
 //    chunk.  Lane 0 runs the producer S chunks ahead of the consumer, across
-//    item boundaries and across dependency waits, so HBM sees S*W chunks per
-//    SM in flight regardless of what the warps are computing;
+//    item boundaries and across dependency waits;
+//  * the item's independent vector operands (z and eta segments, SOC data,
+//    boxes, ...) are staged by bulk copies (16-byte aligned supersets) when the
+//    item starts, in parallel with the dependency-flag waits and the loads of
+//    what other items produced, so an item pays about one memory round trip
+//    before its arithmetic;
 //  * lanes own rows (r = lane + 32k), the chunk is read from shared memory
 //    column by column with the input vector broadcast: fixed summation order,
 //    bitwise run-to-run deterministic.
@@ -38,6 +44,13 @@ namespace spock {
 namespace {
 
 constexpr int kMaxSlots = 8;
+constexpr int kRecSlots = 4;  // record ring: tickets j .. j+3
+
+// span ids (WRec::voff/vcnt/vbase index); leaf items alias the non-leaf ids
+enum : int { B_HEAD = 0, B_QK, B_ZX, B_ZU, B_EC, B_GD, B_H, B_G };
+enum : int { B_SEG3 = B_ZU, B_GDN = B_GD, B_QKN = B_H };
+enum : int { F_ZX = 0, F_ZU, F_AX, F_AU, F_CV, F_SEG2, F_A, F_QK, F_SEG1, F_RB, F_GD, F_LO, F_HI, F_ZY, F_ZT, F_ZS };
+enum : int { F_SEG3 = F_SEG1, F_AN = F_RB, F_QKN = F_GD, F_GDN = F_LO, F_LON = F_HI, F_HIN = F_ZY };
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -75,10 +88,18 @@ __device__ __forceinline__ void st_release(int* p, int v) {
 // data produced by other warps of this launch: L2 only (no stale L1 lines)
 __device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
 
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// poll relaxed (an acquire load invalidates L1 on every poll), then one acquire
+// load of the released value
 __device__ void wait_flag(const int* f) {
-  for (int k = 0; k < 32; ++k)
-    if (ld_acquire(f) >= 1) return;
-  while (ld_acquire(f) < 1) __nanosleep(64);
+  int k = 0;
+  while (ld_relaxed(f) < 1)
+    if (++k > 16) __nanosleep(64);
+  (void)ld_acquire(f);
 }
 // warp barrier (orders every lane's writes before lane 0's), then one release
 // store by lane 0 (st.release is cumulative over the writes it has observed)
@@ -89,84 +110,55 @@ __device__ __forceinline__ void w_release(int* f) {
 
 struct MatD {
   const double* p;
-  int rows, cols;
+  int rows, cols, cc;
 };
-
-// ticket -> (kind, node): 0 backward (node nn-1..0), 1 S2 (parent 0..nnl-1), 2 forward (0..nn-1)
-__device__ __forceinline__ void decode(const Dev& D, int tk, int& kind, int& node) {
-  if (tk < D.nn) {
-    kind = 0;
-    node = D.nn - 1 - tk;
-  } else if (tk < D.nn + D.nnl) {
-    kind = 1;
-    node = tk - D.nn;
-  } else {
-    kind = 2;
-    node = tk - D.nn - D.nnl;
-  }
-}
-
-// The streamed matrices of an item, in the order the item consumes them.
-// Producer and consumer both enumerate this list, so it is the one contract
-// between them.
-__device__ int item_mats(const Dev& D, int kind, int i, MatD* md) {
-  int n = 0;
-  const int nx = D.nx, nu = D.nu, m = nx + nu;
-  const bool root = i == 0, leaf = D.cc[i] == 0;
-  if (kind == 0) {
-    if (!root) {
-      const int k = i - 1;
-      md[n++] = {D.HxT + D.hx_off[k], nx, D.px[k]};
-      md[n++] = {D.HuT + D.hu_off[k], nu, D.pu[k]};
-    }
-    if (leaf) {
-      const int j = i - D.nnl;
-      md[n++] = {D.HNT + D.hn_off[j], nx, D.pN[j]};
-    } else {
-      md[n++] = {D.KT + size_t(i) * D.k_stride, nx, nu};
-      md[n++] = {D.Rinv + size_t(i) * D.r_stride, nu, nu};
-    }
-    if (!root) md[n++] = {D.M1T + size_t(i - 1) * D.m1_stride, m, nx};
-  } else if (kind == 2) {
-    if (!root) md[n++] = {D.M1 + size_t(i - 1) * D.m1_stride, nx, m};
-    if (!leaf) md[n++] = {D.K + size_t(i) * D.k_stride, nu, nx};
-    if (!root) {
-      const int k = i - 1;
-      md[n++] = {D.Hx + D.hx_off[k], D.px[k], nx};
-      md[n++] = {D.Hu + D.hu_off[k], D.pu[k], nu};
-    }
-    if (leaf) {
-      const int j = i - D.nnl;
-      md[n++] = {D.HN + D.hn_off[j], D.pN[j], nx};
-    }
-  }
-  return n;
-}
-
-__device__ __forceinline__ int chunk_cols(int rows, int chunk) { return max(2, (chunk / rows) & ~1); }
 
 // producer cursor of a warp's ring (shared memory, touched by lane 0 only)
 struct Prod {
   uint32_t prod;  // chunks issued
-  int tp, mi, co, nm;
-  MatD md[6];
+  int jp;         // ticket index (of this warp) the producer is on
+  int have;       // matrix list of ticket jp copied from its record
+  int mi, co, nm;
+  MatD md[kWMats];
 };
 
 struct Ring {
   double* buf;
   uint64_t* bar;
   Prod* ps;
-  int S, chunk, stride, total;
+  WRec* rb;  // record ring (kRecSlots)
+  uint64_t* rbar;
+  const WRec* rc;  // record of the item being consumed
+  int mk;          // next streamed matrix of that item
+  int S, sshift, chunk, stride, total, gw;
+  bool prof;
+  int jc;         // ticket index the consumer is on
   uint32_t cons;  // chunks consumed (uniform across the warp)
   long long t_ring, t_flag;  // optional profile: cycles waiting on chunks / dependency flags
+  long long t_span, t_refill;  // ... on staged spans / in the producer
 };
 
-// lane 0: keep S chunks in flight, walking this warp's tickets ahead of the consumer
-__device__ __noinline__ void refill(const Dev& D, Prod* __restrict__ P, uint32_t cons, int S, int chunk,
-                                    double* buf, uint64_t* bar, int stride, int total) {
+// lane 0: keep S chunks in flight, walking this warp's tickets ahead of the
+// consumer (at most two tickets ahead: records are requested three ahead)
+__device__ __forceinline__ void refill(Prod* __restrict__ P, WRec* rb, uint64_t* rbar, uint32_t cons, int jc, int S,
+                                    int chunk, double* buf, uint64_t* bar, int stride, int total, int gw) {
+  // S is a power of two
   while (P->prod < cons + uint32_t(S)) {
     for (;;) {
-      if (P->tp >= total) return;
+      if (gw + P->jp * stride >= total) return;
+      if (!P->have) {
+        if (P->jp > jc + 2) return;
+        const int s = P->jp & (kRecSlots - 1);
+        const uint32_t par = uint32_t(P->jp / kRecSlots) & 1u;
+        while (!mbar_try_wait(&rbar[s], par)) {
+        }
+        const WRec& rc = rb[s];
+        P->nm = rc.nmat;
+        for (int k = 0; k < rc.nmat; ++k) P->md[k] = MatD{rc.mp[k], rc.mrows[k], rc.mcols[k], rc.mcc[k]};
+        P->mi = 0;
+        P->co = 0;
+        P->have = 1;
+      }
       if (P->mi < P->nm) {
         const MatD& M = P->md[P->mi];
         if (M.rows > 0 && P->co < M.cols) break;
@@ -174,23 +166,28 @@ __device__ __noinline__ void refill(const Dev& D, Prod* __restrict__ P, uint32_t
         P->co = 0;
         continue;
       }
-      P->tp += stride;
-      if (P->tp >= total) return;
-      int kind, node;
-      decode(D, P->tp, kind, node);
-      P->nm = item_mats(D, kind, node, P->md);
-      P->mi = 0;
-      P->co = 0;
+      ++P->jp;
+      P->have = 0;
     }
     const MatD M = P->md[P->mi];
-    const int cc = min(chunk_cols(M.rows, chunk), M.cols - P->co);
+    const int cc = min(M.cc, M.cols - P->co);
     const uint32_t bytes = (uint32_t(cc) * uint32_t(M.rows) * 8u + 15u) & ~15u;
-    const int slot = int(P->prod % uint32_t(S));
+    const int slot = int(P->prod & uint32_t(S - 1));
     fence_proxy_async();
     mbar_expect_tx(&bar[slot], bytes);
     bulk_g2s(buf + size_t(slot) * chunk, M.p + size_t(P->co) * M.rows, bytes, &bar[slot]);
     ++P->prod;
     P->co += cc;
+  }
+}
+
+__device__ __forceinline__ void refill_lane0(Ring& R) {
+  long long t0 = 0;
+  if (R.prof) t0 = clock64();
+  if (lane_id() == 0) refill(R.ps, R.rb, R.rbar, R.cons, R.jc, R.S, R.chunk, R.buf, R.bar, R.stride, R.total, R.gw);
+  if (R.prof) {
+    __syncwarp();
+    R.t_refill += clock64() - t0;
   }
 }
 
@@ -224,25 +221,29 @@ __device__ __forceinline__ void gemv_cols(const double* A, int rows, int cc, con
   }
 }
 
-// consume the chunks of one streamed matrix: acc += M x
+// consume the chunks of the item's next streamed matrix (record order): acc += M x
 template <int RR>
-__device__ __forceinline__ void sgemv(const Dev& D, Ring& R, const MatD M, const double* x, double (&acc)[RR]) {
-  if (M.rows <= 0) return;
-  const int ccmax = chunk_cols(M.rows, R.chunk);
-  for (int co = 0; co < M.cols; co += ccmax) {
-    const int cc = min(ccmax, M.cols - co);
-    const int slot = int(R.cons % uint32_t(R.S));
-    const uint32_t par = (R.cons / uint32_t(R.S)) & 1u;
-    if (!mbar_try_wait(&R.bar[slot], par)) {
-      const long long t0 = clock64();
+__device__ __forceinline__ void sgemv(Ring& R, const double* x, double (&acc)[RR]) {
+  const int k = R.mk++;
+  const int rows = R.rc->mrows[k], cols = R.rc->mcols[k], ccmax = R.rc->mcc[k];
+  if (rows <= 0) return;
+  for (int co = 0; co < cols; co += ccmax) {
+    const int cc = min(ccmax, cols - co);
+    const int slot = int(R.cons & uint32_t(R.S - 1));
+    const uint32_t par = (R.cons >> R.sshift) & 1u;
+    if (R.prof) {
+      const long long t0 = clock64();  // try_wait may suspend: time the whole wait
       while (!mbar_try_wait(&R.bar[slot], par)) {
       }
       R.t_ring += clock64() - t0;
+    } else {
+      while (!mbar_try_wait(&R.bar[slot], par)) {
+      }
     }
-    gemv_cols<RR>(R.buf + size_t(slot) * R.chunk, M.rows, cc, x + co, acc);
+    gemv_cols<RR>(R.buf + size_t(slot) * R.chunk, rows, cc, x + co, acc);
     __syncwarp();
     ++R.cons;
-    if (lane_id() == 0) refill(D, R.ps, R.cons, R.S, R.chunk, R.buf, R.bar, R.stride, R.total);
+    refill_lane0(R);
   }
 }
 
@@ -270,7 +271,7 @@ __device__ __forceinline__ void zero(double (&a)[RR]) {
 // translated SOC projection (proj_soc_inplace, projections.cpp:11-24) of
 // (v rows < p, vp, vp1) about a; cone head = rows 0..p, axis vp1
 template <int RR>
-__device__ void soc_proj(double (&v)[RR], int p, double& vp, double& vp1, const double* __restrict__ a) {
+__device__ void soc_proj(double (&v)[RR], int p, double& vp, double& vp1, const double* a) {
   const int l = lane_id();
   double s = 0.0;
 #pragma unroll
@@ -345,32 +346,124 @@ __device__ void ycone(const Dev& D, int i, double* t) {
 }
 
 // ---------------------------------------------------------------------------
-// Backward item of node i.
+// Staged vector operands of one item.
+struct Spans {
+  const WideArgs* A;
+  const WRec* rc;
+  const double* vrec;
+  const int* doff;
+  __device__ __forceinline__ const double* base(int b) const {
+    return b == WB_Z ? A->z : (b == WB_ETA ? A->eta : A->vb[b]);
+  }
+  __device__ __forceinline__ const double* operator()(int id) const {
+    if ((rc->unstaged >> id) & 1) return base(rc->vbase[id]) + rc->voff[id];
+    return vrec + doff[id];
+  }
+};
+
+// lane 0: bulk-copy the item's staged spans (16-byte aligned supersets) into
+// vrec; one mbarrier phase per item (completes at once when nothing is staged)
+__device__ void stage_spans(const WideArgs& A, const WRec& rc, double* vrec, int* doff, uint64_t* sbar) {
+  if (lane_id() != 0) return;
+  // z / eta may be 8-byte aligned sub-vectors (SuperMann's stacked (z | eta)):
+  // the alignment shift is taken from the address
+  int off = 0;
+  uint32_t total = 0;
+  for (int k = 0; k < rc.nspan; ++k) {
+    const int n = rc.vcnt[k];
+    if (((rc.unstaged >> k) & 1) || n == 0) {
+      doff[k] = 0;
+      continue;
+    }
+    const int b = rc.vbase[k];
+    const double* src = (b == WB_Z ? A.z : (b == WB_ETA ? A.eta : A.vb[b])) + rc.voff[k];
+    const int sh = int((reinterpret_cast<uintptr_t>(src) >> 3) & 1);
+    doff[k] = off + sh;
+    off += (n + sh + 1) & ~1;
+  }
+  total = uint32_t(off) * 8u;
+  fence_proxy_async();
+  mbar_expect_tx(sbar, total);
+  off = 0;
+  for (int k = 0; k < rc.nspan; ++k) {
+    const int n = rc.vcnt[k];
+    if (((rc.unstaged >> k) & 1) || n == 0) continue;
+    const int b = rc.vbase[k];
+    const double* src = (b == WB_Z ? A.z : (b == WB_ETA ? A.eta : A.vb[b])) + rc.voff[k];
+    const int sh = int((reinterpret_cast<uintptr_t>(src) >> 3) & 1);
+    const int nn = (n + sh + 1) & ~1;
+    bulk_g2s(vrec + off, src - sh, uint32_t(nn) * 8u, sbar);
+    off += nn;
+  }
+}
+
+struct SpanWait {
+  uint64_t* bar;
+  uint32_t parity;
+};
+__device__ __forceinline__ void spans_ready(Ring& R, const SpanWait& W) {
+  long long t0 = 0;
+  if (R.prof) t0 = clock64();
+  while (!mbar_try_wait(W.bar, W.parity)) {
+  }
+  if (R.prof) R.t_span += clock64() - t0;
+}
+
+// ---------------------------------------------------------------------------
+// Backward item of node i.  Streamed (record order): HxT, HuT (non-root) |
+// HNT (leaf) or KT, Rinv (non-leaf) | M1T (non-root).
 template <int RR>
-__device__ void w_back(const WideArgs& A, Ring& R, int i, double* xs, double* xs2) {
+__device__ void w_back(const WideArgs& A, Ring& R, const WRec& rc, const Spans& sp, const SpanWait& W, double* xs,
+                       double* xs2) {
   const Dev& D = A.D;
   const int l = lane_id(), nx = D.nx, nu = D.nu, m = nx + nu;
   const double al = A.alpha;
-  const double* __restrict__ z = A.z;
-  const double* __restrict__ eta = A.eta;
-  const bool root = i == 0, leaf = D.cc[i] == 0;
-  // streamed matrices, consumed in item_mats order:
-  //   HxT, HuT (non-root) | HNT (leaf) or KT, Rinv (non-leaf) | M1T (non-root)
+  const int i = rc.node;
+  const bool root = i == 0, leaf = rc.nch == 0;
+  // children: flags, then their adj (L* stage-cost terms) and T12 sums
+  double vx[RR], vu[RR], sx[RR], su[RR];
+  zero(vx);
+  zero(vu);
+  zero(sx);
+  zero(su);
+  if (!leaf) {
+    const int c0 = rc.c0, nch = rc.nch;
+    long long t0 = 0;
+    if (R.prof) t0 = clock64();
+    for (int k = l; k < nch; k += 32) wait_flag(A.flagB + c0 + k);
+    __syncwarp();
+    if (R.prof) R.t_flag += clock64() - t0;
+    for (int c = 0; c < nch; ++c) {  // ascending child order (tree_operator.cpp:106-113)
+      const double* ad = D.adj + size_t(c0 + c - 1) * m;
+      const double* T = D.T12 + size_t(c0 + c - 1) * m;
+#pragma unroll
+      for (int kk = 0; kk < RR; ++kk) {
+        const int r = l + 32 * kk;
+        if (r < nx) {
+          vx[kk] += ldcg(ad + r);
+          sx[kk] += ldcg(T + r);
+        }
+        if (r < nu) {
+          vu[kk] += ldcg(ad + nx + r);
+          su[kk] += ldcg(T + nx + r);
+        }
+      }
+    }
+  }
+  spans_ready(R, W);
   double acc[RR];
   if (!root) {  // own stage-SOC adjoint term for the parent (tree_operator.cpp:80-88)
-    const int k = i - 1, px = D.px[k], pu = D.pu[k], p = px + pu;
-    const double* seg = eta + D.s2_off[k];
-    for (int r = l; r < p; r += 32) xs[r] = seg[r];
-    const double rsum = seg[p] + seg[p + 1];
-    const double* qk = D.qk + size_t(k) * m;
+    const int k = i - 1, px = rc.px, pu = rc.pu, p = px + pu;
+    const double* head = sp(B_HEAD);
+    const double rsum = head[p] + head[p + 1];
+    const double* qk = sp(B_QK);
     double* adj = D.adj + size_t(k) * m;
-    __syncwarp();
 #pragma unroll
     for (int kk = 0; kk < RR; ++kk) {
       const int r = l + 32 * kk;
       acc[kk] = r < nx ? -0.5 * rsum * qk[r] : 0.0;
     }
-    sgemv<RR>(D, R, MatD{D.HxT + D.hx_off[k], nx, px}, xs, acc);
+    sgemv<RR>(R, head, acc);
 #pragma unroll
     for (int kk = 0; kk < RR; ++kk) {
       const int r = l + 32 * kk;
@@ -381,38 +474,32 @@ __device__ void w_back(const WideArgs& A, Ring& R, int i, double* xs, double* xs
       const int r = l + 32 * kk;
       acc[kk] = r < nu ? -0.5 * rsum * qk[nx + r] : 0.0;
     }
-    sgemv<RR>(D, R, MatD{D.HuT + D.hu_off[k], nu, pu}, xs + px, acc);
+    sgemv<RR>(R, head + px, acc);
 #pragma unroll
     for (int kk = 0; kk < RR; ++kk) {
       const int r = l + 32 * kk;
       if (r < nu) adj[nx + r] = acc[kk];
     }
-    __syncwarp();
   }
-  const double* zx = z + 1 + size_t(i) * nx;
+  const double* zx = sp(B_ZX);
   if (leaf) {  // L* leaf rows, then q = -xbar and T12 = M1' q
-    const int j = i - D.nnl, nc = D.s3_nc[j], pN = D.pN[j];
-    const double* ec = eta + D.s3_off[j];
+    const int j = i - D.nnl, nc = rc.nc, pN = rc.pN;
+    const double* ec = sp(B_SEG3);
     const double* hd = ec + nc;
     const double rsumN = hd[pN] + hd[pN + 1];
     zero(acc);
     if (D.gN_diag) {
-      const double* gd = D.gNd + size_t(j) * nx;
+      const double* gd = sp(B_GDN);
 #pragma unroll
       for (int kk = 0; kk < RR; ++kk) {
         const int r = l + 32 * kk;
         if (r < nx) acc[kk] = gd[r] * ec[r];
       }
     } else {
-      for (int r = l; r < nc; r += 32) xs[r] = ec[r];
-      __syncwarp();
-      gemv_glob<RR>(D.GNT + D.gN_off[j] * nx, nx, nc, nx, xs, acc);
-      __syncwarp();
+      gemv_glob<RR>(D.GNT + D.gN_off[j] * nx, nx, nc, nx, ec, acc);
     }
-    for (int r = l; r < pN; r += 32) xs2[r] = hd[r];
-    __syncwarp();
-    sgemv<RR>(D, R, MatD{D.HNT + D.hn_off[j], nx, pN}, xs2, acc);
-    const double* qk = D.qkN + size_t(j) * nx;
+    sgemv<RR>(R, hd, acc);
+    const double* qk = sp(B_QKN);
 #pragma unroll
     for (int kk = 0; kk < RR; ++kk) {
       const int r = l + 32 * kk;
@@ -421,7 +508,7 @@ __device__ void w_back(const WideArgs& A, Ring& R, int i, double* xs, double* xs
     __syncwarp();
     if (!root) {
       zero(acc);
-      sgemv<RR>(D, R, MatD{D.M1T + size_t(i - 1) * D.m1_stride, m, nx}, xs, acc);
+      sgemv<RR>(R, xs, acc);
       double* T12 = D.T12 + size_t(i - 1) * m;
 #pragma unroll
       for (int kk = 0; kk < RR; ++kk) {
@@ -432,77 +519,48 @@ __device__ void w_back(const WideArgs& A, Ring& R, int i, double* xs, double* xs
     w_release(A.flagB + i);
     return;
   }
-  // non-leaf: G' ec (before the children), then the children's adj and T12
-  const int nc = D.s1_nc[i], ny = D.y_dim[i], so = D.s1_off[i];
-  const double* ec = eta + so + ny + 1;
-  double vx[RR], vu[RR];
-  zero(vx);
-  zero(vu);
+  // non-leaf: (xbar, ubar) = (z_x, z_u) - alpha (G' ec + sum_c adj_c)
+  const int nc = rc.nc;
+  const double* ecs = sp(B_EC);  // [s-row; constraint rows]
+  const double* ec = ecs + 1;
+  double gx[RR], gu[RR];
+  zero(gx);
+  zero(gu);
   if (D.g_diag) {
-    const double* gd = D.gd + size_t(i) * m;
+    const double* gd = sp(B_GD);
 #pragma unroll
     for (int kk = 0; kk < RR; ++kk) {
       const int r = l + 32 * kk;
-      if (r < nx) vx[kk] = gd[r] * ec[r];
-      if (r < nu) vu[kk] = gd[nx + r] * ec[nx + r];
+      if (r < nx) gx[kk] = gd[r] * ec[r];
+      if (r < nu) gu[kk] = gd[nx + r] * ec[nx + r];
     }
   } else {
-    for (int r = l; r < nc; r += 32) xs[r] = ec[r];
-    __syncwarp();
-    gemv_glob<RR>(D.GxT + D.g_off[i] * nx, nx, nc, nx, xs, vx);
-    gemv_glob<RR>(D.GuT + D.g_off[i] * nu, nu, nc, nu, xs, vu);
-    __syncwarp();
+    gemv_glob<RR>(D.GxT + D.g_off[i] * nx, nx, nc, nx, ec, gx);
+    gemv_glob<RR>(D.GuT + D.g_off[i] * nu, nu, nc, nu, ec, gu);
   }
-  const int c0 = D.cf[i], nch = D.cc[i];
-  {
-    const long long t0 = clock64();
-    for (int k = l; k < nch; k += 32) wait_flag(A.flagB + c0 + k);
-    __syncwarp();
-    R.t_flag += clock64() - t0;
-  }
-  double sx[RR], su[RR];
-  zero(sx);
-  zero(su);
-  for (int c = 0; c < nch; ++c) {  // ascending child order (tree_operator.cpp:106-113)
-    const double* ad = D.adj + size_t(c0 + c - 1) * m;
-    const double* T = D.T12 + size_t(c0 + c - 1) * m;
-#pragma unroll
-    for (int kk = 0; kk < RR; ++kk) {
-      const int r = l + 32 * kk;
-      if (r < nx) {
-        vx[kk] += ldcg(ad + r);
-        sx[kk] += ldcg(T + r);
-      }
-      if (r < nu) {
-        vu[kk] += ldcg(ad + nx + r);
-        su[kk] += ldcg(T + nx + r);
-      }
-    }
-  }
-  // (xbar, ubar) = (z_x, z_u) - alpha L* eta on the node's (x, u) rows
-  const double* zu = z + D.u_base + size_t(i) * nu;
-  const double* gv = D.g + size_t(i) * nu;
+  const double* zu = sp(B_ZU);
+  const double* gv = sp(B_G);
 #pragma unroll
   for (int kk = 0; kk < RR; ++kk) {
     const int r = l + 32 * kk;
     if (r < nu) {
-      const double ub = zu[r] - al * vu[kk];
+      const double ub = zu[r] - al * (gu[kk] + vu[kk]);
       xs[r] = ub;
       xs2[r] = ub - gv[r] - su[kk];
     }
   }
   __syncwarp();
   zero(acc);
-  sgemv<RR>(D, R, MatD{D.KT + size_t(i) * D.k_stride, nx, nu}, xs, acc);  // K' ubar
-  const double* h = D.h + size_t(i) * nx;
+  sgemv<RR>(R, xs, acc);  // K' ubar
+  const double* h = sp(B_H);
   double q[RR];
 #pragma unroll
   for (int kk = 0; kk < RR; ++kk) {
     const int r = l + 32 * kk;
-    q[kk] = r < nx ? h[r] - (zx[r] - al * vx[kk]) - acc[kk] + sx[kk] : 0.0;
+    q[kk] = r < nx ? h[r] - (zx[r] - al * (gx[kk] + vx[kk])) - acc[kk] + sx[kk] : 0.0;
   }
   zero(acc);
-  sgemv<RR>(D, R, MatD{D.Rinv + size_t(i) * D.r_stride, nu, nu}, xs2, acc);  // d = Rt^-1 (ubar - g - sum B'q)
+  sgemv<RR>(R, xs2, acc);  // d = Rt^-1 (ubar - g - sum B'q)
   double* dv = D.dvec + size_t(i) * nu;
 #pragma unroll
   for (int kk = 0; kk < RR; ++kk) {
@@ -518,7 +576,7 @@ __device__ void w_back(const WideArgs& A, Ring& R, int i, double* xs, double* xs
     }
     __syncwarp();
     zero(acc);
-    sgemv<RR>(D, R, MatD{D.M1T + size_t(i - 1) * D.m1_stride, m, nx}, xs, acc);  // T12 = [Abar' q; B' q]
+    sgemv<RR>(R, xs, acc);  // T12 = [Abar' q; B' q]
     double* T12 = D.T12 + size_t(i - 1) * m;
 #pragma unroll
     for (int kk = 0; kk < RR; ++kk) {
@@ -526,7 +584,7 @@ __device__ void w_back(const WideArgs& A, Ring& R, int i, double* xs, double* xs
       if (r < m) T12[r] = acc[kk];
     }
   } else if (l == 0) {
-    A.zo[0] = z[0] - al * eta[so + ny] - al;  // CP primal step on s0 (solver.cpp:153-154)
+    A.zo[0] = A.z[0] - al * ecs[0] - al;  // CP primal step on s0 (solver.cpp:153-154)
   }
   w_release(A.flagB + i);
 }
@@ -619,42 +677,58 @@ __device__ void w_s2(const WideArgs& A, int i, double* xs) {
 
 // ---------------------------------------------------------------------------
 // Forward item of node c: S1 forward step, then every dual segment owned by c.
+// Streamed (record order): M1 (non-root) | K (non-leaf) | Hx, Hu (non-root) |
+// HN (leaf).  dep: [u+_anc (nu) | d_c (nu) | tau+_c | s+_c | y+_c (ny <= ycap)]
 template <int RR>
-__device__ void w_fwd(const WideArgs& A, Ring& R, int c, double* xs, double* xs2) {
+__device__ void w_fwd(const WideArgs& A, Ring& R, const WRec& rc, const Spans& sp, const SpanWait& W, double* xs,
+                      double* xs2, double* dep) {
   const Dev& D = A.D;
   const int l = lane_id(), nx = D.nx, nu = D.nu;
   const double al = A.alpha;
-  const double* __restrict__ z = A.z;
-  const double* __restrict__ eta = A.eta;
   double* zo = A.zo;
   double* eo = A.eo;
-  const bool root = c == 0, leaf = D.cc[c] == 0;
-  // streamed matrices, consumed in item_mats order:
-  //   M1 (non-root) | K (non-leaf) | Hx, Hu (non-root) | HN (leaf)
+  const int c = rc.node;
+  const bool root = c == 0, leaf = rc.nch == 0;
+  const int an = root ? 0 : rc.anc;
+  const int ny = leaf ? 0 : rc.ny;
+  const bool ystage = ny <= A.ycap;
+  // dependencies: parent forward (root: the root's backward item), S2 of c and of the parent
+  {
+    long long t0 = 0;
+    if (R.prof) t0 = clock64();
+    if (l == 0) wait_flag(root ? A.flagB : A.flagF + an);
+    if (l == 1 && !leaf) wait_flag(A.flagS2 + c);
+    if (l == 2 && !root) wait_flag(A.flagS2 + an);
+    __syncwarp();
+    if (R.prof) R.t_flag += clock64() - t0;
+  }
+  // everything other items produced for this one, in one batch of L2 loads
+  if (!root) {
+    for (int r = l; r < nx; r += 32) xs[r] = ldcg(zo + 1 + size_t(an) * nx + r);
+    for (int r = l; r < nu; r += 32) {
+      xs[nx + r] = ldcg(D.dvec + size_t(an) * nu + r);
+      dep[r] = ldcg(zo + D.u_base + size_t(an) * nu + r);
+    }
+    if (l == 0) dep[2 * nu] = ldcg(zo + D.tau_base + c - 1);
+  }
+  if (!leaf)
+    for (int r = l; r < nu; r += 32) dep[nu + r] = ldcg(D.dvec + size_t(c) * nu + r);
+  if (l == 0) dep[2 * nu + 1] = ldcg(zo + (root ? 0 : D.s_base + c - 1));
+  if (ystage)
+    for (int r = l; r < ny; r += 32) dep[2 * nu + 2 + r] = ldcg(zo + rc.yo + r);
+  spans_ready(R, W);
   double x[RR], u[RR];
   zero(u);
-  const int an = root ? 0 : D.anc[c];
   if (root) {
-    const long long t0 = clock64();
-    if (l == 0) wait_flag(A.flagB);
-    __syncwarp();
-    R.t_flag += clock64() - t0;
 #pragma unroll
     for (int kk = 0; kk < RR; ++kk) {
       const int r = l + 32 * kk;
       x[kk] = r < nx ? D.xinit[r] : 0.0;
     }
   } else {
-    const long long t0 = clock64();
-    if (l == 0) wait_flag(A.flagF + an);
-    __syncwarp();
-    R.t_flag += clock64() - t0;
-    for (int r = l; r < nx; r += 32) xs[r] = ldcg(zo + 1 + size_t(an) * nx + r);
-    for (int r = l; r < nu; r += 32) xs[nx + r] = ldcg(D.dvec + size_t(an) * nu + r);
-    __syncwarp();
     zero(x);
-    sgemv<RR>(D, R, MatD{D.M1 + size_t(c - 1) * D.m1_stride, nx, nx + nu}, xs, x);  // [Abar B][x_anc; d_anc]
-    const double* cv = D.cvec + size_t(c - 1) * nx;
+    sgemv<RR>(R, xs, x);  // [Abar B][x_anc; d_anc]
+    const double* cv = sp(F_CV);
 #pragma unroll
     for (int kk = 0; kk < RR; ++kk) {
       const int r = l + 32 * kk;
@@ -667,20 +741,18 @@ __device__ void w_fwd(const WideArgs& A, Ring& R, int c, double* xs, double* xs2
     if (r < nx) zo[1 + size_t(c) * nx + r] = x[kk];
   }
   if (!leaf) {
-    __syncwarp();
 #pragma unroll
     for (int kk = 0; kk < RR; ++kk) {
       const int r = l + 32 * kk;
       if (r < nx) xs2[r] = x[kk];
     }
     __syncwarp();
-    sgemv<RR>(D, R, MatD{D.K + size_t(c) * D.k_stride, nu, nx}, xs2, u);  // K x
-    const double* dv = D.dvec + size_t(c) * nu;
+    sgemv<RR>(R, xs2, u);  // K x
 #pragma unroll
     for (int kk = 0; kk < RR; ++kk) {
       const int r = l + 32 * kk;
       if (r < nu) {
-        u[kk] += ldcg(dv + r);
+        u[kk] += dep[nu + r];
         zo[D.u_base + size_t(c) * nu + r] = u[kk];
       }
     }
@@ -688,19 +760,10 @@ __device__ void w_fwd(const WideArgs& A, Ring& R, int c, double* xs, double* xs2
   w_release(A.flagF + c);  // children need only (x+, u+) and d
   // ---- dual update on the segments owned by c (k_L<DUAL>): p = eta + a L w,
   // w = 2 z+ - z, eta+ = p - a Pi_S3(p / a)
-  {
-    const long long t0 = clock64();
-    if (l == 0 && !leaf) wait_flag(A.flagS2 + c);
-    if (l == 1 && !root) wait_flag(A.flagS2 + an);
-    __syncwarp();
-    R.t_flag += clock64() - t0;
-  }
-  auto W = [&](int idx) { return 2.0 * ldcg(zo + idx) - z[idx]; };
-  // own (x^, u^) in registers
   double hx[RR], hu[RR];
   {
-    const double* zx = z + 1 + size_t(c) * nx;
-    const double* zu = z + D.u_base + size_t(c) * nu;
+    const double* zx = sp(F_ZX);
+    const double* zu = leaf ? nullptr : sp(F_ZU);
 #pragma unroll
     for (int kk = 0; kk < RR; ++kk) {
       const int r = l + 32 * kk;
@@ -708,104 +771,103 @@ __device__ void w_fwd(const WideArgs& A, Ring& R, int c, double* xs, double* xs2
       hu[kk] = (!leaf && r < nu) ? 2.0 * u[kk] - zu[r] : 0.0;
     }
   }
+  const double hs = 2.0 * dep[2 * nu + 1] - sp(F_ZS)[0];  // w on s_c
   double acc[RR];
   if (!leaf) {
-    const int ny = D.y_dim[c], yo = D.y_off[c], so = D.s1_off[c];
-    const double* rb = D.rb + (yo - D.y_base);
+    const int so = rc.so;
+    const double* seg1 = sp(F_SEG1);
+    const double* rb = sp(F_RB);
+    const double* zy = sp(F_ZY);
+    auto hy = [&](int r) { return 2.0 * (ystage ? dep[2 * nu + 2 + r] : ldcg(zo + rc.yo + r)) - zy[r]; };
     double part = 0.0;
     for (int r = l; r < ny; r += 32) {
-      const double yv = W(yo + r);
+      const double yv = hy(r);
       part += rb[r] * yv;
-      eo[so + r] = (eta[so + r] + al * yv) / al;  // staged p/a, projected below
+      eo[so + r] = (seg1[r] + al * yv) / al;  // staged p/a, projected below
     }
     const double by = warp_sum(part);
     __syncwarp();
     ycone(D, c, eo + so);
     for (int r = l; r < ny; r += 32) {
-      const double pv = eta[so + r] + al * W(yo + r);
+      const double pv = seg1[r] + al * hy(r);
       eo[so + r] = pv - al * eo[so + r];
     }
     if (l == 0) {
-      const double sv = W(root ? 0 : D.s_base + c - 1) - by;
-      const double pv = eta[so + ny] + al * sv;
+      const double pv = seg1[ny] + al * (hs - by);
       eo[so + ny] = pv - al * fmax(0.0, pv / al);
     }
-    const int nc = D.s1_nc[c];
+    const int nc = rc.nc;
     zero(acc);
-    if (D.g_diag) {
-      const double* gd = D.gd + size_t(c) * (nx + nu);
-      // constraint row r < nx uses x^_r, rows nx.. use u^ (diagonal [Gx Gu])
+#pragma unroll
+    for (int kk = 0; kk < RR; ++kk) {
+      const int r = l + 32 * kk;
+      if (r < nx) xs2[r] = hx[kk];
+      if (r < nu) xs2[nx + r] = hu[kk];
+    }
+    __syncwarp();
+    if (D.g_diag) {  // constraint row r uses [x^; u^]_r (diagonal [Gx Gu])
+      const double* gd = sp(F_GD);
 #pragma unroll
       for (int kk = 0; kk < RR; ++kk) {
         const int r = l + 32 * kk;
-        if (r < nx) xs[r] = hx[kk];
-        if (r < nu) xs[nx + r] = hu[kk];
-      }
-      __syncwarp();
-#pragma unroll
-      for (int kk = 0; kk < RR; ++kk) {
-        const int r = l + 32 * kk;
-        if (r < nc) acc[kk] = gd[r] * xs[r];
+        if (r < nc) acc[kk] = gd[r] * xs2[r];
       }
     } else {
-#pragma unroll
-      for (int kk = 0; kk < RR; ++kk) {
-        const int r = l + 32 * kk;
-        if (r < nx) xs[r] = hx[kk];
-        if (r < nu) xs[nx + r] = hu[kk];
-      }
-      __syncwarp();
-      gemv_glob<RR>(D.Gx + D.g_off[c] * nx, nc, nx, nc, xs, acc);
-      gemv_glob<RR>(D.Gu + D.g_off[c] * nu, nc, nu, nc, xs + nx, acc);
+      gemv_glob<RR>(D.Gx + D.g_off[c] * nx, nc, nx, nc, xs2, acc);
+      gemv_glob<RR>(D.Gu + D.g_off[c] * nu, nc, nu, nc, xs2 + nx, acc);
     }
-    const double* lo = D.lo + D.g_off[c];
-    const double* hi = D.hi + D.g_off[c];
+    const double* lo = sp(F_LO);
+    const double* hi = sp(F_HI);
+    const double* ec = seg1 + ny + 1;
     const int co = so + ny + 1;
 #pragma unroll
     for (int kk = 0; kk < RR; ++kk) {
       const int r = l + 32 * kk;
       if (r < nc) {
-        const double pv = eta[co + r] + al * acc[kk];
+        const double pv = ec[r] + al * acc[kk];
         eo[co + r] = pv - al * fmin(fmax(pv / al, lo[r]), hi[r]);
       }
     }
     __syncwarp();
   }
   if (!root) {  // stage-cost SOC block of (x^_anc, u^_anc, tau^_c)
-    const int k = c - 1, px = D.px[k], pu = D.pu[k], p = px + pu;
-    for (int r = l; r < nx; r += 32) xs[r] = W(1 + an * nx + r);
-    for (int r = l; r < nu; r += 32) xs[nx + r] = W(D.u_base + an * nu + r);
+    const int px = rc.px, pu = rc.pu, p = px + pu, so = rc.s2o;
+    const double* zax = sp(F_AX);
+    const double* zau = sp(F_AU);
+    // xs holds [x+_anc; d_anc]: w_anc = [2 x+_anc - z_x; 2 u+_anc - z_u] into xs2
+    for (int r = l; r < nx; r += 32) xs2[r] = 2.0 * xs[r] - zax[r];
+    for (int r = l; r < nu; r += 32) xs2[nx + r] = 2.0 * dep[r] - zau[r];
     __syncwarp();
-    const double* qk = D.qk + size_t(k) * (nx + nu);
+    const double* qk = sp(F_QK);
     double part = 0.0;
-    for (int r = l; r < nx + nu; r += 32) part += qk[r] * xs[r];
+    for (int r = l; r < nx + nu; r += 32) part += qk[r] * xs2[r];
     const double qd = warp_sum(part);
-    const double row = 0.5 * W(D.tau_base + k) - 0.5 * qd;
+    const double row = 0.5 * (2.0 * dep[2 * nu] - sp(F_ZT)[0]) - 0.5 * qd;
     double ax[RR], au[RR];
     zero(ax);
     zero(au);
-    sgemv<RR>(D, R, MatD{D.Hx + D.hx_off[k], px, nx}, xs, ax);       // Hx x^
-    sgemv<RR>(D, R, MatD{D.Hu + D.hu_off[k], pu, nu}, xs + nx, au);  // Hu u^
-    __syncwarp();
+    sgemv<RR>(R, xs2, ax);       // Hx x^
+    sgemv<RR>(R, xs2 + nx, au);  // Hu u^
+    // realign [Hx x^; Hu u^] (p rows) through shared memory
 #pragma unroll
     for (int kk = 0; kk < RR; ++kk) {
       const int r = l + 32 * kk;
-      if (r < px) xs2[r] = ax[kk];
-      if (r < pu) xs2[px + r] = au[kk];
+      if (r < px) xs[r] = ax[kk];
+      if (r < pu) xs[px + r] = au[kk];
     }
     __syncwarp();
-    const int so = D.s2_off[k];
+    const double* seg2 = sp(F_SEG2);
 #pragma unroll
     for (int kk = 0; kk < RR; ++kk) {
       const int r = l + 32 * kk;
-      acc[kk] = r < p ? eta[so + r] + al * xs2[r] : 0.0;
+      acc[kk] = r < p ? seg2[r] + al * xs[r] : 0.0;
     }
-    double vp = eta[so + p] + al * row, vp1 = eta[so + p + 1] + al * row;
+    double vp = seg2[p] + al * row, vp1 = seg2[p + 1] + al * row;
     double t[RR];
 #pragma unroll
     for (int kk = 0; kk < RR; ++kk) t[kk] = acc[kk] / al;
     double tp = vp / al, tp1 = vp1 / al;
-    soc_proj<RR>(t, p, tp, tp1, D.a + D.a_off[k]);
+    soc_proj<RR>(t, p, tp, tp1, sp(F_A));
 #pragma unroll
     for (int kk = 0; kk < RR; ++kk) {
       const int r = l + 32 * kk;
@@ -818,53 +880,55 @@ __device__ void w_fwd(const WideArgs& A, Ring& R, int c, double* xs, double* xs2
     __syncwarp();
   }
   if (leaf) {  // G_N x^ (box) and the terminal SOC block of (x^, s^)
-    const int j = c - D.nnl, nc = D.s3_nc[j], p = D.pN[j], eo3 = D.s3_off[j];
+    const int j = c - D.nnl, nc = rc.nc, p = rc.pN, eo3 = rc.so;
+    const double* seg3 = sp(F_SEG3);
 #pragma unroll
     for (int kk = 0; kk < RR; ++kk) {
       const int r = l + 32 * kk;
-      if (r < nx) xs[r] = hx[kk];
+      if (r < nx) xs2[r] = hx[kk];
     }
     __syncwarp();
     zero(acc);
     if (D.gN_diag) {
-      const double* gd = D.gNd + size_t(j) * nx;
+      const double* gd = sp(F_GDN);
 #pragma unroll
       for (int kk = 0; kk < RR; ++kk) {
         const int r = l + 32 * kk;
-        if (r < nc) acc[kk] = gd[r] * xs[r];
+        if (r < nc) acc[kk] = gd[r] * xs2[r];
       }
     } else {
-      gemv_glob<RR>(D.GN + D.gN_off[j] * nx, nc, nx, nc, xs, acc);
+      gemv_glob<RR>(D.GN + D.gN_off[j] * nx, nc, nx, nc, xs2, acc);
     }
-    const double* lo = D.loN + D.gN_off[j];
-    const double* hi = D.hiN + D.gN_off[j];
+    const double* lo = sp(F_LON);
+    const double* hi = sp(F_HIN);
 #pragma unroll
     for (int kk = 0; kk < RR; ++kk) {
       const int r = l + 32 * kk;
       if (r < nc) {
-        const double pv = eta[eo3 + r] + al * acc[kk];
+        const double pv = seg3[r] + al * acc[kk];
         eo[eo3 + r] = pv - al * fmin(fmax(pv / al, lo[r]), hi[r]);
       }
     }
-    const double* qk = D.qkN + size_t(j) * nx;
+    const double* qk = sp(F_QKN);
     double part = 0.0;
-    for (int r = l; r < nx; r += 32) part += qk[r] * xs[r];
+    for (int r = l; r < nx; r += 32) part += qk[r] * xs2[r];
     const double qd = warp_sum(part);
-    const double row = 0.5 * W(D.s_base + c - 1) - 0.5 * qd;
+    const double row = 0.5 * hs - 0.5 * qd;
     zero(acc);
-    sgemv<RR>(D, R, MatD{D.HN + D.hn_off[j], p, nx}, xs, acc);  // H_N x^
-    const int so = eo3 + nc;
+    sgemv<RR>(R, xs2, acc);  // H_N x^
+    const double* hseg = seg3 + nc;
 #pragma unroll
     for (int kk = 0; kk < RR; ++kk) {
       const int r = l + 32 * kk;
-      acc[kk] = r < p ? eta[so + r] + al * acc[kk] : 0.0;
+      acc[kk] = r < p ? hseg[r] + al * acc[kk] : 0.0;
     }
-    double vp = eta[so + p] + al * row, vp1 = eta[so + p + 1] + al * row;
+    double vp = hseg[p] + al * row, vp1 = hseg[p + 1] + al * row;
     double t[RR];
 #pragma unroll
     for (int kk = 0; kk < RR; ++kk) t[kk] = acc[kk] / al;
     double tp = vp / al, tp1 = vp1 / al;
-    soc_proj<RR>(t, p, tp, tp1, D.aN + D.aN_off[j]);
+    soc_proj<RR>(t, p, tp, tp1, sp(F_AN));
+    const int so = eo3 + nc;
 #pragma unroll
     for (int kk = 0; kk < RR; ++kk) {
       const int r = l + 32 * kk;
@@ -877,62 +941,111 @@ __device__ void w_fwd(const WideArgs& A, Ring& R, int c, double* xs, double* xs2
   }
 }
 
+// per-warp shared-memory footprint in doubles (16-byte multiples)
+__host__ __device__ __forceinline__ size_t warp_doubles(int S, int CH, int VR, int VD) {
+  return size_t(S) * CH + size_t(VR) + 3 * size_t(VD) + kRecSlots * 32 + 8 /*doff*/ + kMaxSlots + kRecSlots + 2;
+}
+
 template <int RR, int MINB>
 __global__ void __launch_bounds__(256, MINB) k_T_wide(const __grid_constant__ WideArgs A) {
   extern __shared__ __align__(128) double wsm[];
   const Dev& D = A.D;
   const int w = threadIdx.x >> 5, l = lane_id();
-  const int W = A.warps, S = A.slots, CH = A.chunk, VD = A.vecd;
-  double* ring = wsm + size_t(w) * S * CH;
-  double* xs = wsm + size_t(W) * S * CH + size_t(w) * 2 * VD;
+  const int S = A.slots, CH = A.chunk, VR = A.vrec, VD = A.vecd;
+  double* ring = wsm + size_t(w) * warp_doubles(S, CH, VR, VD);
+  double* vrec = ring + size_t(S) * CH;
+  double* xs = vrec + VR;
   double* xs2 = xs + VD;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(wsm + size_t(W) * S * CH + size_t(W) * 2 * VD) + w * kMaxSlots;
+  double* dep = xs2 + VD;
+  WRec* rb = reinterpret_cast<WRec*>(dep + VD);
+  int* doff = reinterpret_cast<int*>(reinterpret_cast<double*>(rb) + kRecSlots * 32);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<double*>(doff) + 8);
+  uint64_t* rbar = bars + kMaxSlots;
+  uint64_t* sbar = rbar + kRecSlots;
   __shared__ Prod prods[8];
   Prod* P = &prods[w];
   Ring R;
   R.ps = P;
   R.buf = ring;
   R.bar = bars;
+  R.rb = rb;
+  R.rbar = rbar;
   R.S = S;
+  R.sshift = __ffs(S) - 1;
   R.chunk = CH;
-  R.stride = gridDim.x * W;
+  R.prof = A.prof != nullptr;
+  R.rc = nullptr;
+  R.mk = 0;
+  R.stride = gridDim.x * A.warps;
   R.total = D.nn + D.nnl + D.nn;
+  R.gw = blockIdx.x * A.warps + w;
+  R.jc = 0;
   R.cons = 0;
   R.t_ring = 0;
   R.t_flag = 0;
-  const int gw = blockIdx.x * W + w;
+  R.t_span = 0;
+  R.t_refill = 0;
+  long long t_rec = 0;
+  auto request = [&](int j) {  // lane 0: bulk copy of the record of ticket index j
+    const int tk = R.gw + j * R.stride;
+    if (tk >= R.total) return;
+    const int s = j & (kRecSlots - 1);
+    fence_proxy_async();
+    mbar_expect_tx(&rbar[s], uint32_t(sizeof(WRec)));
+    bulk_g2s(&rb[s], A.recs + tk, uint32_t(sizeof(WRec)), &rbar[s]);
+  };
   if (l == 0) {
-    for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < kMaxSlots; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < kRecSlots; ++s) mbar_init(&rbar[s], 1);
+    mbar_init(sbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     P->prod = 0;
-    P->tp = gw;
-    P->mi = 0;
-    P->co = 0;
-    P->nm = 0;
-    if (gw < R.total) {
-      int kind, node;
-      decode(D, gw, kind, node);
-      P->nm = item_mats(D, kind, node, P->md);
-    }
-    refill(D, P, 0u, S, CH, ring, bars, R.stride, R.total);
+    P->jp = 0;
+    P->have = 0;
+    P->mi = P->co = P->nm = 0;
+    request(0);
+    request(1);
+    request(2);
   }
   __syncwarp();
   long long t_kind[3] = {0, 0, 0};
   int n_kind[3] = {0, 0, 0};
-  const long long t_start = clock64();
-  for (int tk = gw; tk < R.total; tk += R.stride) {
-    int kind, node;
-    decode(D, tk, kind, node);
-    const long long t0 = clock64();
-    if (kind == 0)
-      w_back<RR>(A, R, node, xs, xs2);
-    else if (kind == 1)
-      w_s2(A, node, xs);
-    else
-      w_fwd<RR>(A, R, node, xs, xs2);
+  const long long t_start = R.prof ? clock64() : 0;
+  for (int j = 0; R.gw + j * R.stride < R.total; ++j) {
+    R.jc = j;
+    if (l == 0) request(j + 3);
+    refill_lane0(R);
+    const int s = j & (kRecSlots - 1);
+    const uint32_t par = uint32_t(j / kRecSlots) & 1u;
+    {
+      long long t0 = 0;
+      if (R.prof) t0 = clock64();
+      while (!mbar_try_wait(&rbar[s], par)) {
+      }
+      if (R.prof) t_rec += clock64() - t0;
+    }
+    const WRec& rc = rb[s];
+    long long t0 = 0;
+    if (R.prof) t0 = clock64();
+    const int kind = rc.kind;
+    R.rc = &rc;
+    R.mk = 0;
+    stage_spans(A, rc, vrec, doff, sbar);
     __syncwarp();
-    t_kind[kind] += clock64() - t0;
-    ++n_kind[kind];
+    const SpanWait W{sbar, uint32_t(j) & 1u};
+    Spans sp{&A, &rc, vrec, doff};
+    if (kind == 0)
+      w_back<RR>(A, R, rc, sp, W, xs, xs2);
+    else if (kind == 1)
+      w_s2(A, rc.node, xs);
+    else
+      w_fwd<RR>(A, R, rc, sp, W, xs, xs2, dep);
+    if (kind == 1) spans_ready(R, W);  // keep the span barrier's phase in step
+    __syncwarp();
+    if (R.prof) {
+      t_kind[kind] += clock64() - t0;
+      ++n_kind[kind];
+    }
   }
   if (A.prof && l == 0) {  // optional: per-warp cycle accounting, summed over warps
     unsigned long long* pf = A.prof;
@@ -944,14 +1057,16 @@ __global__ void __launch_bounds__(256, MINB) k_T_wide(const __grid_constant__ Wi
       atomicAdd(pf + 6 + k, (unsigned long long)n_kind[k]);
     }
     atomicAdd(pf + 9, 1ull);
+    atomicAdd(pf + 10, (unsigned long long)R.t_span);
+    atomicAdd(pf + 11, (unsigned long long)R.t_refill);
+    atomicAdd(pf + 12, (unsigned long long)t_rec);
   }
 }
 
 }  // namespace
 
-int wide_smem_bytes(int warps, int slots, int chunk, int vecd) {
-  return int(sizeof(double) * (size_t(warps) * slots * chunk + size_t(warps) * 2 * vecd) +
-             sizeof(uint64_t) * size_t(warps) * kMaxSlots);
+int wide_smem_bytes(const WideArgs& A) {
+  return int(sizeof(double) * size_t(A.warps) * warp_doubles(A.slots, A.chunk, A.vrec, A.vecd));
 }
 
 int wide_rows(const Dev& D, int max_nc) {
@@ -964,25 +1079,25 @@ int wide_rows(const Dev& D, int max_nc) {
   return 8;
 }
 
-#define WIDE_SWITCH(rows, ctas, F)                    \
-  do {                                                \
-    if (ctas >= 2) {                                  \
-      switch (rows) {                                 \
-        case 1: F(1, 2); break;                       \
-        case 2: F(2, 2); break;                       \
-        case 3: F(3, 2); break;                       \
-        case 4: F(4, 2); break;                       \
-        default: F(8, 2); break;                      \
-      }                                               \
-    } else {                                          \
-      switch (rows) {                                 \
-        case 1: F(1, 1); break;                       \
-        case 2: F(2, 1); break;                       \
-        case 3: F(3, 1); break;                       \
-        case 4: F(4, 1); break;                       \
-        default: F(8, 1); break;                      \
-      }                                               \
-    }                                                 \
+#define WIDE_SWITCH(rows, ctas, F) \
+  do {                             \
+    if (ctas >= 2) {               \
+      switch (rows) {              \
+        case 1: F(1, 2); break;    \
+        case 2: F(2, 2); break;    \
+        case 3: F(3, 2); break;    \
+        case 4: F(4, 2); break;    \
+        default: F(8, 2); break;   \
+      }                            \
+    } else {                       \
+      switch (rows) {              \
+        case 1: F(1, 1); break;    \
+        case 2: F(2, 1); break;    \
+        case 3: F(3, 1); break;    \
+        case 4: F(4, 1); break;    \
+        default: F(8, 1); break;   \
+      }                            \
+    }                              \
   } while (0)
 
 const void* wide_kernel_ptr(int rows, int ctas) {
@@ -998,7 +1113,7 @@ cudaError_t wide_configure(int rows, int ctas, int smem_bytes) {
 }
 
 void launch_T_wide(const WideArgs& A, int rows, int ctas, int grid, cudaStream_t st) {
-  const int smem = wide_smem_bytes(A.warps, A.slots, A.chunk, A.vecd);
+  const int smem = wide_smem_bytes(A);
   const int threads = 32 * A.warps;
 #define WLAUNCH(R, M) k_T_wide<R, M><<<grid, threads, smem, st>>>(A)
   WIDE_SWITCH(rows, ctas, WLAUNCH);

@@ -3,9 +3,41 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdint>
+
 #include "dev.cuh"
 
 namespace spock {
+
+constexpr int kWSpans = 16;  // staged vector operands per item
+constexpr int kWMats = 5;    // streamed matrices per item
+
+// base arrays of the staged vector spans (WB_Z / WB_ETA are the launch's inputs)
+enum WBase : int {
+  WB_Z = 0, WB_ETA, WB_QK, WB_GD, WB_H, WB_G, WB_QKN, WB_GDN, WB_CV, WB_A, WB_LO, WB_HI, WB_RB, WB_AN, WB_LON,
+  WB_HIN, WB_COUNT
+};
+
+// Per-ticket record, built once on the host (Engine::setup_wide), fetched by a
+// 256-byte bulk copy three tickets ahead of use: node metadata, the streamed
+// matrices (producer) and the independent vector operands (staged by cp.async
+// when the item starts).
+struct alignas(16) WRec {
+  int32_t kind, node, nch, c0;
+  int32_t anc, px, pu, pN;
+  int32_t nc, ny, so, s2o;  // so: seg1 offset (non-leaf) / seg3 offset (leaf)
+  int32_t yo, nmat, unstaged, nspan;  // unstaged: bit k -> span k is read from global memory
+  const double* mp[kWMats];
+  int16_t mrows[kWMats];
+  int16_t mcols[kWMats];
+  int16_t mcc[kWMats];  // columns per ring chunk (even; set for the launch's chunk size)
+  int16_t pad0_;
+  int32_t voff[kWSpans];
+  uint16_t vcnt[kWSpans];
+  uint8_t vbase[kWSpans];
+  uint8_t pad1_[8];
+};
+static_assert(sizeof(WRec) == 256, "WRec is one 256-byte bulk copy");
 
 struct WideArgs {
   Dev D;
@@ -17,14 +49,18 @@ struct WideArgs {
   int* flagB;   // [nn]  backward item of node i done (T12_i, adj_i, d_i); zeroed before each launch
   int* flagS2;  // [nnl] S2 of parent i done
   int* flagF;   // [nn]  forward (x+, u+) of node i done
-  int slots;    // ring slots per warp
+  int slots;    // ring slots per warp (power of two)
   int chunk;    // doubles per ring slot (even)
   int warps;    // warps per CTA
-  int vecd;     // doubles per per-warp vector buffer (two per warp)
-  unsigned long long* prof;  // optional [10] cycle counters (SPOCK_WIDE_PROF)
+  int vecd;     // doubles per per-warp vector buffer (three per warp)
+  int vrec;     // doubles of staged vector operands per warp
+  int ycap;     // y-block values staged per forward item (larger blocks read from L2)
+  const WRec* recs;           // [nn + nnl + nn] in ticket order
+  const double* vb[WB_COUNT];  // span bases (WB_Z, WB_ETA unused: taken from z, eta)
+  unsigned long long* prof;   // optional [13] cycle counters (SPOCK_WIDE_PROF)
 };
 
-int wide_smem_bytes(int warps, int slots, int chunk, int vecd);
+int wide_smem_bytes(const WideArgs& A);
 int wide_rows(const Dev& D, int max_nc);  // register row groups (template parameter)
 cudaError_t wide_configure(int rows, int ctas, int smem_bytes);
 const void* wide_kernel_ptr(int rows, int ctas);
