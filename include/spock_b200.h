@@ -200,6 +200,27 @@ int spock_bench_kernels(spock_solver* s, int32_t k, int32_t flush_l2, double* ms
 int spock_traffic_model(spock_solver* s, double* bytes5, int32_t* launches_per_T);
 const char* spock_solver_t_path(const spock_solver* s);
 
+/* Subtree sharding of T over G ranks (no reference counterpart: the reference
+ * runs one process).  The host picks a split stage ts; the rank
+ * owns the stage-ts nodes [b0, b1) = [bfirst + rank*q, bfirst + (rank+1)*q)
+ * (q = ceil(|stage ts| / G)) with their subtrees, and computes the stages < ts
+ * redundantly.  The node lists give the rank's items in dependency order:
+ * back_a = its subtrees' backward items (descending), back_b = the top's
+ * backward items (descending), s2 = parents whose S2 it computes, fwd = forward
+ * items (ascending).  xbuf_dev is a device buffer of G*q*(2(nx+nu)+6) doubles,
+ * all-gathered by the host between the two phases of spock_shard_apply_T
+ * (phase 0: rank's slice written; phase 1: completes T, host pointers in the
+ * boundary layouts; entries outside spock_shard_masks are not computed).
+ * spock_solver_stream returns the cudaStream_t the solver enqueues on. */
+int spock_shard_setup(spock_solver* s, int32_t world, int32_t rank, int32_t split_stage, const int32_t* back_a,
+                      int32_t na, const int32_t* back_b, int32_t nb, const int32_t* s2, int32_t ns2,
+                      const int32_t* fwd, int32_t nf, double* xbuf_dev);
+int spock_shard_apply_T(spock_solver* s, int32_t phase, const double* z, const double* eta, double* z_out,
+                        double* eta_out);
+int spock_shard_bench(spock_solver* s, int32_t phase, int32_t parity);
+int spock_shard_masks(spock_solver* s, uint8_t* z_mask, uint8_t* eta_mask);
+void* spock_solver_stream(const spock_solver* s);
+
 #ifdef __cplusplus
 }
 #endif

@@ -224,6 +224,14 @@ def load_library() -> C.CDLL:
     lib.spock_traffic_model.argtypes = [C.c_void_p, C.c_void_p, P(C.c_int32)]
     lib.spock_solver_t_path.argtypes = [C.c_void_p]
     lib.spock_solver_t_path.restype = C.c_char_p
+    PI = P(C.c_int32)
+    lib.spock_shard_setup.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, PI, C.c_int32, PI, C.c_int32,
+                                      PI, C.c_int32, PI, C.c_int32, C.c_void_p]
+    lib.spock_shard_apply_T.argtypes = [C.c_void_p, C.c_int32] + [C.c_void_p] * 4
+    lib.spock_shard_bench.argtypes = [C.c_void_p, C.c_int32, C.c_int32]
+    lib.spock_shard_masks.argtypes = [C.c_void_p, P(C.c_uint8), P(C.c_uint8)]
+    lib.spock_solver_stream.argtypes = [C.c_void_p]
+    lib.spock_solver_stream.restype = C.c_void_p
     _LIB = lib
     return lib
 
@@ -233,5 +241,6 @@ EXPORTED_SYMBOLS = [
     "spock_solver_dims", "spock_solver_alpha", "spock_solver_solve", "spock_solver_solve_cp",
     "spock_solver_apply_T", "spock_op_apply", "spock_op_apply_adjoint", "spock_op_m_norm",
     "spock_proj_s1", "spock_proj_s2", "spock_proj_s3", "spock_solver_unscale_primal", "spock_bench_T",
-    "spock_bench_kernels", "spock_traffic_model", "spock_solver_t_path",
+    "spock_bench_kernels", "spock_traffic_model", "spock_solver_t_path", "spock_shard_setup", "spock_shard_apply_T",
+    "spock_shard_bench", "spock_shard_masks", "spock_solver_stream",
 ]

@@ -208,6 +208,35 @@ int spock_traffic_model(spock_solver* s, double* bytes5, int32_t* launches_per_T
   });
 }
 
+int spock_shard_setup(spock_solver* s, int32_t world, int32_t rank, int32_t split_stage, const int32_t* back_a,
+                      int32_t na, const int32_t* back_b, int32_t nb, const int32_t* s2, int32_t ns2,
+                      const int32_t* fwd, int32_t nf, double* xbuf_dev) {
+  if (int rc = check(s)) return rc;
+  return guard([&] {
+    s->eng->shard_setup(world, rank, split_stage, back_a, na, back_b, nb, s2, ns2, fwd, nf, xbuf_dev);
+  });
+}
+
+int spock_shard_apply_T(spock_solver* s, int32_t phase, const double* z, const double* eta, double* z_out,
+                        double* eta_out) {
+  if (int rc = check(s)) return rc;
+  return guard([&] { s->eng->shard_apply_T_b(phase, z, eta, z_out, eta_out); });
+}
+
+int spock_shard_bench(spock_solver* s, int32_t phase, int32_t parity) {
+  if (int rc = check(s)) return rc;
+  return guard([&] { s->eng->shard_bench(phase, parity & 1); });
+}
+
+int spock_shard_masks(spock_solver* s, uint8_t* z_mask, uint8_t* eta_mask) {
+  if (int rc = check(s)) return rc;
+  return guard([&] { s->eng->shard_masks(z_mask, eta_mask); });
+}
+
+void* spock_solver_stream(const spock_solver* s) {
+  return (s && s->eng) ? reinterpret_cast<void*>(s->eng->stream()) : nullptr;
+}
+
 const char* spock_solver_t_path(const spock_solver* s) { return (s && s->eng) ? s->eng->t_path() : ""; }
 
 }  // extern "C"

@@ -90,7 +90,7 @@ Engine::Engine(const spock_problem_desc* desc, const Params& prm) : prm_(prm) {
   factorize();
   norm_.analytic_bound = analytic_norm_bound(p_, soc_);
   setup_fused();
-  setup_wide();
+  setup_wide(false);
   power_iteration();
   alpha_ = prm_.alpha > 0.0 ? prm_.alpha : 0.99 / std::max(norm_.estimate, 1e-300);
   CK(cudaStreamSynchronize(st_));
@@ -360,16 +360,16 @@ void Engine::setup_fused() {
 // per-warp TMA rings.  Default for trees the CTA-granular kernel does not take
 // (>= 4096 nodes); SPOCK_T_WIDE=0 selects the per-stage kernels instead,
 // SPOCK_T_WIDE=1 forces it on any tree the fused kernel is not used for.
-void Engine::setup_wide() {
+void Engine::setup_wide(bool force) {
   wide_ok_ = false;
-  if (fused_ok_) return;
+  if (fused_ok_ && !force) return;
   const Tree& tr = p_.tree;
   const int nn = tr.nn(), nnl = tr.nnl(), nx = p_.nx, nu = p_.nu, m = nx + nu;
   auto knob = [](const char* name, int dflt) {
     const char* v = std::getenv(name);
     return (v && v[0]) ? std::atoi(v) : dflt;
   };
-  const int want = knob("SPOCK_T_WIDE", -1);
+  const int want = force ? 1 : knob("SPOCK_T_WIDE", -1);
   if (want == 0) return;
   if (want < 0 && nn < 4096) return;
   int max_nc = 0, max_ny = 0;
@@ -557,6 +557,8 @@ void Engine::setup_wide() {
   CK(cudaMemcpyAsync(drec, recs.data(), sizeof(WRec) * recs.size(), cudaMemcpyHostToDevice, st_));
   CK(cudaStreamSynchronize(st_));
   A.recs = drec;
+  A.ntick = total;
+  wrecs_ = std::move(recs);
   A.vb[WB_QK] = D_.qk, A.vb[WB_GD] = D_.gd, A.vb[WB_H] = D_.h, A.vb[WB_G] = D_.g, A.vb[WB_QKN] = D_.qkN;
   A.vb[WB_GDN] = D_.gNd, A.vb[WB_CV] = D_.cvec, A.vb[WB_A] = D_.a, A.vb[WB_LO] = D_.lo, A.vb[WB_HI] = D_.hi;
   A.vb[WB_RB] = D_.rb, A.vb[WB_AN] = D_.aN, A.vb[WB_LON] = D_.loN, A.vb[WB_HIN] = D_.hiN;
@@ -567,6 +569,185 @@ void Engine::setup_wide() {
   A.flagF = wide_flags_ + nn + nnl;
   if (knob("SPOCK_WIDE_PROF", 0)) A.prof = dalloc<unsigned long long>(16);
   wide_ok_ = true;
+}
+
+// ---------------------------------------------------------------------------
+// Subtree sharding of T.  The host (paper_2505_12078_b200/shard.py)
+// chooses a split stage ts and gives this rank the stage-ts nodes [b0, b1) with
+// their subtrees; stages < ts are computed redundantly on every rank.  One T:
+//   phase A  backward items of the rank's subtrees (stages >= ts), then the
+//            boundary records of its stage-ts nodes are packed into its slice
+//            of the exchange buffer;
+//   (host)   all-gather of the exchange buffer across ranks (NCCL / gloo);
+//   phase B  remote stage-ts records are unpacked (their adj and T12 terms,
+//            the z / eta entries S2 of their parent reads) and their backward
+//            flags set; then the top backward items, S2 of every parent the
+//            rank holds, and the forward items of the top and of its subtrees.
+// Each rank's iterates are valid on the top and on its own subtrees.
+void Engine::shard_setup(int G, int rank, int ts, const int* back_a, int na, const int* back_b, int nb,
+                         const int* s2, int ns2, const int* fwd, int nf, double* xbuf) {
+  const Tree& tr = p_.tree;
+  const int nn = tr.nn(), nnl = tr.nnl();
+  require(G >= 1 && rank >= 0 && rank < G, "spock_shard_setup: bad rank / world size");
+  require(ts >= 1 && ts <= tr.horizon, "spock_shard_setup: split stage must be in [1, N]");
+  if (!wide_ok_) setup_wide(true);
+  require(wide_ok_, "spock_shard_setup: the streaming T kernel is not available for this problem");
+  shard_ = ShardState{};
+  ShardState& S = shard_;
+  S.G = G, S.rank = rank, S.ts = ts;
+  S.bfirst = tr.stage_start[ts];
+  S.nbound = tr.stage_start[ts + 1] - S.bfirst;
+  S.q = (S.nbound + G - 1) / G;
+  S.b0 = S.bfirst + std::min(rank * S.q, S.nbound);
+  S.b1 = S.bfirst + std::min((rank + 1) * S.q, S.nbound);
+  S.E = 2 * (p_.nx + p_.nu) + 6;
+  S.xbuf = xbuf;
+  auto pick = [&](const int* nodes, int n, int kind) {
+    std::vector<WRec> out;
+    out.reserve(size_t(n));
+    for (int k = 0; k < n; ++k) {
+      const int i = nodes[k];
+      require(i >= 0 && i < (kind == 1 ? nnl : nn), "spock_shard_setup: node index out of range");
+      const size_t t = kind == 0 ? size_t(nn - 1 - i) : (kind == 1 ? size_t(nn) + i : size_t(nn) + nnl + i);
+      out.push_back(wrecs_[t]);
+    }
+    return out;
+  };
+  std::vector<WRec> ra = pick(back_a, na, 0), rb = pick(back_b, nb, 0);
+  const std::vector<WRec> r2 = pick(s2, ns2, 1), rf = pick(fwd, nf, 2);
+  rb.insert(rb.end(), r2.begin(), r2.end());
+  rb.insert(rb.end(), rf.begin(), rf.end());
+  S.nA = int(ra.size());
+  S.nB = int(rb.size());
+  S.recA = dalloc<WRec>(std::max<size_t>(ra.size(), 1));
+  S.recB = dalloc<WRec>(std::max<size_t>(rb.size(), 1));
+  if (!ra.empty()) CK(cudaMemcpyAsync(S.recA, ra.data(), sizeof(WRec) * ra.size(), cudaMemcpyHostToDevice, st_));
+  if (!rb.empty()) CK(cudaMemcpyAsync(S.recB, rb.data(), sizeof(WRec) * rb.size(), cudaMemcpyHostToDevice, st_));
+  // per stage-ts node: where S2 of its parent reads its tau / s inputs
+  std::vector<int64_t> idx(size_t(S.nbound) * 6);
+  for (int k = 0; k < S.nbound; ++k) {
+    const int c = S.bfirst + k;
+    const int p = soc_.stage[c - 1].px + soc_.stage[c - 1].pu;
+    int64_t* x = &idx[size_t(k) * 6];
+    x[0] = lay_.tau_base + c - 1;               // z tau_c
+    x[1] = lay_.s_base + c - 1;                 // z s_c
+    x[2] = lay_.seg2_off[c - 1] + p;            // eta tau rows of c's stage-SOC segment
+    x[3] = x[2] + 1;
+    if (c < nnl) {
+      x[4] = lay_.seg1_off[c] + lay_.y_dim[c];  // eta risk scalar row of c
+      x[5] = -1;
+    } else {
+      const int j = c - nnl;
+      x[4] = lay_.seg3_off[j] + p_.ncN[j] + soc_.leaf[j].px;  // eta terminal SOC tau rows
+      x[5] = x[4] + 1;
+    }
+  }
+  S.xidx = dupload(idx);
+  // nodes whose iterate entries this rank computes: the top and its subtrees
+  S.owned.assign(size_t(nn), 0);
+  std::vector<int> root_ts(size_t(nn), -1);
+  for (int i = 0; i < nn; ++i) {
+    if (i < S.bfirst) {
+      S.owned[i] = 1;
+      continue;
+    }
+    root_ts[i] = tr.stage[i] == ts ? i : root_ts[tr.anc[i]];
+    S.owned[i] = (root_ts[i] >= S.b0 && root_ts[i] < S.b1) ? 1 : 0;
+  }
+  CK(cudaStreamSynchronize(st_));
+  S.on = true;
+}
+
+// validity masks of this rank's iterates in the boundary layouts (1: computed here)
+void Engine::shard_masks(uint8_t* zm, uint8_t* em) const {
+  const ShardState& S = shard_;
+  require(S.on, "spock_shard_masks: call spock_shard_setup first");
+  const Tree& tr = p_.tree;
+  const int nn = tr.nn(), nnl = tr.nnl(), nx = p_.nx, nu = p_.nu;
+  if (zm) {
+    std::memset(zm, 0, size_t(lay_.nz));
+    zm[0] = 1;
+    for (int i = 0; i < nn; ++i) {
+      const uint8_t o = S.owned[i];
+      std::memset(zm + 1 + size_t(i) * nx, o, size_t(nx));
+      if (i < nnl) {
+        std::memset(zm + lay_.u_base + size_t(i) * nu, o, size_t(nu));
+        std::memset(zm + lay_.y_off[i], o, size_t(lay_.y_dim[i]));
+      }
+      if (i > 0) {
+        const uint8_t oa = S.owned[tr.anc[i]];  // tau_i, s_i come from S2 of the parent
+        zm[lay_.tau_base + i - 1] = oa;
+        zm[lay_.s_base + i - 1] = oa;
+      }
+    }
+  }
+  if (em) {
+    std::memset(em, 0, size_t(lay_.neta));
+    for (int i = 0; i < nn; ++i) {
+      const uint8_t o = S.owned[i];
+      if (i < nnl) std::memset(em + lay_.seg1_off[i], o, size_t(lay_.y_dim[i] + 1 + p_.nc[i]));
+      if (i > 0) {
+        const int k = i - 1;
+        std::memset(em + lay_.seg2_off[k], o, size_t(soc_.stage[k].px + soc_.stage[k].pu + 2));
+      }
+      if (i >= nnl) {
+        const int j = i - nnl;
+        std::memset(em + lay_.seg3_off[j], o, size_t(p_.ncN[j] + soc_.leaf[j].px + 2));
+      }
+    }
+  }
+}
+
+// boundary-layout sharded T, in two calls around the host's all-gather
+void Engine::shard_apply_T_b(int phase, const double* z, const double* eta, double* zo, double* eo) {
+  double *iz = scratch_z_[0], *ie = scratch_e_[0], *oz = scratch_z_[1], *oe = scratch_e_[1];
+  if (phase == 0) {
+    copy_in_z(z, iz);
+    to_internal_eta(eta, ie);
+    shard_T_A(iz, ie, oz, oe);
+  } else {
+    shard_T_B(iz, ie, oz, oe);
+    copy_out(oz, zo, lay_.nz);
+    from_internal_eta(oe, eo);
+    sync();
+  }
+}
+
+// device-resident ping-pong between the scratch iterates (bench helper)
+void Engine::shard_bench(int phase, int parity) {
+  double *z0 = scratch_z_[parity], *e0 = scratch_e_[parity], *z1 = scratch_z_[1 - parity],
+         *e1 = scratch_e_[1 - parity];
+  if (phase == 0)
+    shard_T_A(z0, e0, z1, e1);
+  else
+    shard_T_B(z0, e0, z1, e1);
+}
+
+void Engine::shard_T_A(const double* z, const double* eta, double* zo, double* eo) {
+  const ShardState& S = shard_;
+  require(S.on, "spock_shard_T: call spock_shard_setup first");
+  WideArgs A = wargs_;
+  A.D = D_, A.z = z, A.eta = eta, A.zo = zo, A.eo = eo, A.alpha = alpha_;
+  A.recs = S.recA;
+  A.ntick = S.nA;
+  CK(cudaMemsetAsync(wide_flags_, 0, wide_flag_bytes_, st_));
+  if (S.nA > 0) launch_T_wide(A, wide_rows_, wide_ctas_, std::min(wide_grid_, (S.nA + A.warps - 1) / A.warps), st_);
+  ShardXArgs X{D_, z, eta, S.xidx, S.xbuf, S.bfirst, S.b0, S.b1, S.E, nullptr};
+  launch_shard_pack(X, st_);
+}
+
+void Engine::shard_T_B(const double* z, const double* eta, double* zo, double* eo) {
+  const ShardState& S = shard_;
+  require(S.on, "spock_shard_T: call spock_shard_setup first");
+  // remote stage-ts records -> adj, T12, the inputs' tau / s entries, backward flags
+  ShardXArgs X{D_, z, eta, S.xidx, S.xbuf, S.bfirst, S.b0, S.b1, S.E, wargs_.flagB};
+  X.nbound = S.nbound;
+  launch_shard_unpack(X, st_);
+  WideArgs A = wargs_;
+  A.D = D_, A.z = z, A.eta = eta, A.zo = zo, A.eo = eo, A.alpha = alpha_;
+  A.recs = S.recB;
+  A.ntick = S.nB;
+  if (S.nB > 0) launch_T_wide(A, wide_rows_, wide_ctas_, std::min(wide_grid_, (S.nB + A.warps - 1) / A.warps), st_);
 }
 
 void Engine::wide_profile(unsigned long long* out) {
@@ -1202,6 +1383,8 @@ void Engine::T(const double* z, const double* eta, double* zo, double* eo) {
     A.zo = zo;
     A.eo = eo;
     A.alpha = alpha_;
+    A.recs = wargs_.recs;
+    A.ntick = wargs_.ntick;
     CK(cudaMemsetAsync(wide_flags_, 0, wide_flag_bytes_, st_));
     launch_T_wide(A, wide_rows_, wide_ctas_, wide_grid_, st_);
     return;

@@ -75,6 +75,17 @@ class Engine {
   double bench_T(int k, bool graph, bool flush);
   void bench_kernels(int k, bool flush, double* ms);
   void traffic(double* bytes) const;
+  // subtree sharding (see engine.cu)
+  void shard_setup(int G, int rank, int ts, const int* back_a, int na, const int* back_b, int nb, const int* s2,
+                   int ns2, const int* fwd, int nf, double* xbuf);
+  void shard_T_A(const double* z, const double* eta, double* zo, double* eo);
+  void shard_T_B(const double* z, const double* eta, double* zo, double* eo);
+  void shard_masks(uint8_t* zm, uint8_t* em) const;
+  void shard_apply_T_b(int phase, const double* z, const double* eta, double* zo, double* eo);
+  void shard_bench(int phase, int parity);
+  cudaStream_t stream() const { return st_; }
+  double* scratch_z(int k) const { return scratch_z_[k]; }
+  double* scratch_e(int k) const { return scratch_e_[k]; }
   int launches_per_T() const { return (fused_ok_ || wide_ok_) ? 1 : 2 + 2 * (p_.tree.horizon + 1) + 1 + 1; }
   // SPOCK_WIDE_PROF=1: cycle counters of the wide kernel (summed over warps and launches)
   void wide_profile(unsigned long long* out10);
@@ -83,7 +94,7 @@ class Engine {
  private:
   void upload();
   void setup_fused();
-  void setup_wide();
+  void setup_wide(bool force);
   void factorize();
   void power_iteration();
   void set_xinit(const double* x_orig_host);
@@ -136,6 +147,16 @@ class Engine {
   int wide_grid_ = 0, wide_rows_ = 0, wide_ctas_ = 1;
   int max_dense_s2_ = 0;
   int* wide_flags_ = nullptr;
+  std::vector<WRec> wrecs_;  // host copy of the full ticket list (shard subsets are drawn from it)
+  struct ShardState {
+    bool on = false;
+    int G = 1, rank = 0, ts = 0, bfirst = 0, nbound = 0, q = 0, b0 = 0, b1 = 0, E = 0, nA = 0, nB = 0;
+    WRec* recA = nullptr;
+    WRec* recB = nullptr;
+    int64_t* xidx = nullptr;
+    double* xbuf = nullptr;
+    std::vector<uint8_t> owned;
+  } shard_;
   size_t wide_flag_bytes_ = 0;
   double* flush_buf_ = nullptr;
   void flush_l2();

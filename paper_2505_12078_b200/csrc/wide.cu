@@ -977,7 +977,7 @@ __global__ void __launch_bounds__(256, MINB) k_T_wide(const __grid_constant__ Wi
   R.rc = nullptr;
   R.mk = 0;
   R.stride = gridDim.x * A.warps;
-  R.total = D.nn + D.nnl + D.nn;
+  R.total = A.ntick;
   R.gw = blockIdx.x * A.warps + w;
   R.jc = 0;
   R.cons = 0;
@@ -1063,7 +1063,56 @@ __global__ void __launch_bounds__(256, MINB) k_T_wide(const __grid_constant__ Wi
   }
 }
 
+// one warp per stage-ts node of this rank: record -> exchange buffer slot
+__global__ void k_shard_pack(const __grid_constant__ ShardXArgs X) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, l = lane_id();
+  const int c = X.b0 + w;
+  if (c >= X.b1) return;
+  const int m = X.D.nx + X.D.nu;
+  const int k = c - X.bfirst;
+  double* o = X.xbuf + size_t(k) * X.E;
+  for (int r = l; r < m; r += 32) {
+    o[r] = X.D.adj[size_t(c - 1) * m + r];
+    o[m + r] = X.D.T12[size_t(c - 1) * m + r];
+  }
+  if (l < 6) {
+    const int64_t ix = X.xidx[size_t(k) * 6 + l];
+    o[2 * m + l] = ix < 0 ? 0.0 : (l < 2 ? X.z[ix] : X.eta[ix]);
+  }
+}
+
+// remote stage-ts nodes: exchange buffer -> adj, T12, the inputs' tau/s entries; backward flag
+__global__ void k_shard_unpack(const __grid_constant__ ShardXArgs X) {
+  const int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, l = lane_id();
+  if (k >= X.nbound) return;
+  const int c = X.bfirst + k;
+  if (c >= X.b0 && c < X.b1) return;
+  const int m = X.D.nx + X.D.nu;
+  const double* o = X.xbuf + size_t(k) * X.E;
+  for (int r = l; r < m; r += 32) {
+    X.D.adj[size_t(c - 1) * m + r] = o[r];
+    X.D.T12[size_t(c - 1) * m + r] = o[m + r];
+  }
+  if (l < 6) {
+    const int64_t ix = X.xidx[size_t(k) * 6 + l];
+    if (ix >= 0) (l < 2 ? const_cast<double*>(X.z) : const_cast<double*>(X.eta))[ix] = o[2 * m + l];
+  }
+  __syncwarp();
+  if (l == 0) {
+    __threadfence();
+    X.flagB[c] = 1;  // visible to the next launch (stream order)
+  }
+}
+
 }  // namespace
+
+void launch_shard_pack(const ShardXArgs& X, cudaStream_t st) {
+  const int n = X.b1 - X.b0;
+  if (n > 0) k_shard_pack<<<(n + 7) / 8, 256, 0, st>>>(X);
+}
+void launch_shard_unpack(const ShardXArgs& X, cudaStream_t st) {
+  if (X.nbound > 0) k_shard_unpack<<<(X.nbound + 7) / 8, 256, 0, st>>>(X);
+}
 
 int wide_smem_bytes(const WideArgs& A) {
   return int(sizeof(double) * size_t(A.warps) * warp_doubles(A.slots, A.chunk, A.vrec, A.vecd));

@@ -55,10 +55,26 @@ struct WideArgs {
   int vecd;     // doubles per per-warp vector buffer (three per warp)
   int vrec;     // doubles of staged vector operands per warp
   int ycap;     // y-block values staged per forward item (larger blocks read from L2)
-  const WRec* recs;           // [nn + nnl + nn] in ticket order
+  const WRec* recs;           // ticket list ([nn + nnl + nn] for a whole T)
+  int ntick;                  // number of tickets
   const double* vb[WB_COUNT];  // span bases (WB_Z, WB_ETA unused: taken from z, eta)
   unsigned long long* prof;   // optional [13] cycle counters (SPOCK_WIDE_PROF)
 };
+
+// exchange records of the stage-ts nodes of a sharded T (engine.cu shard_*):
+// per node [adj (m) | T12 (m) | z_tau | z_s | eta_tau0 | eta_tau1 | eta_s0 | eta_s1]
+struct ShardXArgs {
+  Dev D;
+  const double* z;
+  const double* eta;
+  const int64_t* xidx;  // 6 indices per stage-ts node: z_tau, z_s, eta_tau0, eta_tau1, eta_s0, eta_s1 (-1: none)
+  double* xbuf;         // [G * q * E]
+  int bfirst, b0, b1, E;
+  int* flagB;           // unpack: set for remote nodes
+  int nbound;
+};
+void launch_shard_pack(const ShardXArgs& X, cudaStream_t st);
+void launch_shard_unpack(const ShardXArgs& X, cudaStream_t st);
 
 int wide_smem_bytes(const WideArgs& A);
 int wide_rows(const Dev& D, int max_nc);  // register row groups (template parameter)

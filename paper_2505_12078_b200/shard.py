@@ -1,0 +1,219 @@
+"""Subtree sharding of the CP operator T over G ranks.
+
+The reference runs one process (proj/src/parallel.cpp is a thread pool over
+the nodes of one stage); this is the B200 extension the north star names:
+the tree is cut at a split stage ``ts``, rank ``r`` owns the stage-ts nodes
+``[b0, b1) = [bfirst + r*q, bfirst + (r+1)*q)`` (``q = ceil(|stage ts| / G)``)
+together with their subtrees, and every rank computes the stages ``< ts``
+("the top") redundantly.  Because the tree is numbered breadth first with
+contiguous children (proj/include/spock/tree.hpp:10-13,42-44), every owned
+subtree is one contiguous node range per stage.
+
+One T needs one exchange: after a rank's subtrees ran their backward items,
+each stage-ts node contributes the terms its parent sums over its children
+(the L* stage-cost adjoint adj_c and the S1 sweep term T12_c,
+tree_operator.cpp:106-113 and projections.cpp:157-158,171) and the z / eta
+entries S2 of its parent reads (projections.cpp:189-210); an all-gather of
+those records lets every rank finish the top and then its subtrees' forward
+items.  The stage-ts parent sums run in ascending child order, so the result
+is deterministic for a fixed G (and equal to one GPU up to rounding).
+
+``ShardPlan`` is pure host logic (no device needed, tested on CPU);
+``ShardedSolver`` drives the device library over ``torch.distributed`` (NCCL
+on a B200 box, gloo in the CPU tests and for several ranks sharing one GPU).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from .problem import ScenarioTree
+
+
+def default_split_stage(tree: ScenarioTree, world: int) -> int:
+    """Smallest stage t >= 1 with at least 4 nodes per rank (else the widest
+    stage), so each rank gets several subtrees and the replicated top stays
+    small."""
+    N = tree.horizon
+    best, best_n = 1, -1
+    for t in range(1, N + 1):
+        n = tree.stage_end(t) - tree.stage_begin(t)
+        if n >= 4 * world:
+            return t
+        if n > best_n:
+            best, best_n = t, n
+    return best
+
+
+@dataclass
+class ShardPlan:
+    world: int
+    rank: int
+    split_stage: int
+    bfirst: int
+    nbound: int
+    q: int
+    b0: int
+    b1: int
+    owned: np.ndarray       # bool per node: top or in this rank's subtrees
+    back_a: np.ndarray      # own subtrees' backward items, descending
+    back_b: np.ndarray      # the top's backward items, descending
+    s2: np.ndarray          # parents whose S2 this rank computes
+    fwd: np.ndarray         # forward items, ascending
+    record_len: int         # doubles per exchange record (2(nx+nu)+6)
+
+    @property
+    def xbuf_len(self) -> int:
+        return self.world * self.q * self.record_len
+
+    @property
+    def slice(self) -> slice:
+        """This rank's slice of the exchange buffer."""
+        return slice(self.rank * self.q * self.record_len, (self.rank + 1) * self.q * self.record_len)
+
+
+def make_plan(tree: ScenarioTree, nx: int, nu: int, world: int, rank: int,
+              split_stage: Optional[int] = None) -> ShardPlan:
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("shard plan: bad rank / world size")
+    ts = default_split_stage(tree, world) if split_stage is None else int(split_stage)
+    if not 1 <= ts <= tree.horizon:
+        raise ValueError("shard plan: split stage must be in [1, N]")
+    nn, nnl = tree.num_nodes(), tree.num_nonleaf()
+    bfirst = tree.stage_begin(ts)
+    nbound = tree.stage_end(ts) - bfirst
+    q = -(-nbound // world)
+    b0 = bfirst + min(rank * q, nbound)
+    b1 = bfirst + min((rank + 1) * q, nbound)
+    root_ts = np.full(nn, -1, dtype=np.int64)
+    owned = np.zeros(nn, dtype=bool)
+    owned[:bfirst] = True
+    for i in range(bfirst, nn):
+        root_ts[i] = i if tree.stage[i] == ts else root_ts[tree.anc[i]]
+    owned[bfirst:] = (root_ts[bfirst:] >= b0) & (root_ts[bfirst:] < b1)
+    nodes = np.arange(nn, dtype=np.int32)
+    bottom = nodes[(nodes >= bfirst) & owned]
+    return ShardPlan(
+        world=world, rank=rank, split_stage=ts, bfirst=bfirst, nbound=nbound, q=q, b0=b0, b1=b1, owned=owned,
+        back_a=bottom[::-1].copy(), back_b=nodes[:bfirst][::-1].copy(),
+        s2=nodes[:nnl][owned[:nnl]].copy(), fwd=nodes[owned].copy(), record_len=2 * (nx + nu) + 6)
+
+
+def check_plan(tree: ScenarioTree, plans) -> None:
+    """Invariants of a set of per-rank plans (used by the CPU tests): every
+    node below the split stage is owned by exactly one rank, the top by all,
+    and each rank's item lists respect the dependencies (children before
+    parents backward, parents before children forward)."""
+    nn = tree.num_nodes()
+    cnt = np.zeros(nn, dtype=np.int64)
+    for pl in plans:
+        cnt += pl.owned
+        pos = {}
+        for k, i in enumerate(list(pl.back_a) + list(pl.back_b)):
+            pos[int(i)] = k
+        for i, k in pos.items():
+            for c in range(tree.child_first[i], tree.child_first[i] + tree.child_count[i]):
+                if pl.owned[c]:
+                    assert pos[c] < k, (i, c)
+        fpos = {int(i): k for k, i in enumerate(pl.fwd)}
+        for c, k in fpos.items():
+            if c > 0:
+                assert fpos[int(tree.anc[c])] < k
+    top = tree.stage_begin(plans[0].split_stage)
+    assert np.all(cnt[:top] == len(plans))
+    assert np.all(cnt[top:] == 1)
+
+
+def exchange(xbuf, plan: ShardPlan, group=None, stream=None) -> None:
+    """All-gather every rank's slice of the exchange buffer (in place).  NCCL:
+    device to device, ordered on ``stream`` (the solver's); gloo: through host
+    memory (CPU tests, several ranks sharing one GPU)."""
+    import torch
+    import torch.distributed as dist
+    own = xbuf[plan.slice]
+    if dist.get_backend(group) == "nccl":
+        with torch.cuda.stream(stream):
+            dist.all_gather_into_tensor(xbuf, own.clone(), group=group)
+        return
+    if stream is not None:
+        stream.synchronize()
+    host = own.cpu()
+    parts = [torch.empty_like(host) for _ in range(plan.world)]
+    dist.all_gather(parts, host, group=group)
+    xbuf.copy_(torch.cat(parts).to(xbuf.device))
+    if xbuf.is_cuda:
+        torch.cuda.synchronize(xbuf.device)
+
+
+class ShardedSolver:
+    """apply_T across the ranks of a torch.distributed group: each rank holds
+    the whole problem (memory replicated), computes the top and its subtrees,
+    and all-gathers the stage-ts exchange records once per T."""
+
+    def __init__(self, problem, group=None, split_stage: Optional[int] = None, **params):
+        import torch
+        import torch.distributed as dist
+        from . import capi
+        from .solver import SpockSolver, _raise
+        self.torch, self.dist, self.group = torch, dist, group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.solver = SpockSolver(problem, **params)
+        self.lib = self.solver.lib
+        self.plan = make_plan(problem.tree, problem.nx, problem.nu, self.world, self.rank, split_stage)
+        pl = self.plan
+        self.xbuf = torch.zeros(pl.xbuf_len, dtype=torch.float64, device="cuda")
+        self._keep = [np.ascontiguousarray(a, dtype=np.int32) for a in (pl.back_a, pl.back_b, pl.s2, pl.fwd)]
+        a, b, s2, f = self._keep
+        P = C.POINTER(C.c_int32)
+        _raise(self.lib, self.lib.spock_shard_setup(
+            self.solver.h, self.world, self.rank, pl.split_stage, a.ctypes.data_as(P), a.size,
+            b.ctypes.data_as(P), b.size, s2.ctypes.data_as(P), s2.size, f.ctypes.data_as(P), f.size,
+            C.c_void_p(self.xbuf.data_ptr())))
+        self.stream = torch.cuda.ExternalStream(self.lib.spock_solver_stream(self.solver.h))
+        self._capi = capi
+        self._raise = _raise
+
+    @property
+    def alpha(self) -> float:
+        return self.solver.alpha
+
+    @property
+    def nz(self) -> int:
+        return self.solver.nz
+
+    @property
+    def neta(self) -> int:
+        return self.solver.neta
+
+    def masks(self):
+        zm = np.zeros(self.nz, dtype=np.uint8)
+        em = np.zeros(self.neta, dtype=np.uint8)
+        P = C.POINTER(C.c_uint8)
+        self._raise(self.lib, self.lib.spock_shard_masks(self.solver.h, zm.ctypes.data_as(P), em.ctypes.data_as(P)))
+        return zm.astype(bool), em.astype(bool)
+
+    def _exchange(self):
+        exchange(self.xbuf, self.plan, self.group, self.stream)
+
+    def apply_T(self, z, eta, z_out=None, eta_out=None):
+        """Sharded SpockSolver::apply_T (proj/src/solver.cpp:148-164): entries
+        outside masks() are not computed on this rank."""
+        from .solver import _ptr
+        z = np.ascontiguousarray(z, dtype=np.float64)
+        eta = np.ascontiguousarray(eta, dtype=np.float64)
+        z_out = np.zeros_like(z) if z_out is None else z_out
+        eta_out = np.zeros_like(eta) if eta_out is None else eta_out
+        self._raise(self.lib, self.lib.spock_shard_apply_T(self.solver.h, 0, _ptr(z), _ptr(eta), None, None))
+        self._exchange()
+        self._raise(self.lib, self.lib.spock_shard_apply_T(self.solver.h, 1, None, None, _ptr(z_out), _ptr(eta_out)))
+        return z_out, eta_out
+
+    def bench_step(self, parity: int) -> None:
+        """One sharded T on the device-resident scratch iterates (no host copies)."""
+        self._raise(self.lib, self.lib.spock_shard_bench(self.solver.h, 0, parity))
+        self._exchange()
+        self._raise(self.lib, self.lib.spock_shard_bench(self.solver.h, 1, parity))

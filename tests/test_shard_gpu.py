@@ -1,0 +1,94 @@
+"""Sharded T on the device: G ranks (spawned processes
+sharing cuda:0, gloo exchange) each compute the top and their subtrees; on
+every rank's valid entries the result equals the one-GPU T and the CPU
+oracle's apply_T (proj/src/solver.cpp:148-164).  GPU only."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _problem(name):
+    from paper_2505_12078_b200.generators import make_config
+    from paper_2505_12078_b200.problem import ScenarioTree
+    from support import TinyOpts, make_tiny
+    if name == "mixed":
+        return make_tiny(ScenarioTree.from_branching([3, 2, 2]), 3, 2, 5, TinyOpts(gamma=0.4, box_halfwidth=1.0))
+    if name == "expectation":
+        return make_tiny(ScenarioTree.from_branching([2, 3, 1]), 3, 2, 7, TinyOpts(gamma=1.0))
+    return make_config(name, seed=1)
+
+
+def _worker(rank, world, port, name, ts, q):
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    sys.path.insert(0, os.path.join(root, "tests"))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.oracle import OracleSolver
+        from paper_2505_12078_b200.rng import Philox
+        from paper_2505_12078_b200.shard import ShardedSolver
+        from paper_2505_12078_b200.solver import SpockSolver
+        p = _problem(name)
+        sh = ShardedSolver(p, split_stage=ts)
+        one = SpockSolver(p, alpha=sh.alpha)
+        orc = OracleSolver(p, alpha=sh.alpha)
+        zm, em = sh.masks()
+        errs = []
+        for seed in (3, 4):
+            z = -1.0 + 2.0 * Philox(seed).uniform_array(sh.nz)
+            e = -1.0 + 2.0 * Philox(seed + 50).uniform_array(sh.neta)
+            za, ea = sh.apply_T(z, e)
+            zb, eb = one.apply_T(z, e)
+            zc, ec = orc.apply_T(z, e)
+            sz, se = max(1.0, np.abs(zc).max()), max(1.0, np.abs(ec).max())
+            errs.append(float(np.abs(za - zb)[zm].max() / sz))
+            errs.append(float(np.abs(ea - eb)[em].max() / se))
+            errs.append(float(np.abs(za - zc)[zm].max() / sz))
+            errs.append(float(np.abs(ea - ec)[em].max() / se))
+        q.put((rank, max(errs), int(zm.sum()), int(em.sum()), sh.plan.split_stage))
+    except Exception as ex:  # report instead of hanging the parent
+        q.put((rank, repr(ex), 0, 0, 0))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name,world,ts", [
+    ("mixed", 2, None), ("mixed", 3, 1), ("expectation", 2, 2), ("c1", 2, None), ("c1", 4, 3), ("c2p", 2, None),
+    ("c2p", 4, None),
+])
+def test_sharded_T_matches_one_gpu_and_oracle(name, world, ts):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, name, ts, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = {}
+    for _ in range(world):
+        r, err, nzv, nev, st = q.get(timeout=600)
+        res[r] = (err, nzv, nev, st)
+    for pr in procs:
+        pr.join(timeout=60)
+    for r in range(world):
+        err = res[r][0]
+        assert not isinstance(err, str), res[r]
+        assert err <= 1e-11, (r, res[r])
