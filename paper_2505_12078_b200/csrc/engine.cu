@@ -166,6 +166,13 @@ void Engine::setup_fused() {
   F.threads = threads;
   F.mat_doubles = int(mx);
   F.vec_doubles = int(vx);
+  {
+    int rows = std::max(m + nu, 64);  // cta_gemv2 stacks m + nu rows; cta_sum needs 8
+    for (int i = 0; i < nnl; ++i) rows = std::max(rows, p_.nc[i]);
+    for (int j = 0; j < tr.nl(); ++j) rows = std::max(rows, p_.ncN[j]);
+    rows = std::max(rows, max_dense_s2_);
+    F.red_doubles = int(pad2((threads / 32) * int64_t(rows)));
+  }
   int dev = 0, sms = 148, smem_optin = 0;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -362,16 +369,21 @@ void Engine::setup_fused() {
 // SPOCK_T_WIDE=1 forces it on any tree the fused kernel is not used for.
 void Engine::setup_wide(bool force) {
   wide_ok_ = false;
-  if (fused_ok_ && !force) return;
+  t_wide_ = false;
   const Tree& tr = p_.tree;
   const int nn = tr.nn(), nnl = tr.nnl(), nx = p_.nx, nu = p_.nu, m = nx + nu;
   auto knob = [](const char* name, int dflt) {
     const char* v = std::getenv(name);
     return (v && v[0]) ? std::atoi(v) : dflt;
   };
-  const int want = force ? 1 : knob("SPOCK_T_WIDE", -1);
-  if (want == 0) return;
-  if (want < 0 && nn < 4096) return;
+  // T runs on this kernel when the CTA-granular one is not used and the tree is
+  // wide (or on request); so do the standalone L / L* on wide trees (measured:
+  // on narrow trees one item per warp is latency-bound, narrow.cu's CTA-per-node
+  // kernels win -- profiles/r01_wide_configs.md; SPOCK_LOP_WIDE=0/1 overrides)
+  const int want = knob("SPOCK_T_WIDE", -1);
+  const bool t_wide = !fused_ok_ && want != 0 && (want > 0 || nn >= 4096);
+  lop_wide_ = knob("SPOCK_LOP_WIDE", nn >= 4096 ? 1 : 0) != 0;
+  if (!t_wide && !lop_wide_ && !force) return;
   int max_nc = 0, max_ny = 0;
   for (int i = 0; i < nnl; ++i) max_nc = std::max(max_nc, p_.nc[i]);
   for (int j = 0; j < tr.nl(); ++j) max_nc = std::max(max_nc, p_.ncN[j]);
@@ -381,8 +393,8 @@ void Engine::setup_wide(bool force) {
   A = WideArgs{};
   A.warps = std::max(1, std::min(8, knob("SPOCK_WIDE_WARPS", 8)));
   {
-    const int sl = std::max(1, std::min(8, knob("SPOCK_WIDE_SLOTS", 2)));
-    A.slots = sl >= 8 ? 8 : (sl >= 4 ? 4 : (sl >= 2 ? 2 : 1));  // power of two
+    const int sl = std::max(1, std::min(16, knob("SPOCK_WIDE_SLOTS", 2)));
+    A.slots = sl >= 16 ? 16 : (sl >= 8 ? 8 : (sl >= 4 ? 4 : (sl >= 2 ? 2 : 1)));  // power of two
   }
   A.chunk = std::max(512, knob("SPOCK_WIDE_CHUNK", 512)) & ~1;
   A.ycap = std::min(max_ny, 256);
@@ -523,13 +535,74 @@ void Engine::setup_wide(bool force) {
       span(R, F_HIN, WB_HIN, go, R.nc);
     }
   }
-  int64_t vmax = 2;
-  for (const WRec& R : recs) {
-    int64_t t = 0;
-    for (int k = 0; k < R.nspan; ++k)
-      if (R.vcnt[k]) t += pad2(R.vcnt[k] + 1);  // + alignment shift (taken from the address)
-    vmax = std::max(vmax, t);
+  // standalone L (kind 3) and L* (kind 4: child terms of nodes 1..nn-1, then
+  // kind 5: node rows of 0..nn-1) for the SuperMann loop outside T
+  enum { L_ZX = 0, L_ZU, L_AX, L_AU, L_QK, L_ZT, L_ZS, L_Y, L_RB, L_GD, L_QKN };
+  enum { LC_HEAD = 0, LC_QK };
+  enum { LN_SEG1 = 0, LN_RB, LN_GD, LN_QKN };
+  std::vector<WRec> lrecs(static_cast<size_t>(nn)), ltrecs;
+  for (int i = 0; i < nn; ++i) {
+    WRec& R = lrecs[size_t(i)];
+    meta(R, 3, i);
+    const bool leaf = tr.leaf(i), root = i == 0;
+    span(R, L_ZX, WB_Z, 1 + int64_t(i) * nx, nx);
+    if (!leaf) {
+      span(R, L_ZU, WB_Z, lay_.u_base + int64_t(i) * nu, nu);
+      span(R, L_Y, WB_Z, R.yo, R.ny);
+      span(R, L_RB, WB_RB, R.yo - D_.y_base, R.ny);
+      if (D_.g_diag) span(R, L_GD, WB_GD, int64_t(i) * m, m);
+      span(R, L_ZS, WB_Z, root ? 0 : lay_.s_base + i - 1, 1);
+    }
+    if (!root) {
+      const int an = R.anc;
+      mat(R, D_.Hx + hxo[i - 1], R.px, nx);
+      mat(R, D_.Hu + huo[i - 1], R.pu, nu);
+      span(R, L_AX, WB_Z, 1 + int64_t(an) * nx, nx);
+      span(R, L_AU, WB_Z, lay_.u_base + int64_t(an) * nu, nu);
+      span(R, L_QK, WB_QK, int64_t(i - 1) * m, m);
+      span(R, L_ZT, WB_Z, lay_.tau_base + i - 1, 1);
+    }
+    if (leaf) {
+      const int j = i - nnl;
+      mat(R, D_.HN + hno[j], R.pN, nx);
+      if (D_.gN_diag) span(R, L_GD, WB_GDN, int64_t(j) * nx, nx);
+      span(R, L_QKN, WB_QKN, int64_t(j) * nx, nx);
+      span(R, L_ZS, WB_Z, lay_.s_base + i - 1, 1);
+    }
   }
+  for (int i = 1; i < nn; ++i) {
+    WRec R;
+    meta(R, 4, i);
+    mat(R, D_.HxT + hxo[i - 1], nx, R.px);
+    mat(R, D_.HuT + huo[i - 1], nu, R.pu);
+    span(R, LC_HEAD, WB_ETA, R.s2o, R.px + R.pu + 2);
+    span(R, LC_QK, WB_QK, int64_t(i - 1) * m, m);
+    ltrecs.push_back(R);
+  }
+  for (int i = 0; i < nn; ++i) {
+    WRec R;
+    meta(R, 5, i);
+    if (!tr.leaf(i)) {
+      span(R, LN_SEG1, WB_ETA, R.so, R.ny + 1 + R.nc);
+      span(R, LN_RB, WB_RB, R.yo - D_.y_base, R.ny);
+      if (D_.g_diag) span(R, LN_GD, WB_GD, int64_t(i) * m, m);
+    } else {
+      const int j = i - nnl;
+      mat(R, D_.HNT + hno[j], nx, R.pN);
+      span(R, LN_SEG1, WB_ETA, R.so, R.nc + R.pN + 2);
+      if (D_.gN_diag) span(R, LN_GD, WB_GDN, int64_t(j) * nx, nx);
+      span(R, LN_QKN, WB_QKN, int64_t(j) * nx, nx);
+    }
+    ltrecs.push_back(R);
+  }
+  int64_t vmax = 2;
+  for (const std::vector<WRec>* L : {&recs, &lrecs, &ltrecs})
+    for (const WRec& R : *L) {
+      int64_t t = 0;
+      for (int k = 0; k < R.nspan; ++k)
+        if (R.vcnt[k]) t += pad2(R.vcnt[k] + 1);  // + alignment shift (taken from the address)
+      vmax = std::max(vmax, t);
+    }
   A.vrec = int(pad2(vmax));
   int dev = 0, sms = 148, smem_optin = 0;
   CK(cudaGetDevice(&dev));
@@ -540,9 +613,10 @@ void Engine::setup_wide(bool force) {
   while (wide_smem_bytes(A) > budget && A.warps > 1) --A.warps;
   const int bytes = wide_smem_bytes(A);
   if (bytes > smem_optin) return;
-  for (WRec& R : recs)  // columns per ring chunk (even; a chunk holds >= 2 columns)
-    for (int k = 0; k < R.nmat; ++k)
-      R.mcc[k] = int16_t(R.mrows[k] > 0 ? std::max(2, (A.chunk / R.mrows[k]) & ~1) : 2);
+  for (std::vector<WRec>* L : {&recs, &lrecs, &ltrecs})
+    for (WRec& R : *L)  // columns per ring chunk (even; a chunk holds >= 2 columns)
+      for (int k = 0; k < R.nmat; ++k)
+        R.mcc[k] = int16_t(R.mrows[k] > 0 ? std::max(2, (A.chunk / R.mrows[k]) & ~1) : 2);
   CK(wide_configure(wide_rows_, wide_ctas_, bytes));
   int occ = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wide_kernel_ptr(wide_rows_, wide_ctas_), 32 * A.warps,
@@ -550,7 +624,21 @@ void Engine::setup_wide(bool force) {
   if (occ < 1) return;
   // every CTA must be resident (items spin on flags of smaller tickets)
   wide_grid_ = occ * sms;
-  wide_grid_ = std::max(1, std::min(wide_grid_, (total + A.warps - 1) / A.warps));
+  // latency configuration for launches with about one item per warp (standalone
+  // L / L* on narrow trees): one CTA per SM, few warps, 16-slot rings so a
+  // warp's whole item is requested at once instead of one chunk per round trip
+  wlat_ = A;
+  wlat_.slots = 16;
+  wlat_.warps = 4;
+  while (wlat_.warps > 1 && wide_smem_bytes(wlat_) > smem_optin - 2048) --wlat_.warps;
+  while (wide_smem_bytes(wlat_) > smem_optin - 2048 && wlat_.slots > 2) wlat_.slots /= 2;
+  {
+    const int lb = wide_smem_bytes(wlat_);
+    CK(wide_configure(wide_rows_, 1, wide_ctas_ == 1 ? std::max(lb, bytes) : lb));
+    int occl = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occl, wide_kernel_ptr(wide_rows_, 1), 32 * wlat_.warps, lb));
+    wide_grid_lat_ = std::max(1, occl) * sms;
+  }
   WRec* drec = nullptr;
   CK(cudaMalloc(&drec, sizeof(WRec) * recs.size()));
   allocs_.push_back(drec);
@@ -559,6 +647,13 @@ void Engine::setup_wide(bool force) {
   A.recs = drec;
   A.ntick = total;
   wrecs_ = std::move(recs);
+  lrec_ = dalloc<WRec>(lrecs.size());
+  ltrec_ = dalloc<WRec>(ltrecs.size());
+  CK(cudaMemcpyAsync(lrec_, lrecs.data(), sizeof(WRec) * lrecs.size(), cudaMemcpyHostToDevice, st_));
+  CK(cudaMemcpyAsync(ltrec_, ltrecs.data(), sizeof(WRec) * ltrecs.size(), cudaMemcpyHostToDevice, st_));
+  nlrec_ = int(lrecs.size());
+  nltrec_ = int(ltrecs.size());
+  CK(cudaStreamSynchronize(st_));
   A.vb[WB_QK] = D_.qk, A.vb[WB_GD] = D_.gd, A.vb[WB_H] = D_.h, A.vb[WB_G] = D_.g, A.vb[WB_QKN] = D_.qkN;
   A.vb[WB_GDN] = D_.gNd, A.vb[WB_CV] = D_.cvec, A.vb[WB_A] = D_.a, A.vb[WB_LO] = D_.lo, A.vb[WB_HI] = D_.hi;
   A.vb[WB_RB] = D_.rb, A.vb[WB_AN] = D_.aN, A.vb[WB_LON] = D_.loN, A.vb[WB_HIN] = D_.hiN;
@@ -569,6 +664,7 @@ void Engine::setup_wide(bool force) {
   A.flagF = wide_flags_ + nn + nnl;
   if (knob("SPOCK_WIDE_PROF", 0)) A.prof = dalloc<unsigned long long>(16);
   wide_ok_ = true;
+  t_wide_ = t_wide;
 }
 
 // ---------------------------------------------------------------------------
@@ -731,7 +827,7 @@ void Engine::shard_T_A(const double* z, const double* eta, double* zo, double* e
   A.recs = S.recA;
   A.ntick = S.nA;
   CK(cudaMemsetAsync(wide_flags_, 0, wide_flag_bytes_, st_));
-  if (S.nA > 0) launch_T_wide(A, wide_rows_, wide_ctas_, std::min(wide_grid_, (S.nA + A.warps - 1) / A.warps), st_);
+  if (S.nA > 0) launch_wide(A, S.recA, S.nA);
   ShardXArgs X{D_, z, eta, S.xidx, S.xbuf, S.bfirst, S.b0, S.b1, S.E, nullptr};
   launch_shard_pack(X, st_);
 }
@@ -747,7 +843,7 @@ void Engine::shard_T_B(const double* z, const double* eta, double* zo, double* e
   A.D = D_, A.z = z, A.eta = eta, A.zo = zo, A.eo = eo, A.alpha = alpha_;
   A.recs = S.recB;
   A.ntick = S.nB;
-  if (S.nB > 0) launch_T_wide(A, wide_rows_, wide_ctas_, std::min(wide_grid_, (S.nB + A.warps - 1) / A.warps), st_);
+  if (S.nB > 0) launch_wide(A, S.recB, S.nB);
 }
 
 void Engine::wide_profile(unsigned long long* out) {
@@ -1344,7 +1440,26 @@ void Engine::sync() { CK(cudaStreamSynchronize(st_)); }
 
 // standalone L / L*: CTA-per-node kernels on narrow trees (latency), warp-per-
 // node kernels on wide ones (throughput); same arithmetic
+// one launch of the streaming kernel over a ticket list: the throughput
+// configuration, or the latency one when there is about one item per warp
+void Engine::launch_wide(WideArgs A, const WRec* recs, int ntick) {
+  A.recs = recs;
+  A.ntick = ntick;
+  if (ntick <= wide_grid_lat_ * wlat_.warps) {
+    A.warps = wlat_.warps, A.slots = wlat_.slots;
+    launch_T_wide(A, wide_rows_, 1, std::min(wide_grid_lat_, (ntick + A.warps - 1) / A.warps), st_);
+  } else {
+    launch_T_wide(A, wide_rows_, wide_ctas_, std::min(wide_grid_, (ntick + A.warps - 1) / A.warps), st_);
+  }
+}
+
 void Engine::L(const double* z, double* eta) {
+  if (wide_ok_ && lop_wide_) {  // warp-granular streaming items (wide.cu, kind 3)
+    WideArgs A = wargs_;
+    A.D = D_, A.z = z, A.eo = eta;
+    launch_wide(A, lrec_, nlrec_);
+    return;
+  }
   if (narrow_)
     launch_L_narrow(D_, z, eta, st_);
   else
@@ -1352,6 +1467,13 @@ void Engine::L(const double* z, double* eta) {
 }
 
 void Engine::Lt(const double* eta, double* z) {
+  if (wide_ok_ && lop_wide_) {  // kinds 4 (child terms, flagged) then 5 (node rows)
+    WideArgs A = wargs_;
+    A.D = D_, A.eta = eta, A.zo = z;
+    CK(cudaMemsetAsync(wide_flags_, 0, sizeof(int) * size_t(p_.tree.nn()), st_));
+    launch_wide(A, ltrec_, nltrec_);
+    return;
+  }
   if (narrow_)
     launch_Lt_narrow(D_, eta, z, st_);
   else
@@ -1375,7 +1497,7 @@ void Engine::T(const double* z, const double* eta, double* zo, double* eo) {
     launch_T_fused(F, fused_grid_, st_);
     return;
   }
-  if (wide_ok_) {
+  if (t_wide_) {
     WideArgs A = wargs_;
     A.D = D_;
     A.z = z;

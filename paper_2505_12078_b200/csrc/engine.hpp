@@ -86,10 +86,10 @@ class Engine {
   cudaStream_t stream() const { return st_; }
   double* scratch_z(int k) const { return scratch_z_[k]; }
   double* scratch_e(int k) const { return scratch_e_[k]; }
-  int launches_per_T() const { return (fused_ok_ || wide_ok_) ? 1 : 2 + 2 * (p_.tree.horizon + 1) + 1 + 1; }
+  int launches_per_T() const { return (fused_ok_ || t_wide_) ? 1 : 2 + 2 * (p_.tree.horizon + 1) + 1 + 1; }
   // SPOCK_WIDE_PROF=1: cycle counters of the wide kernel (summed over warps and launches)
   void wide_profile(unsigned long long* out10);
-  const char* t_path() const { return fused_ok_ ? "fused" : (wide_ok_ ? "wide" : "stages"); }
+  const char* t_path() const { return fused_ok_ ? "fused" : (t_wide_ ? "wide" : "stages"); }
 
  private:
   void upload();
@@ -142,7 +142,15 @@ class Engine {
   FusedArgs fargs_{};
   int fused_grid_ = 0;
   size_t fused_sync_bytes_ = 0;
-  bool wide_ok_ = false;
+  bool wide_ok_ = false;  // streaming kernel set up (records, smem, grid)
+  bool t_wide_ = false;   // T runs on it
+  bool lop_wide_ = true;  // standalone L / L* run on it
+  WideArgs wlat_{};
+  int wide_grid_lat_ = 0;
+  void launch_wide(WideArgs A, const WRec* recs, int ntick);
+  WRec* lrec_ = nullptr;
+  WRec* ltrec_ = nullptr;
+  int nlrec_ = 0, nltrec_ = 0;
   WideArgs wargs_{};
   int wide_grid_ = 0, wide_rows_ = 0, wide_ctas_ = 1;
   int max_dense_s2_ = 0;

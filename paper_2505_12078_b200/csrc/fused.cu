@@ -100,7 +100,7 @@ constexpr int kScratchSlots = 6;
 
 int fused_smem_bytes(const FusedArgs& F) {
   return int(sizeof(double) * (size_t(F.nslots) * (size_t(F.mat_doubles) + F.vec_doubles) +
-                               kScratchSlots * kSlotD + 2 * 256));
+                               kScratchSlots * kSlotD + size_t(F.red_doubles)));
 }
 
 cudaError_t fused_configure(int smem_bytes, int threads) {

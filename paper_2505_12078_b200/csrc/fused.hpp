@@ -50,6 +50,7 @@ struct FusedArgs {
   int stage_all;               // 1: stage every block; 0: only the critical-path blocks
   int nslots;                  // 1 or 2 (prefetch ring depth)
   int threads;                 // 128 or 256 threads per CTA
+  int red_doubles;             // shared scratch of the CTA GEMVs: (threads / 32) * max GEMV rows
   const ItemRec* items;        // [nnl + 2 nn]
   unsigned long long* trace;   // optional: 4 globaltimer stamps per item (debug/profiling)
   const double* base[FB_COUNT];

@@ -79,69 +79,88 @@ __device__ __forceinline__ void cta_release(int* flag) {
   if (threadIdx.x == 0) st_release(flag, 1);
 }
 
-// y[r] = (acc ? y[r] : 0) + sum_c A[r + c*lda] x[c], r < m <= kFT; all threads
-// participate (column slices reduced in fixed order => deterministic).
+// Partial GEMV of one warp over its column block [c0, c1): lanes own rows
+// (r = lane + 32k), RB independent accumulators per pass, partial sums to
+// red[w * ldr + r].  Used by cta_gemv / cta_gemv2 below.
+template <int RB>
+__device__ __forceinline__ void warp_cols_gemv(const double* A, int m, int lda, const double* x, int c0, int c1,
+                                               double* redw) {
+  const int l = threadIdx.x & 31;
+  for (int rb = 0; rb < m; rb += 32 * RB) {
+    double a[RB];
+#pragma unroll
+    for (int k = 0; k < RB; ++k) a[k] = 0.0;
+    int c = c0;
+    for (; c + 2 <= c1; c += 2) {
+      const double x0 = x[c], x1 = x[c + 1];
+      const double* col0 = A + size_t(c) * lda;
+      const double* col1 = col0 + lda;
+#pragma unroll
+      for (int k = 0; k < RB; ++k) {
+        const int r = rb + l + 32 * k;
+        if (r < m) {
+          a[k] = fma(col0[r], x0, a[k]);
+          a[k] = fma(col1[r], x1, a[k]);
+        }
+      }
+    }
+    for (; c < c1; ++c) {
+      const double xc = x[c];
+      const double* col = A + size_t(c) * lda;
+#pragma unroll
+      for (int k = 0; k < RB; ++k) {
+        const int r = rb + l + 32 * k;
+        if (r < m) a[k] = fma(col[r], xc, a[k]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < RB; ++k) {
+      const int r = rb + l + 32 * k;
+      if (r < m) redw[r] = a[k];
+    }
+  }
+}
+
+// y[r] = (acc ? y[r] : 0) + sum_c A[r + c*lda] x[c].  The columns are split in
+// kFT/32 contiguous blocks, one per warp (lanes over rows, independent
+// accumulators), and the warp partials are summed in warp order: a short
+// dependent chain per thread and a fixed, run-to-run identical summation order.
+// red holds (kFT/32) * m doubles.
 __device__ void cta_gemv(const double* A, int m, int n, int lda, const double* x, double* y, bool acc,
                          double* red) {
-  const int t = threadIdx.x;
+  constexpr int NW = kFT / 32;
   if (m <= 0) return;
-  if (m > kFT) {  // tall: one thread per row, rows strided by the CTA size
-    for (int r = t; r < m; r += kFT) {
-      double v = acc ? y[r] : 0.0;
-      for (int c = 0; c < n; ++c) v = fma(A[r + size_t(c) * lda], x[c], v);
-      y[r] = v;
-    }
-    __syncthreads();
-    return;
-  }
-  const int slices = max(1, kFT / m);
-  const int r = t % m, s = t / m;
-  double v = 0.0;
-  if (s < slices && n > 0) {
-    int c = s;
-    for (; c + 3 * slices < n; c += 4 * slices) {
-      v = fma(A[r + size_t(c) * lda], x[c], v);
-      v = fma(A[r + size_t(c + slices) * lda], x[c + slices], v);
-      v = fma(A[r + size_t(c + 2 * slices) * lda], x[c + 2 * slices], v);
-      v = fma(A[r + size_t(c + 3 * slices) * lda], x[c + 3 * slices], v);
-    }
-    for (; c < n; c += slices) v = fma(A[r + size_t(c) * lda], x[c], v);
-  }
-  if (t < m * slices) red[t] = v;
+  const int w = threadIdx.x >> 5;
+  const int cb = (n + NW - 1) / NW;
+  const int c0 = min(n, w * cb), c1 = min(n, c0 + cb);
+  warp_cols_gemv<4>(A, m, lda, x, c0, c1, red + size_t(w) * m);
   __syncthreads();
-  if (t < m) {
+  for (int t = threadIdx.x; t < m; t += kFT) {
     double o = acc ? y[t] : 0.0;
-    for (int j = 0; j < slices; ++j) o += red[t + j * m];
+#pragma unroll
+    for (int j = 0; j < NW; ++j) o += red[size_t(j) * m + t];
     y[t] = o;
   }
   __syncthreads();
 }
 
-// y1 = A1 x1 (m1 rows) and y2 = A2 x2 (m2 rows) in one pass: rows of both are
-// spread over the CTA (column slices, fixed-order reduction)
+// y1 = A1 x1 (m1 rows) and y2 = A2 x2 (m2 rows) in one pass and one barrier
+// pair: every warp takes a column block of each product.  red holds
+// (kFT/32) * (m1 + m2) doubles.
 __device__ void cta_gemv2(const double* A1, int m1, int n1, int lda1, const double* x1, double* y1,
                           const double* A2, int m2, int n2, int lda2, const double* x2, double* y2, double* red) {
-  const int t = threadIdx.x, m = m1 + m2;
-  if (m > kFT) {
-    cta_gemv(A1, m1, n1, lda1, x1, y1, false, red);
-    cta_gemv(A2, m2, n2, lda2, x2, y2, false, red);
-    return;
-  }
-  const int slices = max(1, kFT / m);
-  const int r = t % m, s = t / m;
-  double v = 0.0;
-  if (s < slices) {
-    const bool one = r < m1;
-    const double* A = one ? A1 : A2;
-    const double* x = one ? x1 : x2;
-    const int rr = one ? r : r - m1, n = one ? n1 : n2, lda = one ? lda1 : lda2;
-    for (int c = s; c < n; c += slices) v = fma(A[rr + size_t(c) * lda], x[c], v);
-  }
-  if (t < m * slices) red[t] = v;
+  constexpr int NW = kFT / 32;
+  const int w = threadIdx.x >> 5, m = m1 + m2;
+  const int cb1 = (n1 + NW - 1) / NW, cb2 = (n2 + NW - 1) / NW;
+  const int a0 = min(n1, w * cb1), a1 = min(n1, a0 + cb1);
+  const int b0 = min(n2, w * cb2), b1 = min(n2, b0 + cb2);
+  warp_cols_gemv<4>(A1, m1, lda1, x1, a0, a1, red + size_t(w) * m);
+  warp_cols_gemv<2>(A2, m2, lda2, x2, b0, b1, red + size_t(w) * m + m1);
   __syncthreads();
-  if (t < m) {
+  for (int t = threadIdx.x; t < m; t += kFT) {
     double o = 0.0;
-    for (int j = 0; j < slices; ++j) o += red[t + j * m];
+#pragma unroll
+    for (int j = 0; j < NW; ++j) o += red[size_t(j) * m + t];
     if (t < m1)
       y1[t] = o;
     else
@@ -702,7 +721,7 @@ __global__ void __launch_bounds__(kFT, 1) k_T_fused(FusedArgs F) {
   __shared__ ItemRec recs[2];
   const int t = threadIdx.x;
   double* scratch = dsm + F.nslots * (size_t(F.mat_doubles) + F.vec_doubles);
-  double* red = scratch + kScratch * kSlot;
+  double* red = scratch + kScratch * kSlot;  // F.red_doubles (GEMV warp partials, CTA sums)
   if (t == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);

@@ -43,7 +43,7 @@ namespace spock {
 
 namespace {
 
-constexpr int kMaxSlots = 8;
+constexpr int kMaxSlots = 16;
 constexpr int kRecSlots = 4;  // record ring: tickets j .. j+3
 
 // span ids (WRec::voff/vcnt/vbase index); leaf items alias the non-leaf ids
@@ -51,6 +51,12 @@ enum : int { B_HEAD = 0, B_QK, B_ZX, B_ZU, B_EC, B_GD, B_H, B_G };
 enum : int { B_SEG3 = B_ZU, B_GDN = B_GD, B_QKN = B_H };
 enum : int { F_ZX = 0, F_ZU, F_AX, F_AU, F_CV, F_SEG2, F_A, F_QK, F_SEG1, F_RB, F_GD, F_LO, F_HI, F_ZY, F_ZT, F_ZS };
 enum : int { F_SEG3 = F_SEG1, F_AN = F_RB, F_QKN = F_GD, F_GDN = F_LO, F_LON = F_HI, F_HIN = F_ZY };
+// standalone L (kind 3), L* child terms (kind 4), L* node rows (kind 5)
+enum : int { L_ZX = 0, L_ZU, L_AX, L_AU, L_QK, L_ZT, L_ZS, L_Y, L_RB, L_GD, L_QKN };
+enum : int { L_GDN = L_GD };
+enum : int { LC_HEAD = 0, LC_QK };
+enum : int { LN_SEG1 = 0, LN_RB, LN_GD, LN_QKN };
+enum : int { LN_SEG3 = LN_SEG1, LN_GDN = LN_GD };
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -941,6 +947,250 @@ __device__ void w_fwd(const WideArgs& A, Ring& R, const WRec& rc, const Spans& s
   }
 }
 
+// ---------------------------------------------------------------------------
+// Standalone L (TreeOperator::apply, tree_operator.cpp:20-63): eta_out = L z,
+// all rows owned by node i.  Streamed: Hx, Hu (non-root) | HN (leaf).
+template <int RR>
+__device__ void w_L(const WideArgs& A, Ring& R, const WRec& rc, const Spans& sp, const SpanWait& W, double* xs,
+                    double* xs2) {
+  const Dev& D = A.D;
+  const int l = lane_id(), nx = D.nx, nu = D.nu;
+  double* eo = A.eo;
+  const int i = rc.node;
+  const bool root = i == 0, leaf = rc.nch == 0;
+  spans_ready(R, W);
+  double acc[RR];
+  if (!leaf) {  // y-copy rows, risk scalar s - b'y, constraint rows G [x; u]
+    const int ny = rc.ny, so = rc.so, nc = rc.nc;
+    const double* zy = sp(L_Y);
+    const double* rb = sp(L_RB);
+    double part = 0.0;
+    for (int r = l; r < ny; r += 32) {
+      const double yv = zy[r];
+      part += rb[r] * yv;
+      eo[so + r] = yv;
+    }
+    const double by = warp_sum(part);
+    if (l == 0) eo[so + ny] = sp(L_ZS)[0] - by;
+    const double* zx = sp(L_ZX);
+    const double* zu = sp(L_ZU);
+    for (int r = l; r < nx; r += 32) xs[r] = zx[r];
+    for (int r = l; r < nu; r += 32) xs[nx + r] = zu[r];
+    __syncwarp();
+    zero(acc);
+    if (D.g_diag) {
+      const double* gd = sp(L_GD);
+#pragma unroll
+      for (int kk = 0; kk < RR; ++kk) {
+        const int r = l + 32 * kk;
+        if (r < nc) acc[kk] = gd[r] * xs[r];
+      }
+    } else {
+      gemv_glob<RR>(D.Gx + D.g_off[i] * nx, nc, nx, nc, xs, acc);
+      gemv_glob<RR>(D.Gu + D.g_off[i] * nu, nc, nu, nc, xs + nx, acc);
+    }
+#pragma unroll
+    for (int kk = 0; kk < RR; ++kk) {
+      const int r = l + 32 * kk;
+      if (r < nc) eo[so + ny + 1 + r] = acc[kk];
+    }
+    __syncwarp();
+  }
+  if (!root) {  // stage-cost SOC block of (x_anc, u_anc, tau_i)
+    const int px = rc.px, pu = rc.pu, p = px + pu, o2 = rc.s2o;
+    const double* zax = sp(L_AX);
+    const double* zau = sp(L_AU);
+    for (int r = l; r < nx; r += 32) xs2[r] = zax[r];
+    for (int r = l; r < nu; r += 32) xs2[nx + r] = zau[r];
+    __syncwarp();
+    const double* qk = sp(L_QK);
+    double part = 0.0;
+    for (int r = l; r < nx + nu; r += 32) part += qk[r] * xs2[r];
+    const double qd = warp_sum(part);
+    double ax[RR], au[RR];
+    zero(ax);
+    zero(au);
+    sgemv<RR>(R, xs2, ax);       // Hx x_anc
+    sgemv<RR>(R, xs2 + nx, au);  // Hu u_anc
+#pragma unroll
+    for (int kk = 0; kk < RR; ++kk) {
+      const int r = l + 32 * kk;
+      if (r < px) eo[o2 + r] = ax[kk];
+      if (r < pu) eo[o2 + px + r] = au[kk];
+    }
+    if (l == 0) {
+      const double row = 0.5 * sp(L_ZT)[0] - 0.5 * qd;
+      eo[o2 + p] = row;
+      eo[o2 + p + 1] = row;
+    }
+    __syncwarp();
+  }
+  if (leaf) {  // G_N x and the terminal SOC block of (x, s)
+    const int j = i - D.nnl, nc = rc.nc, p = rc.pN, e3 = rc.so;
+    const double* zx = sp(L_ZX);
+    for (int r = l; r < nx; r += 32) xs[r] = zx[r];
+    __syncwarp();
+    zero(acc);
+    if (D.gN_diag) {
+      const double* gd = sp(L_GDN);
+#pragma unroll
+      for (int kk = 0; kk < RR; ++kk) {
+        const int r = l + 32 * kk;
+        if (r < nc) acc[kk] = gd[r] * xs[r];
+      }
+    } else {
+      gemv_glob<RR>(D.GN + D.gN_off[j] * nx, nc, nx, nc, xs, acc);
+    }
+#pragma unroll
+    for (int kk = 0; kk < RR; ++kk) {
+      const int r = l + 32 * kk;
+      if (r < nc) eo[e3 + r] = acc[kk];
+    }
+    const double* qk = sp(L_QKN);
+    double part = 0.0;
+    for (int r = l; r < nx; r += 32) part += qk[r] * xs[r];
+    const double qd = warp_sum(part);
+    zero(acc);
+    sgemv<RR>(R, xs, acc);  // H_N x
+#pragma unroll
+    for (int kk = 0; kk < RR; ++kk) {
+      const int r = l + 32 * kk;
+      if (r < p) eo[e3 + nc + r] = acc[kk];
+    }
+    if (l == 0) {
+      const double row = 0.5 * sp(L_ZS)[0] - 0.5 * qd;
+      eo[e3 + nc + p] = row;
+      eo[e3 + nc + p + 1] = row;
+    }
+  }
+}
+
+// L* child terms of node i (tree_operator.cpp:80-88): adj_i = H_i' head_i -
+// rsum/2 qk_i for the parent, and the tau_i slot.  Streamed: HxT, HuT.
+template <int RR>
+__device__ void w_Lt_child(const WideArgs& A, Ring& R, const WRec& rc, const Spans& sp, const SpanWait& W) {
+  const Dev& D = A.D;
+  const int l = lane_id(), nx = D.nx, nu = D.nu, m = nx + nu;
+  const int i = rc.node, k = i - 1, px = rc.px, pu = rc.pu, p = px + pu;
+  spans_ready(R, W);
+  const double* head = sp(LC_HEAD);
+  const double rsum = head[p] + head[p + 1];
+  const double* qk = sp(LC_QK);
+  double* adj = D.adj + size_t(k) * m;
+  double acc[RR];
+#pragma unroll
+  for (int kk = 0; kk < RR; ++kk) {
+    const int r = l + 32 * kk;
+    acc[kk] = r < nx ? -0.5 * rsum * qk[r] : 0.0;
+  }
+  sgemv<RR>(R, head, acc);
+#pragma unroll
+  for (int kk = 0; kk < RR; ++kk) {
+    const int r = l + 32 * kk;
+    if (r < nx) adj[r] = acc[kk];
+  }
+#pragma unroll
+  for (int kk = 0; kk < RR; ++kk) {
+    const int r = l + 32 * kk;
+    acc[kk] = r < nu ? -0.5 * rsum * qk[nx + r] : 0.0;
+  }
+  sgemv<RR>(R, head + px, acc);
+#pragma unroll
+  for (int kk = 0; kk < RR; ++kk) {
+    const int r = l + 32 * kk;
+    if (r < nu) adj[nx + r] = acc[kk];
+  }
+  if (l == 0) A.zo[D.tau_base + k] = 0.5 * rsum;
+  w_release(A.flagB + i);
+}
+
+// L* rows of node i (tree_operator.cpp:75-79,89-113): own segments plus the
+// ascending sum of the children's adj.  Streamed: HNT (leaf).
+template <int RR>
+__device__ void w_Lt_node(const WideArgs& A, Ring& R, const WRec& rc, const Spans& sp, const SpanWait& W) {
+  const Dev& D = A.D;
+  const int l = lane_id(), nx = D.nx, nu = D.nu, m = nx + nu;
+  double* zo = A.zo;
+  const int i = rc.node;
+  const bool leaf = rc.nch == 0;
+  double vx[RR], vu[RR];
+  zero(vx);
+  zero(vu);
+  if (!leaf) {
+    const int c0 = rc.c0, nch = rc.nch;
+    long long t0 = 0;
+    if (R.prof) t0 = clock64();
+    for (int k = l; k < nch; k += 32) wait_flag(A.flagB + c0 + k);
+    __syncwarp();
+    if (R.prof) R.t_flag += clock64() - t0;
+    for (int c = 0; c < nch; ++c) {  // ascending child order
+      const double* ad = D.adj + size_t(c0 + c - 1) * m;
+#pragma unroll
+      for (int kk = 0; kk < RR; ++kk) {
+        const int r = l + 32 * kk;
+        if (r < nx) vx[kk] += ldcg(ad + r);
+        if (r < nu) vu[kk] += ldcg(ad + nx + r);
+      }
+    }
+  }
+  spans_ready(R, W);
+  if (!leaf) {
+    const int ny = rc.ny, yo = rc.yo, nc = rc.nc;
+    const double* seg1 = sp(LN_SEG1);
+    const double* rb = sp(LN_RB);
+    const double sc = seg1[ny];
+    for (int r = l; r < ny; r += 32) zo[yo + r] = seg1[r] - sc * rb[r];
+    if (l == 0) zo[i == 0 ? 0 : D.s_base + i - 1] = sc;
+    const double* ec = seg1 + ny + 1;
+    double gx[RR], gu[RR];
+    zero(gx);
+    zero(gu);
+    if (D.g_diag) {
+      const double* gd = sp(LN_GD);
+#pragma unroll
+      for (int kk = 0; kk < RR; ++kk) {
+        const int r = l + 32 * kk;
+        if (r < nx) gx[kk] = gd[r] * ec[r];
+        if (r < nu) gu[kk] = gd[nx + r] * ec[nx + r];
+      }
+    } else {
+      gemv_glob<RR>(D.GxT + D.g_off[i] * nx, nx, nc, nx, ec, gx);
+      gemv_glob<RR>(D.GuT + D.g_off[i] * nu, nu, nc, nu, ec, gu);
+    }
+#pragma unroll
+    for (int kk = 0; kk < RR; ++kk) {
+      const int r = l + 32 * kk;
+      if (r < nx) zo[1 + size_t(i) * nx + r] = gx[kk] + vx[kk];
+      if (r < nu) zo[D.u_base + size_t(i) * nu + r] = gu[kk] + vu[kk];
+    }
+  } else {
+    const int j = i - D.nnl, nc = rc.nc, p = rc.pN;
+    const double* ec = sp(LN_SEG3);
+    const double* hd = ec + nc;
+    const double rsum = hd[p] + hd[p + 1];
+    double acc[RR];
+    zero(acc);
+    if (D.gN_diag) {
+      const double* gd = sp(LN_GDN);
+#pragma unroll
+      for (int kk = 0; kk < RR; ++kk) {
+        const int r = l + 32 * kk;
+        if (r < nx) acc[kk] = gd[r] * ec[r];
+      }
+    } else {
+      gemv_glob<RR>(D.GNT + D.gN_off[j] * nx, nx, nc, nx, ec, acc);
+    }
+    sgemv<RR>(R, hd, acc);
+    const double* qk = sp(LN_QKN);
+#pragma unroll
+    for (int kk = 0; kk < RR; ++kk) {
+      const int r = l + 32 * kk;
+      if (r < nx) zo[1 + size_t(i) * nx + r] = acc[kk] - 0.5 * rsum * qk[r];
+    }
+    if (l == 0) zo[D.s_base + i - 1] = 0.5 * rsum;
+  }
+}
+
 // per-warp shared-memory footprint in doubles (16-byte multiples)
 __host__ __device__ __forceinline__ size_t warp_doubles(int S, int CH, int VR, int VD) {
   return size_t(S) * CH + size_t(VR) + 3 * size_t(VD) + kRecSlots * 32 + 8 /*doff*/ + kMaxSlots + kRecSlots + 2;
@@ -949,7 +1199,6 @@ __host__ __device__ __forceinline__ size_t warp_doubles(int S, int CH, int VR, i
 template <int RR, int MINB>
 __global__ void __launch_bounds__(256, MINB) k_T_wide(const __grid_constant__ WideArgs A) {
   extern __shared__ __align__(128) double wsm[];
-  const Dev& D = A.D;
   const int w = threadIdx.x >> 5, l = lane_id();
   const int S = A.slots, CH = A.chunk, VR = A.vrec, VD = A.vecd;
   double* ring = wsm + size_t(w) * warp_doubles(S, CH, VR, VD);
@@ -1008,7 +1257,7 @@ __global__ void __launch_bounds__(256, MINB) k_T_wide(const __grid_constant__ Wi
     request(2);
   }
   __syncwarp();
-  long long t_kind[3] = {0, 0, 0};
+  long long t_kind[3] = {0, 0, 0};  // backward / S2 / forward (+ L, L* items counted as forward)
   int n_kind[3] = {0, 0, 0};
   const long long t_start = R.prof ? clock64() : 0;
   for (int j = 0; R.gw + j * R.stride < R.total; ++j) {
@@ -1034,17 +1283,19 @@ __global__ void __launch_bounds__(256, MINB) k_T_wide(const __grid_constant__ Wi
     __syncwarp();
     const SpanWait W{sbar, uint32_t(j) & 1u};
     Spans sp{&A, &rc, vrec, doff};
-    if (kind == 0)
-      w_back<RR>(A, R, rc, sp, W, xs, xs2);
-    else if (kind == 1)
-      w_s2(A, rc.node, xs);
-    else
-      w_fwd<RR>(A, R, rc, sp, W, xs, xs2, dep);
+    switch (kind) {
+      case 0: w_back<RR>(A, R, rc, sp, W, xs, xs2); break;
+      case 1: w_s2(A, rc.node, xs); break;
+      case 2: w_fwd<RR>(A, R, rc, sp, W, xs, xs2, dep); break;
+      case 3: w_L<RR>(A, R, rc, sp, W, xs, xs2); break;
+      case 4: w_Lt_child<RR>(A, R, rc, sp, W); break;
+      default: w_Lt_node<RR>(A, R, rc, sp, W); break;
+    }
     if (kind == 1) spans_ready(R, W);  // keep the span barrier's phase in step
     __syncwarp();
     if (R.prof) {
-      t_kind[kind] += clock64() - t0;
-      ++n_kind[kind];
+      t_kind[min(kind, 2)] += clock64() - t0;
+      ++n_kind[min(kind, 2)];
     }
   }
   if (A.prof && l == 0) {  // optional: per-warp cycle accounting, summed over warps

@@ -123,3 +123,27 @@ def test_wide_cp_trace_matches_oracle():
     assert a.status["branches"] == b.status["branches"]
     np.testing.assert_allclose(a.status["rnorm_history"], b.status["rnorm_history"], rtol=1e-7, atol=1e-12)
     np.testing.assert_allclose(a.z_scaled, b.z_scaled, rtol=1e-7, atol=1e-9)
+
+
+@pytest.mark.parametrize("lop", ["0", "1"])
+@pytest.mark.parametrize("name,p", PROBLEMS[:3] + PROBLEMS[-2:], ids=[n for n, _ in PROBLEMS[:3] + PROBLEMS[-2:]])
+def test_standalone_L_Lt_both_schedules(lop, name, p):
+    """TreeOperator::apply / apply_adjoint (tree_operator.cpp:20-114) on the
+    streaming kernel (SPOCK_LOP_WIDE=1) and on the CTA-per-node kernels (0)."""
+    from paper_2505_12078_b200.solver import SpockSolver
+    old = os.environ.get("SPOCK_LOP_WIDE")
+    os.environ["SPOCK_LOP_WIDE"] = lop
+    try:
+        g = SpockSolver(p)
+    finally:
+        if old is None:
+            os.environ.pop("SPOCK_LOP_WIDE", None)
+        else:
+            os.environ["SPOCK_LOP_WIDE"] = old
+    o = OracleSolver(p, alpha=g.alpha)
+    z = _rand(g.nz, 8)
+    e = _rand(g.neta, 9)
+    le, lo_ = g.apply_L(z), o.apply_L(z)
+    te, to_ = g.apply_Lt(e), o.apply_Lt(e)
+    assert float(np.abs(le - lo_).max()) <= 1e-12 * max(1.0, float(np.abs(lo_).max()))
+    assert float(np.abs(te - to_).max()) <= 1e-12 * max(1.0, float(np.abs(to_).max()))
