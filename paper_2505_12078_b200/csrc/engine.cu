@@ -84,6 +84,8 @@ Engine::Engine(const spock_problem_desc* desc, const Params& prm) : prm_(prm) {
   int dev = 0;
   CK(cudaGetDevice(&dev));
   CK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+  set_carveout_all();
+  set_carveout_narrow();
   upload();
   narrow_ = p_.tree.nn() < 4096;
   if (const char* nv = std::getenv("SPOCK_NARROW")) narrow_ = nv[0] == '1';
@@ -126,7 +128,9 @@ void Engine::setup_fused() {
   // critical-only staging; narrow trees favour a 256-thread ring
   const bool wide = nn >= 4096;
   const int sall = knob("SPOCK_FUSED_STAGEALL", wide ? 0 : 1);
-  const int nslots = knob("SPOCK_FUSED_SLOTS", wide ? 1 : 2);
+  // measured in the SuperMann loop (tools/e2e_probe.py): 2 slots on c2 (252 vs 280 ms / 500 it),
+  // 1 slot (two CTAs per SM) on c2p (215 vs 259 ms / 300 it)
+  const int nslots = knob("SPOCK_FUSED_SLOTS", nn < 512 ? 2 : 1);
   const int threads = knob("SPOCK_FUSED_FT", wide ? 128 : 256) == 128 ? 128 : 256;
   int64_t mx = 0, vx = 0;
   for (int i = 0; i < nn; ++i) {
@@ -383,7 +387,8 @@ void Engine::setup_wide(bool force) {
   const int want = knob("SPOCK_T_WIDE", -1);
   const bool t_wide = !fused_ok_ && want != 0 && (want > 0 || nn >= 4096);
   lop_wide_ = knob("SPOCK_LOP_WIDE", nn >= 4096 ? 1 : 0) != 0;
-  if (!t_wide && !lop_wide_ && !force) return;
+  lop_narrow_ = knob("SPOCK_LOP_NARROW", 1) != 0;  // 0: narrow.cu's kernels instead of lop.cu
+  (void)force;  // the records also feed lop.cu's narrow L / L*, so they are always built
   int max_nc = 0, max_ny = 0;
   for (int i = 0; i < nnl; ++i) max_nc = std::max(max_nc, p_.nc[i]);
   for (int j = 0; j < tr.nl(); ++j) max_nc = std::max(max_nc, p_.ncN[j]);
@@ -654,6 +659,33 @@ void Engine::setup_wide(bool force) {
   nlrec_ = int(lrecs.size());
   nltrec_ = int(ltrecs.size());
   CK(cudaStreamSynchronize(st_));
+  // lop.cu (narrow trees): staging capacities from the records
+  {
+    auto staged = [](const WRec& R) {
+      int64_t t = 0;
+      for (int k = 0; k < R.nspan; ++k)
+        if (!((R.unstaged >> k) & 1)) t += pad2(R.vcnt[k]);
+      return t;
+    };
+    auto mats = [](const WRec& R) {
+      int64_t t = 0;
+      for (int k = 0; k < R.nmat; ++k) t += pad2(int64_t(R.mrows[k]) * R.mcols[k]);
+      return t;
+    };
+    int64_t vL = 0, v4 = 0, v5 = 0, mL = 0, m4 = 0, m5 = 0;
+    for (const WRec& R : lrecs) vL = std::max(vL, staged(R)), mL = std::max(mL, mats(R));
+    for (const WRec& R : ltrecs) {
+      if (R.kind == 4) v4 = std::max(v4, staged(R)), m4 = std::max(m4, mats(R));
+      else v5 = std::max(v5, staged(R)), m5 = std::max(m5, mats(R));
+    }
+    lop_rows_ = std::max(m, max_nc);
+    lop_vec_ = int(pad2(std::max(vL, v4 + v5) + 2));
+    lop_mat_ = int(pad2(std::max(mL, 2 * std::max(m4, m5))));
+    // matrices that do not fit are read from global memory inside the GEMVs
+    while (lop_smem_bytes(lop_rows_, lop_mat_, lop_vec_) > smem_optin - 2048 && lop_mat_ > 0)
+      lop_mat_ = int(pad2(lop_mat_ / 2));
+    CK(lop_configure(lop_smem_bytes(lop_rows_, lop_mat_, lop_vec_)));
+  }
   A.vb[WB_QK] = D_.qk, A.vb[WB_GD] = D_.gd, A.vb[WB_H] = D_.h, A.vb[WB_G] = D_.g, A.vb[WB_QKN] = D_.qkN;
   A.vb[WB_GDN] = D_.gNd, A.vb[WB_CV] = D_.cvec, A.vb[WB_A] = D_.a, A.vb[WB_LO] = D_.lo, A.vb[WB_HI] = D_.hi;
   A.vb[WB_RB] = D_.rb, A.vb[WB_AN] = D_.aN, A.vb[WB_LON] = D_.loN, A.vb[WB_HIN] = D_.hiN;
@@ -1454,6 +1486,10 @@ void Engine::launch_wide(WideArgs A, const WRec* recs, int ntick) {
 }
 
 void Engine::L(const double* z, double* eta) {
+  if (wide_ok_ && !lop_wide_ && lop_narrow_) {
+    launch_L_lop(D_, wargs_, lrec_, z, eta, lop_rows_, lop_mat_, lop_vec_, st_);
+    return;
+  }
   if (wide_ok_ && lop_wide_) {  // warp-granular streaming items (wide.cu, kind 3)
     WideArgs A = wargs_;
     A.D = D_, A.z = z, A.eo = eta;
@@ -1467,6 +1503,10 @@ void Engine::L(const double* z, double* eta) {
 }
 
 void Engine::Lt(const double* eta, double* z) {
+  if (wide_ok_ && !lop_wide_ && lop_narrow_) {
+    launch_Lt_lop(D_, wargs_, ltrec_, eta, z, lop_rows_, lop_mat_, lop_vec_, st_);
+    return;
+  }
   if (wide_ok_ && lop_wide_) {  // kinds 4 (child terms, flagged) then 5 (node rows)
     WideArgs A = wargs_;
     A.D = D_, A.eta = eta, A.zo = z;

@@ -145,6 +145,8 @@ class Engine {
   bool wide_ok_ = false;  // streaming kernel set up (records, smem, grid)
   bool t_wide_ = false;   // T runs on it
   bool lop_wide_ = true;  // standalone L / L* run on it
+  bool lop_narrow_ = true;  // else lop.cu (CTA per node, one-shot staging)
+  int lop_rows_ = 0, lop_mat_ = 0, lop_vec_ = 0;
   WideArgs wlat_{};
   int wide_grid_lat_ = 0;
   void launch_wide(WideArgs A, const WRec* recs, int ntick);

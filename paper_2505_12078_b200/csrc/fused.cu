@@ -104,9 +104,12 @@ int fused_smem_bytes(const FusedArgs& F) {
 }
 
 cudaError_t fused_configure(int smem_bytes, int threads) {
-  if (threads == 128)
-    return cudaFuncSetAttribute(fused128::k_T_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
-  return cudaFuncSetAttribute(fused256::k_T_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+  const void* f = threads == 128 ? reinterpret_cast<const void*>(&fused128::k_T_fused)
+                                 : reinterpret_cast<const void*>(&fused256::k_T_fused);
+  // every kernel of the engine prefers the maximum shared-memory carveout, so
+  // consecutive launches never wait for an SM to change its L1 / smem split
+  cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
 }
 
 const void* fused_kernel_ptr(int threads) {

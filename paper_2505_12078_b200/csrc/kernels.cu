@@ -1101,6 +1101,21 @@ void launch_alg1_child_abar(const Alg1Args& P, int count, cudaStream_t st) {
   if (count > 0) k_alg1_child_abar<<<count, 256, 0, st>>>(P);
 }
 
+// every kernel of the engine prefers the maximum shared-memory carveout (see fused.cu)
+void set_carveout_all() {
+  const void* fs[] = {
+      reinterpret_cast<const void*>(&k_Lt_child), reinterpret_cast<const void*>(&k_Lt_node),
+      reinterpret_cast<const void*>(&k_L<true>), reinterpret_cast<const void*>(&k_L<false>),
+      reinterpret_cast<const void*>(&k_s3), reinterpret_cast<const void*>(&k_s1_back),
+      reinterpret_cast<const void*>(&k_s1_fwd), reinterpret_cast<const void*>(&k_s2),
+      reinterpret_cast<const void*>(&k_axpby), reinterpret_cast<const void*>(&k_lincomb),
+      reinterpret_cast<const void*>(&k_gather), reinterpret_cast<const void*>(&k_scatter),
+      reinterpret_cast<const void*>(&k_dots), reinterpret_cast<const void*>(&k_finalize_sum),
+      reinterpret_cast<const void*>(&k_xi), reinterpret_cast<const void*>(&k_finalize_max)};
+  for (const void* f : fs)
+    cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+}
+
 cudaError_t set_alg1_smem(int bytes) {
   return cudaFuncSetAttribute(k_alg1_parent, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }

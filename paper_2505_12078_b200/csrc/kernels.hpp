@@ -80,7 +80,9 @@ void launch_alg1_parent(const Alg1Args& P, int count, cudaStream_t st);
 void launch_alg1_parent2(const Alg1Args& P, int count, cudaStream_t st);
 void launch_alg1_child_abar(const Alg1Args& P, int count, cudaStream_t st);
 cudaError_t set_alg1_smem(int bytes);
+void set_carveout_all();
 // latency-optimised CTA-per-node L / L* (narrow.cu)
+void set_carveout_narrow();
 void launch_L_narrow(const Dev& D, const double* z, double* eta, cudaStream_t st);
 void launch_Lt_narrow(const Dev& D, const double* eta, double* z, cudaStream_t st);
 

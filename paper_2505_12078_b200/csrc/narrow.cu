@@ -222,6 +222,12 @@ __global__ void __launch_bounds__(kT) k_Lt_node_cta(Dev D, const double* __restr
 
 }  // namespace
 
+void set_carveout_narrow() {
+  cudaFuncSetAttribute(k_L_cta, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  cudaFuncSetAttribute(k_Lt_child_cta, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  cudaFuncSetAttribute(k_Lt_node_cta, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+}
+
 void launch_L_narrow(const Dev& D, const double* z, double* eta, cudaStream_t st) {
   k_L_cta<<<std::min(D.nn, 4 * 148), kT, 0, st>>>(D, z, eta);
 }

@@ -1409,6 +1409,12 @@ const void* wide_kernel_ptr(int rows, int ctas) {
 }
 
 cudaError_t wide_configure(int rows, int ctas, int smem_bytes) {
+  cudaFuncSetAttribute(wide_kernel_ptr(rows, ctas), cudaFuncAttributePreferredSharedMemoryCarveout,
+                       cudaSharedmemCarveoutMaxShared);
+  cudaFuncSetAttribute(reinterpret_cast<const void*>(&k_shard_pack), cudaFuncAttributePreferredSharedMemoryCarveout,
+                       cudaSharedmemCarveoutMaxShared);
+  cudaFuncSetAttribute(reinterpret_cast<const void*>(&k_shard_unpack),
+                       cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   return cudaFuncSetAttribute(wide_kernel_ptr(rows, ctas), cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
 }
 

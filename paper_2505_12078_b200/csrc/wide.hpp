@@ -76,6 +76,14 @@ struct ShardXArgs {
 void launch_shard_pack(const ShardXArgs& X, cudaStream_t st);
 void launch_shard_unpack(const ShardXArgs& X, cudaStream_t st);
 
+// standalone L / L* for narrow trees, CTA per node (lop.cu)
+int lop_smem_bytes(int rows, int mat_cap, int vec_cap);
+cudaError_t lop_configure(int bytes);
+void launch_L_lop(const Dev& D, const WideArgs& W, const WRec* lrec, const double* z, double* eta, int rows,
+                  int mat_cap, int vec_cap, cudaStream_t st);
+void launch_Lt_lop(const Dev& D, const WideArgs& W, const WRec* ltrec, const double* eta, double* z, int rows,
+                   int mat_cap, int vec_cap, cudaStream_t st);
+
 int wide_smem_bytes(const WideArgs& A);
 int wide_rows(const Dev& D, int max_nc);  // register row groups (template parameter)
 cudaError_t wide_configure(int rows, int ctas, int smem_bytes);

@@ -125,25 +125,30 @@ def test_wide_cp_trace_matches_oracle():
     np.testing.assert_allclose(a.z_scaled, b.z_scaled, rtol=1e-7, atol=1e-9)
 
 
-@pytest.mark.parametrize("lop", ["0", "1"])
+@pytest.mark.parametrize("lop", ["wide", "lop", "cta"])
 @pytest.mark.parametrize("name,p", PROBLEMS[:3] + PROBLEMS[-2:], ids=[n for n, _ in PROBLEMS[:3] + PROBLEMS[-2:]])
-def test_standalone_L_Lt_both_schedules(lop, name, p):
+def test_standalone_L_Lt_all_schedules(lop, name, p):
     """TreeOperator::apply / apply_adjoint (tree_operator.cpp:20-114) on the
-    streaming kernel (SPOCK_LOP_WIDE=1) and on the CTA-per-node kernels (0)."""
+    streaming kernel (wide.cu), the one-shot CTA-per-node kernels (lop.cu) and
+    narrow.cu's CTA-per-node kernels."""
     from paper_2505_12078_b200.solver import SpockSolver
-    old = os.environ.get("SPOCK_LOP_WIDE")
-    os.environ["SPOCK_LOP_WIDE"] = lop
+    env = {"wide": {"SPOCK_LOP_WIDE": "1"}, "lop": {"SPOCK_LOP_WIDE": "0"},
+           "cta": {"SPOCK_LOP_WIDE": "0", "SPOCK_LOP_NARROW": "0"}}[lop]
+    old = {k: os.environ.get(k) for k in ("SPOCK_LOP_WIDE", "SPOCK_LOP_NARROW")}
+    os.environ.update(env)
     try:
         g = SpockSolver(p)
     finally:
-        if old is None:
-            os.environ.pop("SPOCK_LOP_WIDE", None)
-        else:
-            os.environ["SPOCK_LOP_WIDE"] = old
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
     o = OracleSolver(p, alpha=g.alpha)
-    z = _rand(g.nz, 8)
-    e = _rand(g.neta, 9)
-    le, lo_ = g.apply_L(z), o.apply_L(z)
-    te, to_ = g.apply_Lt(e), o.apply_Lt(e)
-    assert float(np.abs(le - lo_).max()) <= 1e-12 * max(1.0, float(np.abs(lo_).max()))
-    assert float(np.abs(te - to_).max()) <= 1e-12 * max(1.0, float(np.abs(to_).max()))
+    for seed in (8, 11):
+        z = _rand(g.nz, seed)
+        e = _rand(g.neta, seed + 1)
+        le, lo_ = g.apply_L(z), o.apply_L(z)
+        te, to_ = g.apply_Lt(e), o.apply_Lt(e)
+        assert float(np.abs(le - lo_).max()) <= 1e-12 * max(1.0, float(np.abs(lo_).max()))
+        assert float(np.abs(te - to_).max()) <= 1e-12 * max(1.0, float(np.abs(to_).max()))
