@@ -886,6 +886,8 @@ void Engine::wide_profile(unsigned long long* out) {
 }
 
 Engine::~Engine() {
+  for (GraphLoop& G : gloop_)
+    if (G.exec) cudaGraphExecDestroy(G.exec);
   if (wargs_.prof) {  // SPOCK_WIDE_PROF=1: per-warp cycle shares of the wide kernel
     unsigned long long p[13] = {};
     try {
@@ -1777,11 +1779,246 @@ std::vector<double> aa_kappa(const std::vector<double>& G, const std::vector<dou
 }
 
 // ---------------------------------------------------------------------------
+// Device-resident loop (loop.cu): one CUDA graph per solve.
+//   WHILE(h_loop) {
+//     L*(r_eta), xi norms, [history push, Gram]      -> k_begin (termination,
+//     Anderson coefficients, branch) -> [psi]
+//     SWITCH(h_sw) { 0: done | 1: K0 v += psi | 2: M psi, WHILE(h_ls) { trial
+//       v + tau psi, refresh, dots, k_ls }, SWITCH(h_act) { K1 copies | K2 |
+//       KM } | 3: CP v <- T v }
+//     IF(h_ref) { refresh(v), M-norm dots }
+//     k_end (branch record, counters, loop condition)
+//   }
+// The host only launches the graph (in chunks of iterations) and reads the
+// state back; the arithmetic is the host loop's (solve_b) kernel for kernel.
+bool Engine::solve_graph(const double* x_init, const double* wz, const double* we, double* oz, double* ozs,
+                         double* oe, bool supermann, Status& st) {
+  const int m = prm_.aa_memory;
+  if (prm_.cancelled || m > kLoopMaxMem) return false;
+  const char* env = std::getenv("SPOCK_SOLVE_GRAPH");
+  if (env && env[0] == '0') return false;
+  const int64_t nz = lay_.nz, ne = lay_.neta, nv = nz + ne;
+  set_xinit(x_init ? x_init : raw_.x_init.data());
+  GraphLoop& G = gloop_[supermann ? 1 : 0];
+  if (!G.exec) build_loop_graph(G, supermann);
+  const LoopArgs& A = G.A;
+  double *V = A.V, *TV = A.TV, *R = A.R;
+  CK(cudaMemsetAsync(V, 0, sizeof(double) * nv, st_));
+  if (wz || we) {
+    if (!wz || !we) throw std::invalid_argument("solve: warm start has wrong dimensions");
+    copy_in_z(wz, V);
+    to_internal_eta(we, V + nz);
+  }
+  // prologue (solver.cpp:211-235): r = v - T v and its M-norm dots
+  T(V, V + nz, TV, TV + nz);
+  launch_axpby(int(nv), 1.0, V, -1.0, TV, R, st_);
+  L(R, G.Lrz);
+  {
+    DotArgs D{};
+    D.x[0] = R, D.y[0] = R, D.n[0] = int(nz);
+    D.x[1] = R + nz, D.y[1] = G.Lrz, D.n[1] = int(ne);
+    D.x[2] = R + nz, D.y[2] = R + nz, D.n[2] = int(ne);
+    D.ndots = 3;
+    launch_dots(D, partial_, red_out_, st_);
+  }
+  LoopState S0{};
+  S0.reason = -1;
+  S0.n_T = 1;
+  S0.n_L = 1;
+  S0.k_stop = prm_.max_iters + 1;
+  CK(cudaMemcpyAsync(A.st, &S0, sizeof(S0), cudaMemcpyHostToDevice, st_));
+  CK(cudaGraphLaunch(G.exec, st_));
+  LoopState Sh{};
+  CK(cudaMemcpyAsync(&Sh, A.st, sizeof(Sh), cudaMemcpyDeviceToHost, st_));
+  CK(cudaStreamSynchronize(st_));
+  if (Sh.reason == -2) throw std::runtime_error("spock: negative M-norm radicand (alpha too large)");
+  const int iters = Sh.k;
+  std::vector<double> rn(size_t(std::max(iters, 1)));
+  std::vector<char> br(size_t(std::max(iters, 1)));
+  if (iters > 0) {
+    CK(cudaMemcpy(rn.data(), A.rnorm, sizeof(double) * iters, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(br.data(), A.branch, size_t(iters), cudaMemcpyDeviceToHost));
+  }
+  st.iterations = iters;
+  st.reason = Sh.reason < 0 ? SPOCK_MAX_ITERS : Sh.reason;
+  st.xi1 = Sh.xi1;
+  st.xi2 = Sh.xi2;
+  st.k0 = Sh.k0, st.k1 = Sh.k1, st.k2 = Sh.k2, st.stalled = Sh.stalled;
+  st.n_T = Sh.n_T, st.n_L = Sh.n_L, st.n_Lt = Sh.n_Lt;
+  st.rnorm.assign(rn.begin(), rn.begin() + iters);
+  st.branches.assign(br.begin(), br.begin() + iters);
+  if (prm_.progress)  // replayed after the graph (the one behavioural difference)
+    for (int k = 0; k < iters; ++k) prm_.progress(k, rn[k], br[k]);
+  if (ozs) copy_out(TV, ozs, nz);
+  if (oe) from_internal_eta(TV + nz, oe);
+  sync();
+  if (oz) unscale_b(TV, oz);
+  return true;
+}
+
+// Buffers and the instantiated graph of the device-resident loop, built on the
+// first solve of each kind (SuperMann / CP) and reused: pointers are baked in.
+void Engine::build_loop_graph(GraphLoop& G, bool supermann) {
+  const int m = prm_.aa_memory;
+  const int64_t nz = lay_.nz, ne = lay_.neta, nv = nz + ne;
+  auto pair = [&]() { return dalloc<double>(size_t(nv)); };
+  LoopArgs& A = G.A;
+  A = LoopArgs{};
+  double *V = pair(), *TV = pair(), *R = pair(), *C = pair(), *TC = pair(), *CR = pair(), *PV = pair(),
+         *PSI = pair();
+  double* Lrz = dalloc<double>(size_t(ne));
+  double* cLrz = dalloc<double>(size_t(ne));
+  double* Lsre = dalloc<double>(size_t(nz));
+  double* tmpz = dalloc<double>(size_t(nz));
+  double* tmpe = dalloc<double>(size_t(ne));
+  G.Lrz = Lrz;
+  for (int j = 0; j < m + 1 && supermann; ++j) A.RH[j] = pair();
+  for (int j = 0; j < m && supermann; ++j) A.DH[j] = pair();
+  const int cap = prm_.max_iters + 2;
+  A.rnorm = dalloc<double>(size_t(cap));
+  A.branch = dalloc<char>(size_t(cap));
+  A.st = dalloc<LoopState>(1);
+  const double alpha = alpha_;
+  A.P = LoopParams{prm_.eps_abs, prm_.eps_rel, prm_.c0, prm_.c1, prm_.c2, prm_.beta, prm_.sigma, prm_.lambda,
+                   alpha, prm_.max_iters, prm_.max_backtracks, m, supermann ? 1 : 0};
+  A.red = red_out_;
+  A.cap = cap;
+  A.nz = nz;
+  A.nv = nv;
+  A.V = V, A.TV = TV, A.R = R, A.C = C, A.CR = CR, A.PSI = PSI;
+  auto refresh = [&](const double* v, double* tv, double* r, double* lrz) {  // T, r = v - Tv, L rz
+    T(v, v + nz, tv, tv + nz);
+    launch_axpby(int(nv), 1.0, v, -1.0, tv, r, st_);
+    L(r, lrz);
+  };
+  auto mnorm = [&](const double* r, const double* lrz) {
+    DotArgs D{};
+    D.x[0] = r, D.y[0] = r, D.n[0] = int(nz);
+    D.x[1] = r + nz, D.y[1] = lrz, D.n[1] = int(ne);
+    D.x[2] = r + nz, D.y[2] = r + nz, D.n[2] = int(ne);
+    D.ndots = 3;
+    launch_dots(D, partial_, red_out_, st_);
+  };
+  std::vector<cudaGraph_t> owned;
+  auto capture = [&](auto&& f) {
+    cudaGraph_t c;
+    CK(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
+    f();
+    CK(cudaStreamEndCapture(st_, &c));
+    owned.push_back(c);
+    return c;
+  };
+  auto child = [&](cudaGraph_t parent, cudaGraph_t c, cudaGraphNode_t dep) {
+    cudaGraphNode_t n;
+    CK(cudaGraphAddChildGraphNode(&n, parent, dep ? &dep : nullptr, dep ? 1 : 0, c));
+    return n;
+  };
+  auto cond = [&](cudaGraph_t parent, cudaGraphConditionalHandle h, cudaGraphConditionalNodeType type,
+                  unsigned size, cudaGraphNode_t dep, cudaGraph_t* bodies) {
+    cudaGraphNodeParams np{};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = h;
+    np.conditional.type = type;
+    np.conditional.size = size;
+    cudaGraphNode_t n;
+    CK(cudaGraphAddNode(&n, parent, dep ? &dep : nullptr, dep ? 1 : 0, &np));
+    for (unsigned k = 0; k < size; ++k) bodies[k] = np.conditional.phGraph_out[k];
+    return n;
+  };
+  cudaGraph_t g;
+  CK(cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle h_loop, h_sw, h_ls, h_act, h_ref;
+  CK(cudaGraphConditionalHandleCreate(&h_loop, g, 1, cudaGraphCondAssignDefault));
+  cudaGraph_t body;
+  cond(g, h_loop, cudaGraphCondTypeWhile, 1, nullptr, &body);
+  // handles live on the graph that holds their node; the kernels that set a
+  // handle are captured after it exists (A is copied into their arguments)
+  CK(cudaGraphConditionalHandleCreate(&h_sw, body, 0, cudaGraphCondAssignDefault));
+  CK(cudaGraphConditionalHandleCreate(&h_ref, body, 0, cudaGraphCondAssignDefault));
+  A.h_loop = (unsigned long long)h_loop;
+  A.h_sw = (unsigned long long)h_sw;
+  A.h_ref = (unsigned long long)h_ref;
+  cudaGraph_t gtop = capture([&] {
+    Lt(R + nz, Lsre);
+    XiArgs X{};
+    X.x[0] = R, X.y[0] = Lsre, X.d[0] = d1_, X.n[0] = int(nz);
+    X.x[1] = R + nz, X.y[1] = Lrz, X.d[1] = d2_, X.n[1] = int(ne);
+    X.alpha = alpha;
+    launch_xi(X, partial_ + kMaxDots * kRedBlocks, red_out_ + 4, st_);
+    if (supermann) {
+      loop_push(A, st_);
+      loop_gram(A, partial_ + 2 * kMaxDots * kRedBlocks, red_out_ + 8, st_);
+    }
+    loop_begin(A, st_);
+    if (supermann) loop_psi(A, st_);
+  });
+  cudaGraphNode_t n_top = child(body, gtop, nullptr);
+  cudaGraph_t sw[4];
+  cudaGraphNode_t n_sw = cond(body, h_sw, cudaGraphCondTypeSwitch, 4, n_top, sw);
+  CK(cudaGraphConditionalHandleCreate(&h_ls, sw[2], 0, cudaGraphCondAssignDefault));
+  CK(cudaGraphConditionalHandleCreate(&h_act, sw[2], 0, cudaGraphCondAssignDefault));
+  A.h_ls = (unsigned long long)h_ls;
+  A.h_act = (unsigned long long)h_act;
+  // case 1 (K0): v += psi
+  child(sw[1], capture([&] { launch_axpby(int(nv), 1.0, V, 1.0, PSI, V, st_); }), nullptr);
+  // case 2: M psi, line search, K1 / K2 / KM
+  {
+    cudaGraph_t gm = capture([&] {
+      loop_ls_init(A, st_);
+      Lt(PSI + nz, tmpz);
+      launch_axpby(int(nz), 1.0, PSI, -alpha, tmpz, PV, st_);
+      L(PSI, tmpe);
+      launch_axpby(int(ne), 1.0, PSI + nz, -alpha, tmpe, PV + nz, st_);
+    });
+    cudaGraphNode_t n_m = child(sw[2], gm, nullptr);
+    cudaGraph_t lsb;
+    cudaGraphNode_t n_ls = cond(sw[2], h_ls, cudaGraphCondTypeWhile, 1, n_m, &lsb);
+    child(lsb, capture([&] {
+            loop_axpy_tau(A, st_);
+            refresh(C, TC, CR, cLrz);
+            mnorm(CR, cLrz);
+            DotArgs D{};
+            D.x[0] = CR, D.y[0] = PV, D.n[0] = int(nz);
+            D.x[1] = CR + nz, D.y[1] = PV + nz, D.n[1] = int(ne);
+            D.ndots = 2;
+            launch_dots(D, partial_ + 3 * kMaxDots * kRedBlocks, red_out_ + 3, st_);
+            loop_ls(A, st_);
+          }),
+          nullptr);
+    cudaGraph_t act[4];
+    cond(sw[2], h_act, cudaGraphCondTypeSwitch, 4, n_ls, act);
+    child(act[1], capture([&] {  // K1: the candidate becomes the iterate
+            loop_copy(V, C, nv, st_);
+            loop_copy(TV, TC, nv, st_);
+            loop_copy(R, CR, nv, st_);
+            loop_copy(Lrz, cLrz, ne, st_);
+          }),
+          nullptr);
+    child(act[2], capture([&] { loop_k2(A, st_); }), nullptr);
+    child(act[3], capture([&] { loop_copy(V, TV, nv, st_); }), nullptr);
+  }
+  // case 3 (CP): v <- T v
+  child(sw[3], capture([&] { loop_copy(V, TV, nv, st_); }), nullptr);
+  cudaGraph_t rb;
+  cudaGraphNode_t n_ref = cond(body, h_ref, cudaGraphCondTypeIf, 1, n_sw, &rb);
+  child(rb, capture([&] {
+          refresh(V, TV, R, Lrz);
+          mnorm(R, Lrz);
+        }),
+        nullptr);
+  child(body, capture([&] { loop_end(A, st_); }), n_ref);
+  CK(cudaGraphInstantiate(&G.exec, g, 0));
+  for (cudaGraph_t c : owned) cudaGraphDestroy(c);
+  cudaGraphDestroy(g);
+}
+
+// ---------------------------------------------------------------------------
 // SuperMann / CP loop (proj/src/solver.cpp:189-350).  State lives on device;
 // one host round trip per iteration (omega, xi norms and the Anderson Gram
 // matrix come back together) plus one per line-search trial.
 void Engine::solve_b(const double* x_init, const double* wz, const double* we, double* oz, double* ozs, double* oe,
                      bool supermann, Status& st) {
+  if (solve_graph(x_init, wz, we, oz, ozs, oe, supermann, st)) return;
   const int64_t nz = lay_.nz, ne = lay_.neta, nv = nz + ne;
   set_xinit(x_init ? x_init : raw_.x_init.data());
   const int m = prm_.aa_memory;

@@ -13,6 +13,7 @@
 #include "dev.cuh"
 #include "fused.hpp"
 #include "kernels.hpp"
+#include "loop.hpp"
 #include "model.hpp"
 #include "wide.hpp"
 
@@ -72,6 +73,17 @@ class Engine {
   void unscale_b(const double* zs, double* z);
   void solve_b(const double* x_init, const double* wz, const double* we, double* oz, double* ozs, double* oe,
                bool supermann, Status& st);
+  // device-resident loop (CUDA graph with conditional nodes); false: not applicable
+  // (cancellation callback, Anderson memory above kLoopMaxMem, SPOCK_SOLVE_GRAPH=0)
+  bool solve_graph(const double* x_init, const double* wz, const double* we, double* oz, double* ozs, double* oe,
+                   bool supermann, Status& st);
+  struct GraphLoop {
+    cudaGraphExec_t exec = nullptr;
+    LoopArgs A{};
+    double* Lrz = nullptr;
+  };
+  GraphLoop gloop_[2];  // CP, SuperMann
+  void build_loop_graph(GraphLoop& G, bool supermann);
   double bench_T(int k, bool graph, bool flush);
   void bench_kernels(int k, bool flush, double* ms);
   void traffic(double* bytes) const;
