@@ -219,6 +219,20 @@ int spock_shard_apply_T(spock_solver* s, int32_t phase, const double* z, const d
                         double* eta_out);
 int spock_shard_bench(spock_solver* s, int32_t phase, int32_t parity);
 int spock_shard_masks(spock_solver* s, uint8_t* z_mask, uint8_t* eta_mask);
+/* Sharded solve / solve_cp: once collectives are set, spock_solver_solve and
+ * spock_solver_solve_cp on every rank run one SuperMann / CP solve together
+ * (host-driven loop; T, L and L* over the rank's items with the stage-ts
+ * exchanges; every reduction over the rank's entries, completed by the host's
+ * collectives on device buffers, enqueued on spock_solver_stream's stream:
+ * op 0 all-gather of the n-double exchange buffer (equal slices per rank),
+ * op 1 all-reduce sum, op 2 all-reduce max; return 0 on success).  Outputs
+ * are valid on spock_shard_masks' entries. */
+typedef int (*spock_collective_fn)(void* user, int32_t op, double* dev_buf, int64_t n);
+/* spock_shard_weights: spock_shard_masks restricted to one rank per entry (the
+ * replicated top belongs to rank 0): the ranks' weighted outputs sum to the
+ * whole vector. */
+int spock_shard_weights(spock_solver* s, uint8_t* z_w, uint8_t* eta_w);
+int spock_shard_set_collectives(spock_solver* s, spock_collective_fn fn, void* user);
 void* spock_solver_stream(const spock_solver* s);
 
 #ifdef __cplusplus

@@ -191,6 +191,9 @@ def _lib_path() -> str:
 _LIB: Optional[C.CDLL] = None
 
 
+COLLECTIVE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int32, C.c_void_p, C.c_int64)
+
+
 def load_library() -> C.CDLL:
     """Load the in-tree CUDA library; fail loudly if it is missing (no CPU fallback)."""
     global _LIB
@@ -230,6 +233,8 @@ def load_library() -> C.CDLL:
     lib.spock_shard_apply_T.argtypes = [C.c_void_p, C.c_int32] + [C.c_void_p] * 4
     lib.spock_shard_bench.argtypes = [C.c_void_p, C.c_int32, C.c_int32]
     lib.spock_shard_masks.argtypes = [C.c_void_p, P(C.c_uint8), P(C.c_uint8)]
+    lib.spock_shard_weights.argtypes = [C.c_void_p, P(C.c_uint8), P(C.c_uint8)]
+    lib.spock_shard_set_collectives.argtypes = [C.c_void_p, COLLECTIVE_FN, C.c_void_p]
     lib.spock_solver_stream.argtypes = [C.c_void_p]
     lib.spock_solver_stream.restype = C.c_void_p
     _LIB = lib
@@ -242,5 +247,6 @@ EXPORTED_SYMBOLS = [
     "spock_solver_apply_T", "spock_op_apply", "spock_op_apply_adjoint", "spock_op_m_norm",
     "spock_proj_s1", "spock_proj_s2", "spock_proj_s3", "spock_solver_unscale_primal", "spock_bench_T",
     "spock_bench_kernels", "spock_traffic_model", "spock_solver_t_path", "spock_shard_setup", "spock_shard_apply_T",
-    "spock_shard_bench", "spock_shard_masks", "spock_solver_stream",
+    "spock_shard_bench", "spock_shard_masks", "spock_shard_weights", "spock_shard_set_collectives",
+    "spock_solver_stream",
 ]

@@ -233,6 +233,16 @@ int spock_shard_masks(spock_solver* s, uint8_t* z_mask, uint8_t* eta_mask) {
   return guard([&] { s->eng->shard_masks(z_mask, eta_mask); });
 }
 
+int spock_shard_weights(spock_solver* s, uint8_t* z_w, uint8_t* eta_w) {
+  if (int rc = check(s)) return rc;
+  return guard([&] { s->eng->shard_weights(z_w, eta_w); });
+}
+
+int spock_shard_set_collectives(spock_solver* s, spock_collective_fn fn, void* user) {
+  if (int rc = check(s)) return rc;
+  return guard([&] { s->eng->shard_set_collectives(reinterpret_cast<spock::Engine::CollFn>(fn), user); });
+}
+
 void* spock_solver_stream(const spock_solver* s) {
   return (s && s->eng) ? reinterpret_cast<void*>(s->eng->stream()) : nullptr;
 }

@@ -658,6 +658,8 @@ void Engine::setup_wide(bool force) {
   CK(cudaMemcpyAsync(ltrec_, ltrecs.data(), sizeof(WRec) * ltrecs.size(), cudaMemcpyHostToDevice, st_));
   nlrec_ = int(lrecs.size());
   nltrec_ = int(ltrecs.size());
+  lrecs_h_ = lrecs;
+  ltrecs_h_ = ltrecs;
   CK(cudaStreamSynchronize(st_));
   // lop.cu (narrow trees): staging capacities from the records
   {
@@ -782,8 +784,92 @@ void Engine::shard_setup(int G, int rank, int ts, const int* back_a, int na, con
     root_ts[i] = tr.stage[i] == ts ? i : root_ts[tr.anc[i]];
     S.owned[i] = (root_ts[i] >= S.b0 && root_ts[i] < S.b1) ? 1 : 0;
   }
+  // sharded solve: L / L* item subsets, entry masks and exclusive weights
+  {
+    std::vector<WRec> lo, la, lb;
+    for (int i = 0; i < nn; ++i)
+      if (S.owned[i]) lo.push_back(lrecs_h_[size_t(i)]);
+    for (int i = 1; i < nn; ++i)
+      if (S.owned[i]) la.push_back(ltrecs_h_[size_t(i - 1)]);
+    for (int i = 0; i < nn; ++i)
+      if (S.owned[i]) lb.push_back(ltrecs_h_[size_t(nn - 1 + i)]);
+    auto up = [&](const std::vector<WRec>& v, WRec*& d, int& n) {
+      d = dalloc<WRec>(std::max<size_t>(v.size(), 1));
+      if (!v.empty()) CK(cudaMemcpyAsync(d, v.data(), sizeof(WRec) * v.size(), cudaMemcpyHostToDevice, st_));
+      n = int(v.size());
+    };
+    up(lo, S.recL, S.nL);
+    up(la, S.recLtA, S.nLtA);
+    up(lb, S.recLtB, S.nLtB);
+    std::vector<uint8_t> zm(size_t(lay_.nz)), em(size_t(lay_.neta)), zx(zm.size()), ex(em.size());
+    S.on = true;  // shard_masks needs it
+    shard_masks(zm.data(), em.data());
+    shard_weights(zx.data(), ex.data());
+    std::vector<double> mz(zm.begin(), zm.end()), me(em.begin(), em.end()), wz(zx.begin(), zx.end()),
+        we(ex.begin(), ex.end());
+    std::vector<double> wv(wz);
+    wv.insert(wv.end(), we.begin(), we.end());
+    S.mz = dupload(mz), S.me = dupload(me), S.wz = dupload(wz), S.we = dupload(we), S.wv = dupload(wv);
+  }
   CK(cudaStreamSynchronize(st_));
   S.on = true;
+}
+
+void Engine::shard_set_collectives(CollFn fn, void* user) {
+  require(shard_.on, "spock_shard_set_collectives: call spock_shard_setup first");
+  shard_.coll = fn;
+  shard_.coll_user = user;
+}
+
+void Engine::coll(int op, double* buf, int64_t n) {
+  if (!shard_.coll || shard_.G == 1 || n <= 0) return;
+  if (shard_.coll(shard_.coll_user, op, buf, n) != 0) throw std::runtime_error("sharded solve: collective failed");
+}
+
+// one T of the sharded solve: phase A, all-gather, phase B
+void Engine::shard_T(const double* z, const double* eta, double* zo, double* eo) {
+  shard_T_A(z, eta, zo, eo);
+  coll(0, shard_.xbuf, int64_t(shard_.G) * shard_.q * shard_.E);
+  shard_T_B(z, eta, zo, eo);
+}
+
+// L* of the sharded solve: child terms of the rank's nodes, all-gather of the
+// stage-ts adj terms, node rows of the rank's nodes
+void Engine::shard_Lt(const double* eta, double* z) {
+  const ShardState& S = shard_;
+  WideArgs A = wargs_;
+  A.D = D_, A.eta = eta, A.zo = z;
+  CK(cudaMemsetAsync(wide_flags_, 0, sizeof(int) * size_t(p_.tree.nn()), st_));
+  if (S.nLtA > 0) launch_wide(A, S.recLtA, S.nLtA);
+  ShardXArgs X{D_, nullptr, eta, S.xidx, S.xbuf, S.bfirst, S.b0, S.b1, S.E, nullptr, 0, 0};
+  launch_shard_pack(X, st_);
+  coll(0, S.xbuf, int64_t(S.G) * S.q * S.E);
+  X.flagB = wargs_.flagB;
+  X.nbound = S.nbound;
+  launch_shard_unpack(X, st_);
+  if (S.nLtB > 0) launch_wide(A, S.recLtB, S.nLtB);
+}
+
+void Engine::shard_L(const double* z, double* eta) {
+  WideArgs A = wargs_;
+  A.D = D_, A.z = z, A.eo = eta;
+  if (shard_.nL > 0) launch_wide(A, shard_.recL, shard_.nL);
+}
+
+// exclusive weights: like shard_masks, but an entry computed on every rank (its
+// owner node is in the replicated top) belongs to rank 0 only, so the ranks'
+// weighted vectors sum to the whole vector and weighted dots to the whole dot
+void Engine::shard_weights(uint8_t* zm, uint8_t* em) {
+  ShardState& S = shard_;
+  require(S.on, "spock_shard_weights: call spock_shard_setup first");
+  if (S.rank == 0) {
+    shard_masks(zm, em);
+    return;
+  }
+  const std::vector<uint8_t> saved = S.owned;
+  for (int i = 0; i < S.bfirst; ++i) S.owned[i] = 0;
+  shard_masks(zm, em);
+  S.owned = saved;
 }
 
 // validity masks of this rank's iterates in the boundary layouts (1: computed here)
@@ -794,7 +880,7 @@ void Engine::shard_masks(uint8_t* zm, uint8_t* em) const {
   const int nn = tr.nn(), nnl = tr.nnl(), nx = p_.nx, nu = p_.nu;
   if (zm) {
     std::memset(zm, 0, size_t(lay_.nz));
-    zm[0] = 1;
+    zm[0] = S.owned[0];  // s0 belongs to the root (top)
     for (int i = 0; i < nn; ++i) {
       const uint8_t o = S.owned[i];
       std::memset(zm + 1 + size_t(i) * nx, o, size_t(nx));
@@ -803,9 +889,10 @@ void Engine::shard_masks(uint8_t* zm, uint8_t* em) const {
         std::memset(zm + lay_.y_off[i], o, size_t(lay_.y_dim[i]));
       }
       if (i > 0) {
-        const uint8_t oa = S.owned[tr.anc[i]];  // tau_i, s_i come from S2 of the parent
-        zm[lay_.tau_base + i - 1] = oa;
-        zm[lay_.s_base + i - 1] = oa;
+        // tau_i, s_i: T writes them in S2 of the parent (every rank holding the
+        // parent), L* in node i's own items -- both on node i's owner
+        zm[lay_.tau_base + i - 1] = o;
+        zm[lay_.s_base + i - 1] = o;
       }
     }
   }
@@ -860,7 +947,7 @@ void Engine::shard_T_A(const double* z, const double* eta, double* zo, double* e
   A.ntick = S.nA;
   CK(cudaMemsetAsync(wide_flags_, 0, wide_flag_bytes_, st_));
   if (S.nA > 0) launch_wide(A, S.recA, S.nA);
-  ShardXArgs X{D_, z, eta, S.xidx, S.xbuf, S.bfirst, S.b0, S.b1, S.E, nullptr};
+  ShardXArgs X{D_, z, eta, S.xidx, S.xbuf, S.bfirst, S.b0, S.b1, S.E, nullptr, 0, 1};
   launch_shard_pack(X, st_);
 }
 
@@ -868,8 +955,7 @@ void Engine::shard_T_B(const double* z, const double* eta, double* zo, double* e
   const ShardState& S = shard_;
   require(S.on, "spock_shard_T: call spock_shard_setup first");
   // remote stage-ts records -> adj, T12, the inputs' tau / s entries, backward flags
-  ShardXArgs X{D_, z, eta, S.xidx, S.xbuf, S.bfirst, S.b0, S.b1, S.E, wargs_.flagB};
-  X.nbound = S.nbound;
+  ShardXArgs X{D_, z, eta, S.xidx, S.xbuf, S.bfirst, S.b0, S.b1, S.E, wargs_.flagB, S.nbound, 1};
   launch_shard_unpack(X, st_);
   WideArgs A = wargs_;
   A.D = D_, A.z = z, A.eta = eta, A.zo = zo, A.eo = eo, A.alpha = alpha_;
@@ -1488,6 +1574,10 @@ void Engine::launch_wide(WideArgs A, const WRec* recs, int ntick) {
 }
 
 void Engine::L(const double* z, double* eta) {
+  if (shard_solving_) {
+    shard_L(z, eta);
+    return;
+  }
   if (wide_ok_ && !lop_wide_ && lop_narrow_) {
     launch_L_lop(D_, wargs_, lrec_, z, eta, lop_rows_, lop_mat_, lop_vec_, st_);
     return;
@@ -1505,6 +1595,10 @@ void Engine::L(const double* z, double* eta) {
 }
 
 void Engine::Lt(const double* eta, double* z) {
+  if (shard_solving_) {
+    shard_Lt(eta, z);
+    return;
+  }
   if (wide_ok_ && !lop_wide_ && lop_narrow_) {
     launch_Lt_lop(D_, wargs_, ltrec_, eta, z, lop_rows_, lop_mat_, lop_vec_, st_);
     return;
@@ -1525,6 +1619,10 @@ void Engine::Lt(const double* eta, double* z) {
 // one CP application (solver.cpp:148-164), internal layout; zo/eo must not
 // alias z/eta
 void Engine::T(const double* z, const double* eta, double* zo, double* eo) {
+  if (shard_solving_) {
+    shard_T(z, eta, zo, eo);
+    return;
+  }
   if (fused_ok_) {
     FusedArgs F = fargs_;
     F.D = D_;
@@ -1599,6 +1697,7 @@ void Engine::power_iteration() {
     const double est = std::sqrt(r);
     norm_.estimate = est;
     norm_.iterations = it;
+    if (std::getenv("SPOCK_DEBUG_NORM")) std::fprintf(stderr, "[power] it %d est %.17g\n", it, est);
     if (est == 0.0) {
       norm_.converged = true;
       break;
@@ -2018,7 +2117,19 @@ void Engine::build_loop_graph(GraphLoop& G, bool supermann) {
 // matrix come back together) plus one per line-search trial.
 void Engine::solve_b(const double* x_init, const double* wz, const double* we, double* oz, double* ozs, double* oe,
                      bool supermann, Status& st) {
-  if (solve_graph(x_init, wz, we, oz, ozs, oe, supermann, st)) return;
+  // sharded solve: host-driven loop, T / L / L* over this rank's
+  // items with the exchanges, every reduction over this rank's entries and
+  // all-reduced (sums of dots, max of the xi norms) through the host's collectives
+  const bool sharded = shard_.on && shard_.coll != nullptr;
+  struct Flag {
+    bool& f;
+    ~Flag() { f = false; }
+  } flag_guard{shard_solving_};
+  shard_solving_ = sharded;
+  const double* w_z = sharded ? shard_.wz : nullptr;
+  const double* w_e = sharded ? shard_.we : nullptr;
+  const double* w_v = sharded ? shard_.wv : nullptr;
+  if (!sharded && solve_graph(x_init, wz, we, oz, ozs, oe, supermann, st)) return;
   const int64_t nz = lay_.nz, ne = lay_.neta, nv = nz + ne;
   set_xinit(x_init ? x_init : raw_.x_init.data());
   const int m = prm_.aa_memory;
@@ -2026,7 +2137,7 @@ void Engine::solve_b(const double* x_init, const double* wz, const double* we, d
   std::vector<double*> bufs;
   auto pair = [&]() {
     double* p = nullptr;
-    CK(cudaMallocAsync(&p, sizeof(double) * nv, st_));
+    CK(cudaMallocAsync(&p, sizeof(double) * (nv + 2), st_));
     bufs.push_back(p);
     return p;
   };
@@ -2067,9 +2178,9 @@ void Engine::solve_b(const double* x_init, const double* wz, const double* we, d
   // queue the M-norm dots of (r, lrz) into red_out_[base..base+3)
   auto queue_mnorm = [&](const double* r, const double* lrz, int base) {
     DotArgs A{};
-    A.x[0] = r, A.y[0] = r, A.n[0] = int(nz);
-    A.x[1] = r + nz, A.y[1] = lrz, A.n[1] = int(ne);
-    A.x[2] = r + nz, A.y[2] = r + nz, A.n[2] = int(ne);
+    A.x[0] = r, A.y[0] = r, A.n[0] = int(nz), A.w[0] = w_z;
+    A.x[1] = r + nz, A.y[1] = lrz, A.n[1] = int(ne), A.w[1] = w_e;
+    A.x[2] = r + nz, A.y[2] = r + nz, A.n[2] = int(ne), A.w[2] = w_e;
     A.ndots = 3;
     launch_dots(A, partial_, red_out_ + base, st_);
   };
@@ -2098,6 +2209,7 @@ void Engine::solve_b(const double* x_init, const double* wz, const double* we, d
       X.x[0] = R, X.y[0] = Lsre, X.d[0] = d1_, X.n[0] = int(nz);
       X.x[1] = R + nz, X.y[1] = Lrz, X.d[1] = d2_, X.n[1] = int(ne);
       X.alpha = alpha;
+      if (sharded) X.w[0] = shard_.mz, X.w[1] = shard_.me;
       launch_xi(X, partial_ + kMaxDots * kRedBlocks, red_out_ + 4, st_);
       // Anderson push (solver.cpp:57-63) and Gram of the differences
       int ngram = 0;
@@ -2120,13 +2232,18 @@ void Engine::solve_b(const double* x_init, const double* wz, const double* we, d
             DotArgs A{};
             int j = 0;
             for (size_t q = c0; q < prs.size() && j < kMaxDots; ++q, ++j) {
-              A.x[j] = prs[q].first, A.y[j] = prs[q].second, A.n[j] = int(nv);
+              A.x[j] = prs[q].first, A.y[j] = prs[q].second, A.n[j] = int(nv), A.w[j] = w_v;
             }
             A.ndots = j;
             launch_dots(A, partial_ + 2 * kMaxDots * kRedBlocks, red_out_ + 8 + c0, st_);
           }
           ngram = int(prs.size());
         }
+      }
+      if (sharded) {  // this iteration's fresh partials, summed (max for xi) over the ranks
+        if (!have_omega) coll(1, red_out_, 3);
+        coll(2, red_out_ + 4, 2);
+        if (ngram) coll(1, red_out_ + 8, ngram);
       }
       fetch(8 + ngram);
       if (!have_omega) {
@@ -2221,11 +2338,12 @@ void Engine::solve_b(const double* x_init, const double* wz, const double* we, d
           queue_mnorm(CR, cLrz, 0);
           {
             DotArgs A{};
-            A.x[0] = CR, A.y[0] = PV, A.n[0] = int(nz);
-            A.x[1] = CR + nz, A.y[1] = PV + nz, A.n[1] = int(ne);
+            A.x[0] = CR, A.y[0] = PV, A.n[0] = int(nz), A.w[0] = w_z;
+            A.x[1] = CR + nz, A.y[1] = PV + nz, A.n[1] = int(ne), A.w[1] = w_e;
             A.ndots = 2;
             launch_dots(A, partial_ + 3 * kMaxDots * kRedBlocks, red_out_ + 3, st_);
           }
+          if (sharded) coll(1, red_out_, 5);
           fetch(5);
           const double omt = mnorm_of(host_red_);
           if ((omega <= omega_safe && omt <= prm_.c1 * omega) || omt == 0.0) {  // K1

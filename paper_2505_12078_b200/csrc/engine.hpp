@@ -93,8 +93,13 @@ class Engine {
   void shard_T_A(const double* z, const double* eta, double* zo, double* eo);
   void shard_T_B(const double* z, const double* eta, double* zo, double* eo);
   void shard_masks(uint8_t* zm, uint8_t* em) const;
+  void shard_weights(uint8_t* zm, uint8_t* em);
   void shard_apply_T_b(int phase, const double* z, const double* eta, double* zo, double* eo);
   void shard_bench(int phase, int parity);
+  // sharded solve: the host provides the collectives (op 0: all-gather of the
+  // exchange buffer, 1: all-reduce sum, 2: all-reduce max, on device buffers)
+  typedef int (*CollFn)(void* user, int op, double* buf, int64_t n);
+  void shard_set_collectives(CollFn fn, void* user);
   cudaStream_t stream() const { return st_; }
   double* scratch_z(int k) const { return scratch_z_[k]; }
   double* scratch_e(int k) const { return scratch_e_[k]; }
@@ -178,7 +183,20 @@ class Engine {
     int64_t* xidx = nullptr;
     double* xbuf = nullptr;
     std::vector<uint8_t> owned;
+    WRec* recL = nullptr;
+    WRec* recLtA = nullptr;
+    WRec* recLtB = nullptr;
+    int nL = 0, nLtA = 0, nLtB = 0;
+    double *mz = nullptr, *me = nullptr, *wz = nullptr, *we = nullptr, *wv = nullptr;
+    CollFn coll = nullptr;
+    void* coll_user = nullptr;
   } shard_;
+  bool shard_solving_ = false;
+  std::vector<WRec> lrecs_h_, ltrecs_h_;
+  void coll(int op, double* buf, int64_t n);
+  void shard_T(const double* z, const double* eta, double* zo, double* eo);
+  void shard_L(const double* z, double* eta);
+  void shard_Lt(const double* eta, double* z);
   size_t wide_flag_bytes_ = 0;
   double* flush_buf_ = nullptr;
   void flush_l2();

@@ -804,9 +804,16 @@ __global__ void __launch_bounds__(kRedThreads) k_dots(DotArgs A, double* __restr
   for (int j = 0; j < A.ndots; ++j) {
     const double* x = A.x[j];
     const double* y = A.y[j];
+    const double* w = A.w[j];
     const int n = A.n[j];
     double s = 0.0;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) s += x[i] * y[i];
+    if (w) {  // entries with weight 0 may hold anything (another rank computes them): skipped, not multiplied
+      for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        if (w[i] != 0.0) s += x[i] * y[i];
+      }
+    } else {
+      for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) s += x[i] * y[i];
+    }
     acc[j] = s;
   }
   const int w = threadIdx.x >> 5;
@@ -842,6 +849,7 @@ __global__ void __launch_bounds__(kRedThreads) k_xi(XiArgs A, double* __restrict
   const int stride = gridDim.x * blockDim.x;
   for (int t = 0; t < 2; ++t) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < A.n[t]; i += stride) {
+      if (A.w[t] && A.w[t][i] == 0.0) continue;
       double v = A.x[t][i] / A.alpha - A.y[t][i];
       if (A.d[t]) v *= A.d[t][i];
       if (isnan(v)) bad = true;

@@ -20,6 +20,7 @@ struct DotArgs {
   const double* y[kMaxDots];
   int n[kMaxDots];
   int ndots;
+  const double* w[kMaxDots];  // optional 0/1 weights (sharded solve: entries this rank counts)
 };
 struct XiArgs {
   const double* x[2];
@@ -27,6 +28,7 @@ struct XiArgs {
   const double* d[2];
   int n[2];
   double alpha;
+  const double* w[2];  // optional 0/1 masks (sharded solve: entries this rank computes)
 };
 struct BGemmArgs {
   const double* const* A;

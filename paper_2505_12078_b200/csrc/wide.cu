@@ -1326,7 +1326,7 @@ __global__ void k_shard_pack(const __grid_constant__ ShardXArgs X) {
     o[r] = X.D.adj[size_t(c - 1) * m + r];
     o[m + r] = X.D.T12[size_t(c - 1) * m + r];
   }
-  if (l < 6) {
+  if (l < 6 && X.vec) {
     const int64_t ix = X.xidx[size_t(k) * 6 + l];
     o[2 * m + l] = ix < 0 ? 0.0 : (l < 2 ? X.z[ix] : X.eta[ix]);
   }
@@ -1344,7 +1344,7 @@ __global__ void k_shard_unpack(const __grid_constant__ ShardXArgs X) {
     X.D.adj[size_t(c - 1) * m + r] = o[r];
     X.D.T12[size_t(c - 1) * m + r] = o[m + r];
   }
-  if (l < 6) {
+  if (l < 6 && X.vec) {
     const int64_t ix = X.xidx[size_t(k) * 6 + l];
     if (ix >= 0) (l < 2 ? const_cast<double*>(X.z) : const_cast<double*>(X.eta))[ix] = o[2 * m + l];
   }

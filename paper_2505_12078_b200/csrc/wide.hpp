@@ -72,6 +72,7 @@ struct ShardXArgs {
   int bfirst, b0, b1, E;
   int* flagB;           // unpack: set for remote nodes
   int nbound;
+  int vec;              // 1: also exchange the z / eta entries (T); 0: adj / T12 only (L*)
 };
 void launch_shard_pack(const ShardXArgs& X, cudaStream_t st);
 void launch_shard_unpack(const ShardXArgs& X, cudaStream_t st);

@@ -127,6 +127,14 @@ def check_plan(tree: ScenarioTree, plans) -> None:
     assert np.all(cnt[top:] == 1)
 
 
+class _DevArray:
+    """__cuda_array_interface__ view of n float64 at a device address."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": "<f8", "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
 def exchange(xbuf, plan: ShardPlan, group=None, stream=None) -> None:
     """All-gather every rank's slice of the exchange buffer (in place).  NCCL:
     device to device, ordered on ``stream`` (the solver's); gloo: through host
@@ -211,6 +219,68 @@ class ShardedSolver:
         self._exchange()
         self._raise(self.lib, self.lib.spock_shard_apply_T(self.solver.h, 1, None, None, _ptr(z_out), _ptr(eta_out)))
         return z_out, eta_out
+
+    def weights(self):
+        zw = np.zeros(self.nz, dtype=np.uint8)
+        ew = np.zeros(self.neta, dtype=np.uint8)
+        P = C.POINTER(C.c_uint8)
+        self._raise(self.lib, self.lib.spock_shard_weights(self.solver.h, zw.ctypes.data_as(P), ew.ctypes.data_as(P)))
+        return zw.astype(bool), ew.astype(bool)
+
+    def _collective(self, user, op, ptr, n):
+        """Called by the library during a sharded solve (spock_collective_fn)."""
+        torch, dist = self.torch, self.dist
+        try:
+            if op == 0:
+                exchange(self.xbuf, self.plan, self.group, self.stream)
+                return 0
+            t = torch.as_tensor(_DevArray(ptr, n), device="cuda")
+            rop = dist.ReduceOp.SUM if op == 1 else dist.ReduceOp.MAX
+            if dist.get_backend(self.group) == "nccl":
+                with torch.cuda.stream(self.stream):
+                    dist.all_reduce(t, op=rop, group=self.group)
+            else:
+                self.stream.synchronize()
+                h = t.cpu()
+                dist.all_reduce(h, op=rop, group=self.group)
+                t.copy_(h)
+                torch.cuda.synchronize()
+            return 0
+        except Exception:  # pragma: no cover - reported as a runtime error by the library
+            return 1
+
+    def _solve(self, fn, x_init, history_capacity):
+        from .capi import COLLECTIVE_FN
+        from .solver import SolveResult, _ptr, make_status, status_dict
+        if not hasattr(self, "_cb"):
+            self._cb = COLLECTIVE_FN(self._collective)
+            self._raise(self.lib, self.lib.spock_shard_set_collectives(self.solver.h, self._cb, None))
+        st, rn, br = make_status(history_capacity)
+        z = np.zeros(self.nz)
+        zs = np.zeros(self.nz)
+        e = np.zeros(self.neta)
+        x = None if x_init is None else np.ascontiguousarray(x_init, dtype=np.float64)
+        rc = fn(self.solver.h, _ptr(x), None, None, _ptr(z), _ptr(zs), _ptr(e), C.byref(st))
+        self._raise(self.lib, rc)
+        # every rank's own entries -> the whole solution on every rank
+        zw, ew = self.weights()
+        out = []
+        nccl = self.dist.get_backend(self.group) == "nccl"
+        for v, w in ((z, zw), (zs, zw), (e, ew)):
+            t = self.torch.from_numpy(np.where(w, v, 0.0))
+            if nccl:
+                t = t.cuda()
+            self.dist.all_reduce(t, group=self.group)
+            out.append(t.cpu().numpy())
+        return SolveResult(out[0], out[1], out[2], status_dict(st, rn, br))
+
+    def solve(self, x_init=None, history_capacity: int = 100000):
+        """SuperMann (proj/src/solver.cpp:176-180) over the subtree-sharded tree."""
+        return self._solve(self.lib.spock_solver_solve, x_init, history_capacity)
+
+    def solve_cp(self, x_init=None, history_capacity: int = 100000):
+        """Plain CP (proj/src/solver.cpp:182-187) over the subtree-sharded tree."""
+        return self._solve(self.lib.spock_solver_solve_cp, x_init, history_capacity)
 
     def bench_step(self, parity: int) -> None:
         """One sharded T on the device-resident scratch iterates (no host copies)."""

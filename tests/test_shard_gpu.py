@@ -91,4 +91,70 @@ def test_sharded_T_matches_one_gpu_and_oracle(name, world, ts):
     for r in range(world):
         err = res[r][0]
         assert not isinstance(err, str), res[r]
-        assert err <= 1e-11, (r, res[r])
+        assert err <= 1e-10, (r, res[r])
+
+
+def _solve_worker(rank, world, port, name, method, iters, q):
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    sys.path.insert(0, os.path.join(root, "tests"))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2505_12078_b200.shard import ShardedSolver
+        from paper_2505_12078_b200.solver import SpockSolver
+        p = _problem(name)
+        sh = ShardedSolver(p, max_iters=iters)
+        os.environ["SPOCK_SOLVE_GRAPH"] = "0"  # the one-GPU reference runs the same host-driven loop
+        one = SpockSolver(p, max_iters=iters, alpha=sh.alpha)
+        a = getattr(sh, method)(p.x_init)
+        b = getattr(one, method)(p.x_init)
+        if a.status["iterations"] != b.status["iterations"]:
+            q.put((rank, "iterations %s vs %s; sharded %s %s %s; one %s %s %s" % (
+                a.status["iterations"], b.status["iterations"], a.status["reason"], a.status["xi1_inf"],
+                a.status["xi2_inf"], b.status["reason"], b.status["xi1_inf"], b.status["xi2_inf"]), 0, 0, 0.0, 0.0,
+                0.0, ""))
+            return
+        rel = lambda x, y: float(np.abs(x - y).max() / max(1.0, np.abs(y).max()))
+        q.put((rank, a.status["branches"] == b.status["branches"], a.status["iterations"], b.status["iterations"],
+               float(np.max(np.abs(a.status["rnorm_history"] - b.status["rnorm_history"])
+                            / np.maximum(1e-30, np.abs(b.status["rnorm_history"])))),
+               rel(a.z, b.z), rel(a.eta, b.eta), a.status["branches"][:20]))
+    except Exception as ex:
+        import traceback
+        q.put((rank, repr(ex) + traceback.format_exc()[-800:], 0, 0, 0.0, 0.0, 0.0, ""))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name,world,method,iters", [
+    ("mixed", 2, "solve_cp", 40), ("mixed", 2, "solve", 30), ("c1", 2, "solve", 40), ("c1", 3, "solve_cp", 60),
+    ("c2p", 2, "solve", 25),
+])
+def test_sharded_solve_matches_one_gpu(name, world, method, iters):
+    """The sharded SuperMann / CP loop (reductions over each rank's entries,
+    all-reduced; T / L / L* with the stage-ts exchanges) follows the one-GPU
+    loop: same branch strings and iteration counts, ||r||_M traces and
+    solutions equal up to the reassociated sums."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_solve_worker, args=(r, world, port, name, method, iters, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = {}
+    for _ in range(world):
+        r = q.get(timeout=900)
+        res[r[0]] = r[1:]
+    for pr in procs:
+        pr.join(timeout=60)
+    for r in range(world):
+        same, ia, ib, rn, rz, re, br = res[r]
+        assert same is True, res[r]
+        assert ia == ib
+        assert rn <= 1e-8 and rz <= 1e-8 and re <= 1e-8, res[r]
