@@ -699,6 +699,37 @@ void Engine::setup_wide(bool force) {
   if (knob("SPOCK_WIDE_PROF", 0)) A.prof = dalloc<unsigned long long>(16);
   wide_ok_ = true;
   t_wide_ = t_wide;
+  // Split T for trees with a narrow top: stages whose nodes are fewer than the
+  // latency configuration's warps run in their own launch with 16-slot rings
+  // (a whole item prefetched at once); the wide stages stay on the throughput
+  // configuration.  L1: backward of the wide stages + every S2; L2: the top's
+  // backward then forward; L3: forward of the wide stages.
+  const int split_min = knob("SPOCK_T_SPLIT_NODES", wide_grid_lat_ * wlat_.warps);
+  t_split_ = 0;
+  if (t_wide_ && split_min > 0 && knob("SPOCK_T_SPLIT", 0)) {  // measured slower: c3 1.50 vs 1.40 ms
+    int s = 0;
+    while (s <= tr.horizon && tr.stage_start[s + 1] - tr.stage_start[s] < split_min) ++s;
+    if (s >= 2 && s <= tr.horizon) {
+      const int top = tr.stage_start[s];
+      std::vector<WRec> l1, l2, l3;
+      for (int k = 0; k < nn; ++k) {  // backward, node nn-1 .. 0
+        const int i = nn - 1 - k;
+        (i >= top ? l1 : l2).push_back(wrecs_[size_t(k)]);
+      }
+      for (int i = 0; i < nnl; ++i) l1.push_back(wrecs_[size_t(nn) + i]);
+      for (int c = 0; c < nn; ++c) (c >= top ? l3 : l2).push_back(wrecs_[size_t(nn) + nnl + c]);
+      auto up = [&](const std::vector<WRec>& v, WRec*& d, int& n) {
+        d = dalloc<WRec>(v.size());
+        CK(cudaMemcpyAsync(d, v.data(), sizeof(WRec) * v.size(), cudaMemcpyHostToDevice, st_));
+        n = int(v.size());
+      };
+      up(l1, tsplit_rec_[0], tsplit_n_[0]);
+      up(l2, tsplit_rec_[1], tsplit_n_[1]);
+      up(l3, tsplit_rec_[2], tsplit_n_[2]);
+      CK(cudaStreamSynchronize(st_));
+      t_split_ = s;
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1645,9 +1676,13 @@ void Engine::T(const double* z, const double* eta, double* zo, double* eo) {
     A.zo = zo;
     A.eo = eo;
     A.alpha = alpha_;
+    CK(cudaMemsetAsync(wide_flags_, 0, wide_flag_bytes_, st_));
+    if (t_split_) {
+      for (int k = 0; k < 3; ++k) launch_wide(A, tsplit_rec_[k], tsplit_n_[k]);
+      return;
+    }
     A.recs = wargs_.recs;
     A.ntick = wargs_.ntick;
-    CK(cudaMemsetAsync(wide_flags_, 0, wide_flag_bytes_, st_));
     launch_T_wide(A, wide_rows_, wide_ctas_, wide_grid_, st_);
     return;
   }

@@ -103,7 +103,9 @@ class Engine {
   cudaStream_t stream() const { return st_; }
   double* scratch_z(int k) const { return scratch_z_[k]; }
   double* scratch_e(int k) const { return scratch_e_[k]; }
-  int launches_per_T() const { return (fused_ok_ || t_wide_) ? 1 : 2 + 2 * (p_.tree.horizon + 1) + 1 + 1; }
+  int launches_per_T() const {
+    return fused_ok_ ? 1 : (t_wide_ ? (t_split_ ? 3 : 1) : 2 + 2 * (p_.tree.horizon + 1) + 1 + 1);
+  }
   // SPOCK_WIDE_PROF=1: cycle counters of the wide kernel (summed over warps and launches)
   void wide_profile(unsigned long long* out10);
   const char* t_path() const { return fused_ok_ ? "fused" : (t_wide_ ? "wide" : "stages"); }
@@ -161,6 +163,9 @@ class Engine {
   size_t fused_sync_bytes_ = 0;
   bool wide_ok_ = false;  // streaming kernel set up (records, smem, grid)
   bool t_wide_ = false;   // T runs on it
+  int t_split_ = 0;       // > 0: T in three launches, the stages below t_split_ on the latency configuration
+  WRec* tsplit_rec_[3] = {};
+  int tsplit_n_[3] = {};
   bool lop_wide_ = true;  // standalone L / L* run on it
   bool lop_narrow_ = true;  // else lop.cu (CTA per node, one-shot staging)
   int lop_rows_ = 0, lop_mat_ = 0, lop_vec_ = 0;
