@@ -8,6 +8,7 @@
 //   Engine::solve_b      <- SpockSolver::run           proj/src/solver.cpp:189-350
 #include "engine.hpp"
 
+#include <chrono>
 #include <climits>
 #include <cstdint>
 #include <cstdio>
@@ -73,11 +74,24 @@ Ty* Engine::dupload(const std::vector<Ty>& h) {
 }
 
 Engine::Engine(const spock_problem_desc* desc, const Params& prm) : prm_(prm) {
+  // SPOCK_DEBUG_SETUP=1: wall time of each setup phase on stderr
+  const bool dbg = std::getenv("SPOCK_DEBUG_SETUP") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!dbg) return;
+    const auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[setup] %-22s %8.1f ms\n", what,
+                 std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  };
   prm_.validate();
   raw_ = problem_from_desc(desc);
   p_ = raw_;
+  mark("problem_from_desc");
   pc_ = prm_.use_preconditioner ? precondition_inplace(p_) : identity_precond(p_);
+  mark("precondition");
   soc_ = soc_epigraph_data(p_);
+  mark("soc_epigraph_data");
   lay_ = make_layouts(p_, soc_);
   require(p_.nx + p_.nu <= kMaxD, "spock-b200: nx + nu above 256 is not supported");
   stage_start_ = p_.tree.stage_start;
@@ -86,16 +100,25 @@ Engine::Engine(const spock_problem_desc* desc, const Params& prm) : prm_(prm) {
   CK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
   set_carveout_all();
   set_carveout_narrow();
+  mark("layouts + stream");
   upload();
+  CK(cudaStreamSynchronize(st_));
+  mark("upload");
   narrow_ = p_.tree.nn() < 4096;
   if (const char* nv = std::getenv("SPOCK_NARROW")) narrow_ = nv[0] == '1';
   factorize();
+  CK(cudaStreamSynchronize(st_));
+  mark("factorize (Alg. 1)");
   norm_.analytic_bound = analytic_norm_bound(p_, soc_);
+  mark("analytic bound");
   setup_fused();
   setup_wide(false);
+  CK(cudaStreamSynchronize(st_));
+  mark("fused / wide records");
   power_iteration();
   alpha_ = prm_.alpha > 0.0 ? prm_.alpha : 0.99 / std::max(norm_.estimate, 1e-300);
   CK(cudaStreamSynchronize(st_));
+  mark("power iteration");
 }
 
 // Persistent dataflow T (fused.cu): flags, ticket, shared-memory staging size
@@ -403,6 +426,7 @@ void Engine::setup_wide(bool force) {
   }
   A.chunk = std::max(512, knob("SPOCK_WIDE_CHUNK", 512)) & ~1;
   A.ycap = std::min(max_ny, 256);
+  A.l2_prefetch = knob("SPOCK_WIDE_L2PF", 0);  // measured slower (c3 1.80 vs 1.40 ms)
   A.vecd = int((std::max({m, max_nc, max_dense_s2_, 2 * nu + 2 + A.ycap}) + 2 + 7) & ~7);
   wide_ctas_ = knob("SPOCK_WIDE_CTAS", 2) >= 2 ? 2 : 1;
   wide_rows_ = wide_rows(D_, max_nc);

@@ -83,6 +83,10 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// bulk prefetch of [src, src + bytes) into L2 (no shared memory involved)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -1262,7 +1266,22 @@ __global__ void __launch_bounds__(256, MINB) k_T_wide(const __grid_constant__ Wi
   const long long t_start = R.prof ? clock64() : 0;
   for (int j = 0; R.gw + j * R.stride < R.total; ++j) {
     R.jc = j;
-    if (l == 0) request(j + 3);
+    if (l == 0) {
+      request(j + 3);
+      // L2 prefetch of the next ticket's matrices: the smem ring only runs S
+      // chunks ahead, L2 holds the rest of the next item so its chunks arrive at
+      // L2 rather than HBM latency (record j+1 was requested two items ago)
+      if (A.l2_prefetch && R.gw + (j + 1) * R.stride < R.total) {
+        const int s1 = (j + 1) & (kRecSlots - 1);
+        if (mbar_try_wait(&rbar[s1], uint32_t((j + 1) / kRecSlots) & 1u)) {
+          const WRec& rn = rb[s1];
+          for (int k = 0; k < rn.nmat; ++k) {
+            const uint32_t bytes = (uint32_t(rn.mrows[k]) * uint32_t(rn.mcols[k]) * 8u + 15u) & ~15u;
+            if (bytes) bulk_prefetch_l2(rn.mp[k], bytes);
+          }
+        }
+      }
+    }
     refill_lane0(R);
     const int s = j & (kRecSlots - 1);
     const uint32_t par = uint32_t(j / kRecSlots) & 1u;

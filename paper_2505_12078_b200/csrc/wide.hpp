@@ -55,6 +55,7 @@ struct WideArgs {
   int vecd;     // doubles per per-warp vector buffer (three per warp)
   int vrec;     // doubles of staged vector operands per warp
   int ycap;     // y-block values staged per forward item (larger blocks read from L2)
+  int l2_prefetch;  // 1: bulk-prefetch the next ticket's matrices into L2
   const WRec* recs;           // ticket list ([nn + nnl + nn] for a whole T)
   int ntick;                  // number of tickets
   const double* vb[WB_COUNT];  // span bases (WB_Z, WB_ETA unused: taken from z, eta)
