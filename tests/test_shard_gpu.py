@@ -73,7 +73,7 @@ def _worker(rank, world, port, name, ts, q):
 
 @pytest.mark.parametrize("name,world,ts", [
     ("mixed", 2, None), ("mixed", 3, 1), ("expectation", 2, 2), ("c1", 2, None), ("c1", 4, 3), ("c2p", 2, None),
-    ("c2p", 4, None),
+    ("c2p", 4, None), ("c3", 2, None), ("c3", 3, 2),
 ])
 def test_sharded_T_matches_one_gpu_and_oracle(name, world, ts):
     ctx = mp.get_context("spawn")
