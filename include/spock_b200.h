@@ -200,6 +200,18 @@ int spock_bench_kernels(spock_solver* s, int32_t k, int32_t flush_l2, double* ms
 int spock_traffic_model(spock_solver* s, double* bytes5, int32_t* launches_per_T);
 const char* spock_solver_t_path(const spock_solver* s);
 
+/* Concurrent solves (batched multi-x_init; no reference
+ * counterpart -- the reference solves one x_init at a time, solver.hpp:104-105).
+ * Narrow trees are latency-bound, so several solvers, each on its own stream
+ * (spock_solver_stream), solve side by side when each T launch is capped to a
+ * share of the SMs.  spock_solver_set_grid_cap caps the CTAs of the fused T
+ * launch (0 = the full-device default); it must precede the first solve or
+ * bench of the solver (SPOCK_EINVAL otherwise) and is a no-op on the wide and
+ * per-stage schedules.  spock_solver_grid returns the current fused T grid
+ * (0 when T does not run on the fused kernel). */
+int spock_solver_set_grid_cap(spock_solver* s, int32_t ctas);
+int32_t spock_solver_grid(const spock_solver* s);
+
 /* Subtree sharding of T over G ranks (no reference counterpart: the reference
  * runs one process).  The host picks a split stage ts; the rank
  * owns the stage-ts nodes [b0, b1) = [bfirst + rank*q, bfirst + (rank+1)*q)

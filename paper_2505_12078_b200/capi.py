@@ -237,6 +237,9 @@ def load_library() -> C.CDLL:
     lib.spock_shard_set_collectives.argtypes = [C.c_void_p, COLLECTIVE_FN, C.c_void_p]
     lib.spock_solver_stream.argtypes = [C.c_void_p]
     lib.spock_solver_stream.restype = C.c_void_p
+    lib.spock_solver_set_grid_cap.argtypes = [C.c_void_p, C.c_int32]
+    lib.spock_solver_grid.argtypes = [C.c_void_p]
+    lib.spock_solver_grid.restype = C.c_int32
     _LIB = lib
     return lib
 
@@ -248,5 +251,5 @@ EXPORTED_SYMBOLS = [
     "spock_proj_s1", "spock_proj_s2", "spock_proj_s3", "spock_solver_unscale_primal", "spock_bench_T",
     "spock_bench_kernels", "spock_traffic_model", "spock_solver_t_path", "spock_shard_setup", "spock_shard_apply_T",
     "spock_shard_bench", "spock_shard_masks", "spock_shard_weights", "spock_shard_set_collectives",
-    "spock_solver_stream",
+    "spock_solver_stream", "spock_solver_set_grid_cap", "spock_solver_grid",
 ]

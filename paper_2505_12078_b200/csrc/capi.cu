@@ -249,4 +249,11 @@ void* spock_solver_stream(const spock_solver* s) {
 
 const char* spock_solver_t_path(const spock_solver* s) { return (s && s->eng) ? s->eng->t_path() : ""; }
 
+int spock_solver_set_grid_cap(spock_solver* s, int32_t ctas) {
+  if (int rc = check(s)) return rc;
+  return guard([&] { s->eng->set_grid_cap(ctas); });
+}
+
+int32_t spock_solver_grid(const spock_solver* s) { return (s && s->eng) ? s->eng->fused_grid() : 0; }
+
 }  // extern "C"

@@ -222,6 +222,8 @@ void Engine::setup_fused() {
   fused_grid_ = std::max(1, std::min(occ, occ_cap)) * sms;
   const int total = nnl + 2 * nn;
   fused_grid_ = std::min(fused_grid_, total);
+  fused_grid_full_ = fused_grid_;
+  if (const int cap = knob("SPOCK_FUSED_GRID", 0); cap > 0) fused_grid_ = std::min(fused_grid_, cap);
   const size_t fb = 8 + sizeof(int) * size_t(nnl + 2 * nn);
   fused_sync_bytes_ = fb;
   char* buf = dalloc<char>(fb);
@@ -1024,6 +1026,14 @@ void Engine::wide_profile(unsigned long long* out) {
   if (!wargs_.prof) return;
   CK(cudaStreamSynchronize(st_));
   CK(cudaMemcpy(out, wargs_.prof, sizeof(unsigned long long) * 13, cudaMemcpyDeviceToHost));
+}
+
+void Engine::set_grid_cap(int ctas) {
+  if (ctas < 0) throw std::invalid_argument("set_grid_cap: negative CTA count");
+  if (gloop_[0].exec || gloop_[1].exec || bench_graph_)
+    throw std::invalid_argument("set_grid_cap: must be called before the first solve or bench");
+  if (!fused_ok_) return;  // the streaming schedules are HBM-bound: nothing to share
+  fused_grid_ = ctas > 0 ? std::min(fused_grid_full_, ctas) : fused_grid_full_;
 }
 
 Engine::~Engine() {

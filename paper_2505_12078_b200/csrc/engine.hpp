@@ -109,6 +109,11 @@ class Engine {
   // SPOCK_WIDE_PROF=1: cycle counters of the wide kernel (summed over warps and launches)
   void wide_profile(unsigned long long* out10);
   const char* t_path() const { return fused_ok_ ? "fused" : (t_wide_ ? "wide" : "stages"); }
+  // CTAs of the fused T launch; a cap lets several solvers share the SMs
+  // (concurrent solves on their own streams).  Must precede the first solve /
+  // bench: the cached graphs hold the launch configuration.
+  int fused_grid() const { return fused_ok_ ? fused_grid_ : 0; }
+  void set_grid_cap(int ctas);
 
  private:
   void upload();
@@ -159,7 +164,7 @@ class Engine {
   bool fused_ok_ = false;
   bool narrow_ = true;
   FusedArgs fargs_{};
-  int fused_grid_ = 0;
+  int fused_grid_ = 0, fused_grid_full_ = 0;
   size_t fused_sync_bytes_ = 0;
   bool wide_ok_ = false;  // streaming kernel set up (records, smem, grid)
   bool t_wide_ = false;   // T runs on it

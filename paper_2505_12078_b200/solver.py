@@ -199,3 +199,92 @@ class SpockSolver:
         n = C.c_int32()
         _raise(self.lib, self.lib.spock_traffic_model(self.h, out.ctypes.data, C.byref(n)))
         return out, n.value
+
+    @property
+    def grid(self) -> int:
+        """CTAs of the fused T launch (0 when T runs on another schedule)."""
+        return int(self.lib.spock_solver_grid(self.h))
+
+    def set_grid_cap(self, ctas: int) -> None:
+        """Cap the fused T launch at `ctas` CTAs (0: full device); before the first solve."""
+        _raise(self.lib, self.lib.spock_solver_set_grid_cap(self.h, int(ctas)))
+
+
+class BatchSolver:
+    """Several x_init of one problem solved side by side (batched
+    multi-x_init / warm-started MPC solves; the reference solves one x_init per
+    call, proj/include/spock/solver.hpp:104-105, warm start 58-61).
+
+    On narrow trees one solve is bound by the latency of the 2N+2 dependent
+    tree levels and leaves most SMs idle, so `streams` solvers -- each with its
+    own device state, CUDA stream and cached solve graph, its fused T launch
+    capped to 1/streams of the device's CTAs -- run concurrently from host
+    threads (the C calls release the GIL).  Results are bitwise those of
+    sequential SpockSolver solves: every T item and reduction has a fixed
+    summation order whatever the grid.  On wide trees T is HBM-bound and the
+    streams only overlap the small kernels."""
+
+    def __init__(self, problem: Raocp, streams: int = 4, grid_cap: Optional[int] = None, **params):
+        if streams < 1:
+            raise ValueError("BatchSolver: streams must be >= 1")
+        import threading
+        self.solvers = [None] * streams
+        errs = []
+
+        def make(k):
+            try:
+                self.solvers[k] = SpockSolver(problem, **params)
+            except Exception as e:  # surfaced in the caller's thread
+                errs.append(e)
+
+        th = [threading.Thread(target=make, args=(k,)) for k in range(streams)]
+        for h in th:
+            h.start()
+        for h in th:
+            h.join()
+        if errs:
+            raise errs[0]
+        full = self.solvers[0].grid
+        cap = grid_cap if grid_cap is not None else (max(16, full // streams) if streams > 1 else 0)
+        for s in self.solvers:
+            s.set_grid_cap(cap)
+
+    def _run(self, algo: str, x_inits, warm):
+        import threading
+        n = len(x_inits)
+        if warm is not None and len(warm) != n:
+            raise ValueError("BatchSolver: one warm start per x_init")
+        out = [None] * n
+        errs = []
+        nxt = [0]
+        lock = threading.Lock()
+
+        def worker(s):
+            while True:
+                with lock:
+                    k = nxt[0]
+                    nxt[0] += 1
+                if k >= n or errs:
+                    return
+                try:
+                    out[k] = getattr(s, algo)(x_inits[k], None if warm is None else warm[k])
+                except Exception as e:  # surfaced in the caller's thread
+                    errs.append(e)
+                    return
+
+        th = [threading.Thread(target=worker, args=(s,)) for s in self.solvers[:max(1, min(n, len(self.solvers)))]]
+        for h in th:
+            h.start()
+        for h in th:
+            h.join()
+        if errs:
+            raise errs[0]
+        return out
+
+    def solve(self, x_inits, warm=None):
+        """SuperMann solves of every x_init (optional per-x_init warm (z, eta))."""
+        return self._run("solve", x_inits, warm)
+
+    def solve_cp(self, x_inits, warm=None):
+        """Plain CP solves of every x_init."""
+        return self._run("solve_cp", x_inits, warm)
