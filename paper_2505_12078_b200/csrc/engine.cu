@@ -1436,7 +1436,7 @@ void Engine::upload() {
     d1_ = dupload(d1);
     d2_ = dupload(d2);
   }
-  partial_ = dalloc<double>(size_t(4) * kMaxDots * kRedBlocks);
+  partial_ = dalloc<double>(size_t(4) * kRedRegion);
   red_out_ = dalloc<double>(256);
   CK(cudaMallocHost(&host_red_, 256 * sizeof(double)));
   for (int t = 0; t < 3; ++t) {
@@ -2112,10 +2112,10 @@ void Engine::build_loop_graph(GraphLoop& G, bool supermann) {
     X.x[0] = R, X.y[0] = Lsre, X.d[0] = d1_, X.n[0] = int(nz);
     X.x[1] = R + nz, X.y[1] = Lrz, X.d[1] = d2_, X.n[1] = int(ne);
     X.alpha = alpha;
-    launch_xi(X, partial_ + kMaxDots * kRedBlocks, red_out_ + 4, st_);
+    launch_xi(X, partial_ + kRedRegion, red_out_ + 4, st_);
     if (supermann) {
       loop_push(A, st_);
-      loop_gram(A, partial_ + 2 * kMaxDots * kRedBlocks, red_out_ + 8, st_);
+      loop_gram(A, partial_ + 2 * kRedRegion, red_out_ + 8, st_);
     }
     loop_begin(A, st_);
     if (supermann) loop_psi(A, st_);
@@ -2149,7 +2149,7 @@ void Engine::build_loop_graph(GraphLoop& G, bool supermann) {
             D.x[0] = CR, D.y[0] = PV, D.n[0] = int(nz);
             D.x[1] = CR + nz, D.y[1] = PV + nz, D.n[1] = int(ne);
             D.ndots = 2;
-            launch_dots(D, partial_ + 3 * kMaxDots * kRedBlocks, red_out_ + 3, st_);
+            launch_dots(D, partial_ + 3 * kRedRegion, red_out_ + 3, st_);
             loop_ls(A, st_);
           }),
           nullptr);
@@ -2279,7 +2279,7 @@ void Engine::solve_b(const double* x_init, const double* wz, const double* we, d
       X.x[1] = R + nz, X.y[1] = Lrz, X.d[1] = d2_, X.n[1] = int(ne);
       X.alpha = alpha;
       if (sharded) X.w[0] = shard_.mz, X.w[1] = shard_.me;
-      launch_xi(X, partial_ + kMaxDots * kRedBlocks, red_out_ + 4, st_);
+      launch_xi(X, partial_ + kRedRegion, red_out_ + 4, st_);
       // Anderson push (solver.cpp:57-63) and Gram of the differences
       int ngram = 0;
       if (supermann) {
@@ -2304,7 +2304,7 @@ void Engine::solve_b(const double* x_init, const double* wz, const double* we, d
               A.x[j] = prs[q].first, A.y[j] = prs[q].second, A.n[j] = int(nv), A.w[j] = w_v;
             }
             A.ndots = j;
-            launch_dots(A, partial_ + 2 * kMaxDots * kRedBlocks, red_out_ + 8 + c0, st_);
+            launch_dots(A, partial_ + 2 * kRedRegion, red_out_ + 8 + c0, st_);
           }
           ngram = int(prs.size());
         }
@@ -2410,7 +2410,7 @@ void Engine::solve_b(const double* x_init, const double* wz, const double* we, d
             A.x[0] = CR, A.y[0] = PV, A.n[0] = int(nz), A.w[0] = w_z;
             A.x[1] = CR + nz, A.y[1] = PV + nz, A.n[1] = int(ne), A.w[1] = w_e;
             A.ndots = 2;
-            launch_dots(A, partial_ + 3 * kMaxDots * kRedBlocks, red_out_ + 3, st_);
+            launch_dots(A, partial_ + 3 * kRedRegion, red_out_ + 3, st_);
           }
           if (sharded) coll(1, red_out_, 5);
           fetch(5);

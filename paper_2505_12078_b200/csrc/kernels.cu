@@ -795,7 +795,7 @@ __global__ void k_scatter(int n, const int* __restrict__ perm, const double* __r
 
 // Deterministic multi-dot: block partials over a fixed grid, then one block
 // sums them in index order.
-__global__ void __launch_bounds__(kRedThreads) k_dots(DotArgs A, double* __restrict__ partial) {
+__global__ void __launch_bounds__(kRedThreads) k_dots(DotArgs A, double* __restrict__ partial, double* out) {
   __shared__ double sm[kMaxDots][kRedThreads / 32];
   double acc[kMaxDots];
 #pragma unroll
@@ -827,19 +827,12 @@ __global__ void __launch_bounds__(kRedThreads) k_dots(DotArgs A, double* __restr
     for (int k = 0; k < kRedThreads / 32; ++k) s += sm[threadIdx.x][k];
     partial[size_t(threadIdx.x) * gridDim.x + blockIdx.x] = s;
   }
-}
-
-__global__ void k_finalize_sum(int nvals, int nparts, const double* __restrict__ partial, double* out) {
-  const int j = threadIdx.x;
-  if (j >= nvals) return;
-  double s = 0.0;
-  for (int k = 0; k < nparts; ++k) s += partial[size_t(j) * nparts + k];
-  out[j] = s;
+  grid_finalize<false>(partial, A.ndots, out, red_counter(partial));
 }
 
 // xi infinity norms: max_i |(x_i / alpha - y_i) * d_i| for two (x, y, d)
 // triples; NaN flagged through a separate count.
-__global__ void __launch_bounds__(kRedThreads) k_xi(XiArgs A, double* __restrict__ partial) {
+__global__ void __launch_bounds__(kRedThreads) k_xi(XiArgs A, double* __restrict__ partial, double* out) {
   __shared__ double sm[2][kRedThreads / 32];
   __shared__ int nanflag;
   if (threadIdx.x == 0) nanflag = 0;
@@ -868,19 +861,7 @@ __global__ void __launch_bounds__(kRedThreads) k_xi(XiArgs A, double* __restrict
     for (int k = 0; k < kRedThreads / 32; ++k) s = fmax(s, sm[threadIdx.x][k]);
     partial[size_t(threadIdx.x) * gridDim.x + blockIdx.x] = nanflag ? NAN : s;
   }
-}
-
-__global__ void k_finalize_max(int nvals, int nparts, const double* __restrict__ partial, double* out) {
-  const int j = threadIdx.x;
-  if (j >= nvals) return;
-  double s = 0.0;
-  bool nan = false;
-  for (int k = 0; k < nparts; ++k) {
-    const double v = partial[size_t(j) * nparts + k];
-    if (isnan(v)) nan = true;
-    s = fmax(s, v);
-  }
-  out[j] = nan ? NAN : s;
+  grid_finalize<true>(partial, 2, out, red_counter(partial));
 }
 
 // ---------------------------------------------------------------------------
@@ -1084,13 +1065,11 @@ void launch_scatter(int n, const int* perm, const double* src, double* dst, cuda
 }
 
 void launch_dots(const DotArgs& A, double* partial, double* out, cudaStream_t st) {
-  k_dots<<<kRedBlocks, kRedThreads, 0, st>>>(A, partial);
-  k_finalize_sum<<<1, 32, 0, st>>>(A.ndots, kRedBlocks, partial, out);
+  k_dots<<<kRedBlocks, kRedThreads, 0, st>>>(A, partial, out);
 }
 
 void launch_xi(const XiArgs& A, double* partial, double* out, cudaStream_t st) {
-  k_xi<<<kRedBlocks, kRedThreads, 0, st>>>(A, partial);
-  k_finalize_max<<<1, 32, 0, st>>>(2, kRedBlocks, partial, out);
+  k_xi<<<kRedBlocks, kRedThreads, 0, st>>>(A, partial, out);
 }
 
 void launch_bgemm(const BGemmArgs& G, int count, cudaStream_t st) {
@@ -1118,8 +1097,7 @@ void set_carveout_all() {
       reinterpret_cast<const void*>(&k_s1_fwd), reinterpret_cast<const void*>(&k_s2),
       reinterpret_cast<const void*>(&k_axpby), reinterpret_cast<const void*>(&k_lincomb),
       reinterpret_cast<const void*>(&k_gather), reinterpret_cast<const void*>(&k_scatter),
-      reinterpret_cast<const void*>(&k_dots), reinterpret_cast<const void*>(&k_finalize_sum),
-      reinterpret_cast<const void*>(&k_xi), reinterpret_cast<const void*>(&k_finalize_max)};
+      reinterpret_cast<const void*>(&k_dots), reinterpret_cast<const void*>(&k_xi)};
   for (const void* f : fs)
     cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
 }

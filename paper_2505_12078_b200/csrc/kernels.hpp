@@ -10,6 +10,12 @@ namespace spock {
 constexpr int kRedBlocks = 2 * 148;  // fixed grid => run-to-run identical reductions
 constexpr int kRedThreads = 256;
 constexpr int kMaxDots = 16;
+// one reduction scratch region: kMaxDots x kRedBlocks block partials, then the
+// arrival counter of the last-block finalize (grid_finalize, dev.cuh)
+constexpr int kRedRegion = kMaxDots * kRedBlocks + 2;
+__host__ __device__ inline unsigned int* red_counter(double* partial) {
+  return reinterpret_cast<unsigned int*>(partial + size_t(kMaxDots) * kRedBlocks);
+}
 
 struct LinCombArgs {
   const double* x[16];

@@ -87,7 +87,8 @@ __global__ void k_push(const __grid_constant__ LoopArgs A) {
 }
 
 // Gram of the difference columns and M_d' r: pairs (a <= b) row-major, then a
-__global__ void __launch_bounds__(kRedThreads) k_gram(const __grid_constant__ LoopArgs A, double* __restrict__ partial) {
+__global__ void __launch_bounds__(kRedThreads) k_gram(const __grid_constant__ LoopArgs A, double* __restrict__ partial,
+                                                      double* out) {
   constexpr int MD = kLoopMaxMem * (kLoopMaxMem + 1) / 2 + kLoopMaxMem;
   __shared__ double sm[MD][kRedThreads / 32];
   const LoopState& S = *A.st;
@@ -129,15 +130,9 @@ __global__ void __launch_bounds__(kRedThreads) k_gram(const __grid_constant__ Lo
     for (int k = 0; k < kRedThreads / 32; ++k) s += sm[threadIdx.x][k];
     partial[size_t(threadIdx.x) * gridDim.x + blockIdx.x] = s;
   }
+  grid_finalize<false>(partial, MD, out, red_counter(partial));
 }
 
-__global__ void k_gram_final(int nvals, int nparts, const double* __restrict__ partial, double* out) {
-  const int j = threadIdx.x;
-  if (j >= nvals) return;
-  double s = 0.0;
-  for (int k = 0; k < nparts; ++k) s += partial[size_t(j) * nparts + k];
-  out[j] = s;
-}
 
 // top of iteration k (solver.cpp:233-290): M-norm, xi thresholds, termination,
 // Anderson direction coefficients, K0 test; selects the branch body
@@ -346,9 +341,7 @@ inline int vec_blocks(int64_t n) { return int(std::min<int64_t>((n + 255) / 256,
 
 void loop_push(const LoopArgs& A, cudaStream_t st) { k_push<<<vec_blocks(A.nv), 256, 0, st>>>(A); }
 void loop_gram(const LoopArgs& A, double* partial, double* out, cudaStream_t st) {
-  constexpr int MD = kLoopMaxMem * (kLoopMaxMem + 1) / 2 + kLoopMaxMem;
-  k_gram<<<kRedBlocks, kRedThreads, 0, st>>>(A, partial);
-  k_gram_final<<<1, 32, 0, st>>>(MD, kRedBlocks, partial, out);
+  k_gram<<<kRedBlocks, kRedThreads, 0, st>>>(A, partial, out);
 }
 void loop_begin(const LoopArgs& A, cudaStream_t st) { k_begin<<<1, 1, 0, st>>>(A); }
 void loop_psi(const LoopArgs& A, cudaStream_t st) { k_psi<<<vec_blocks(A.nv), 256, 0, st>>>(A); }
