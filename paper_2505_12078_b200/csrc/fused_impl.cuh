@@ -192,6 +192,7 @@ __device__ void cta_soc_project(double* v, const double* a, int d, double* red) 
   }
   const double hn = sqrt(cta_sum(s, red));
   const double tt = v[d - 1];
+  __syncthreads();  // every thread has read v[d-1] before thread 0 rewrites it
   if (hn <= tt) {
   } else if (hn <= -tt) {
     for (int r = t; r < d; r += kFT) v[r] = 0.0;
@@ -465,11 +466,23 @@ __device__ void item_back(const FusedArgs& F, const ItemRec& P, const Slot& S, d
   stamp(F, item, 1);
   stamp(F, item, 4);
   for (int r = t; r < m; r += kFT) {
+    // children terms: up to four children's loads in flight at once (one L2
+    // round trip instead of one per child), summed in child order
     double sa = 0.0, st = 0.0;
-    for (int c = 0; c < nch; ++c) {
-      const size_t o = size_t(c0 + c - 1) * m + r;
-      sa += ldcg(D.adj + o);
-      st += ldcg(D.T12 + o);
+    for (int c = 0; c < nch; c += 4) {
+      double va[4], vt[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const size_t o = size_t(c0 + c + k - 1) * m + r;
+        va[k] = c + k < nch ? ldcg(D.adj + o) : 0.0;
+        vt[k] = c + k < nch ? ldcg(D.T12 + o) : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (c + k < nch) {
+          sa += va[k];
+          st += vt[k];
+        }
     }
     if (r < nx) {
       q[r] += st + al * sa;  // v_x
@@ -516,6 +529,7 @@ __device__ void item_fwd(const FusedArgs& F, const ItemRec& P, const Slot& S, do
   double* ahat = xn + kSlot;   // anc (x^, u^)
   double* val = ahat + kSlot;  // segment values
   double* pv = val + kSlot;    // p / alpha
+  double* early = pv + kSlot;    // own d (nu), then hat tau_c, hat s_c (loaded early)
   const int px = P.px, pu = P.pu;
   int mk = 0;
   const double* Mf = root ? nullptr : S.mp[mk++];  // M1 (leaf) or [M1; K M1] (non-leaf)
@@ -538,6 +552,9 @@ __device__ void item_fwd(const FusedArgs& F, const ItemRec& P, const Slot& S, do
   if (!root) {
     const double* zax = sp(F_AX);
     const double* zau = sp(F_AU);
+    // hat tau_c, hat s_c (written by the parent's S2): in the same load round
+    if (t == kFT - 1) early[nu] = 2.0 * ldcg(zo + D.tau_base + c - 1) - z[D.tau_base + c - 1];
+    if (t == kFT - 2) early[nu + 1] = 2.0 * ldcg(zo + D.s_base + c - 1) - z[D.s_base + c - 1];
     for (int r = t; r < m; r += kFT) {
       if (r < nx) {
         const double xp = ldcg(zo + 1 + size_t(an) * nx + r);
@@ -545,16 +562,24 @@ __device__ void item_fwd(const FusedArgs& F, const ItemRec& P, const Slot& S, do
         ahat[r] = 2.0 * xp - zax[r];
       } else {
         xd[r] = ldcg(D.dvec + size_t(an) * nu + (r - nx));
+        // own d in the same load round (final: every backward item precedes the root forward)
+        if (!leaf) early[r - nx] = ldcg(D.dvec + size_t(c) * nu + (r - nx));
         ahat[r] = 2.0 * ldcg(zo + D.u_base + size_t(an) * nu + (r - nx)) - zau[r - nx];
       }
     }
     __syncthreads();
     cta_gemv(Mf, leaf ? nx : m, m, leaf ? nx : m, xd, xn, false, red);  // [x; u - d] = Mf xd
+    // one owner per entry: u rows get their own d in the same pass (a second
+    // pass indexed by r - nx would race with this one on xn[nx..m))
     const double* fc = sp(F_FC);
-    for (int r = t; r < (leaf ? nx : m); r += kFT) xn[r] += fc[r];
+    for (int r = t; r < (leaf ? nx : m); r += kFT) {
+      double v = xn[r] + fc[r];
+      if (!leaf && r >= nx) v += early[r - nx];
+      xn[r] = v;
+    }
+  } else {
+    for (int r = t; r < nu; r += kFT) xn[nx + r] += ldcg(D.dvec + r);
   }
-  if (!leaf)
-    for (int r = t; r < nu; r += kFT) xn[nx + r] += ldcg(D.dvec + size_t(c) * nu + r);
   __syncthreads();
   for (int r = t; r < (leaf ? nx : m); r += kFT) {
     if (r < nx)
@@ -574,7 +599,7 @@ __device__ void item_fwd(const FusedArgs& F, const ItemRec& P, const Slot& S, do
   __syncthreads();
   auto hatv = [&](int idx) { return 2.0 * ldcg(zo + idx) - z[idx]; };
   if (!root) {  // stage-cost SOC block of (x_anc, u_anc, tau_c)
-    const int k = c - 1, p = px + pu, o2 = P.s2o;
+    const int p = px + pu, o2 = P.s2o;
     const double* qk = sp(F_QK);
     double part = 0.0;
     for (int r = t; r < m; r += kFT) part += qk[r] * ahat[r];
@@ -582,7 +607,7 @@ __device__ void item_fwd(const FusedArgs& F, const ItemRec& P, const Slot& S, do
     cta_gemv(Hx, px, nx, px, ahat, val, false, red);
     cta_gemv(Hu, pu, nu, pu, ahat + nx, val + px, false, red);
     if (t == 0) {
-      const double row = 0.5 * hatv(D.tau_base + k) - 0.5 * qd;
+      const double row = 0.5 * early[nu] - 0.5 * qd;  // hat tau_c
       val[p] = row;
       val[p + 1] = row;
     }
@@ -651,7 +676,7 @@ __device__ void item_fwd(const FusedArgs& F, const ItemRec& P, const Slot& S, do
       }
     }
     if (t == 0) {
-      const double sv = hatv(c == 0 ? 0 : D.s_base + c - 1) - by;
+      const double sv = (c == 0 ? hatv(0) : early[nu + 1]) - by;
       const double pp = seg1[ny] + al * sv;
       eo[so + ny] = pp - al * fmax(0.0, pp / al);
     }
@@ -695,7 +720,7 @@ __device__ void item_fwd(const FusedArgs& F, const ItemRec& P, const Slot& S, do
     const double qd = cta_sum(part, red);
     cta_gemv(HN, p, nx, p, hat, val, false, red);
     if (t == 0) {
-      const double row = 0.5 * hatv(D.s_base + c - 1) - 0.5 * qd;
+      const double row = 0.5 * early[nu + 1] - 0.5 * qd;  // hat s_c
       val[p] = row;
       val[p + 1] = row;
     }
@@ -735,6 +760,7 @@ __global__ void __launch_bounds__(kFT, 1) k_T_fused(FusedArgs F) {
   }
   uint32_t phase[2] = {0u, 0u};
   const int total = F.D.nnl + 2 * F.D.nn;
+
   __syncthreads();
   int cur = 0;
   if (tk[0] < total) {
