@@ -25,7 +25,7 @@ for g in ([0, 16, 24, 32, 48, 64, 96, 148] if "--grid" in sys.argv else []):
 
 rng = np.random.default_rng(3)
 xs = [p.x_init * (1.0 + 0.2 * rng.standard_normal(p.x_init.shape)) for _ in range(8)]
-for B, g in ((1, 0), (4, 37), (4, 74), (4, 148), (8, 18), (8, 37), (8, 74)):
+for B, g in ((1, 0), (2, 74), (4, 74), (8, 37)):
     os.environ["SPOCK_FUSED_GRID"] = str(g)
     sv = [SpockSolver(p, max_iters=iters) for _ in range(B)]
     for s, x in zip(sv, xs):
