@@ -416,6 +416,9 @@ __device__ __forceinline__ void spans_ready(Ring& R, const SpanWait& W) {
   if (R.prof) t0 = clock64();
   while (!mbar_try_wait(W.bar, W.parity)) {
   }
+  // the lanes' dependency loads into shared scratch (xs, dep) are read by other
+  // lanes from here on: order them explicitly (independent thread scheduling)
+  __syncwarp();
   if (R.prof) R.t_span += clock64() - t0;
 }
 
