@@ -24,8 +24,9 @@ for g in ([0, 16, 24, 32, 48, 64, 96, 148] if "--grid" in sys.argv else []):
     del s
 
 rng = np.random.default_rng(3)
-xs = [p.x_init * (1.0 + 0.2 * rng.standard_normal(p.x_init.shape)) for _ in range(8)]
-for B, g in ((1, 0), (2, 74), (4, 74), (8, 37)):
+xs = [p.x_init * (1.0 + 0.2 * rng.standard_normal(p.x_init.shape)) for _ in range(64)]
+plan = os.environ.get("PROBE_B", "1:0,2:74,4:74,8:37")
+for B, g in [tuple(int(v) for v in item.split(":")) for item in plan.split(",")]:
     os.environ["SPOCK_FUSED_GRID"] = str(g)
     sv = [SpockSolver(p, max_iters=iters) for _ in range(B)]
     for s, x in zip(sv, xs):
