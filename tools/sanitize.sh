@@ -1,7 +1,7 @@
 #!/bin/bash
 # compute-sanitizer sweep over every T schedule and the solve loop (GPU box):
 #   bash tools/sanitize.sh > gpurun_out/sanitize.txt
-# racecheck (shared-memory hazards) and memcheck (out-of-bounds / misaligned
+# racecheck (shared-memory hazards), synccheck (barrier misuse) and memcheck (out-of-bounds / misaligned
 # global and shared accesses) on c2 (223 nodes); prints one summary per run.
 cd "$(dirname "$0")/.."
 run() {  # name, env, tool, command...
@@ -11,7 +11,7 @@ run() {  # name, env, tool, command...
   echo "$name [$tool] $(echo "$out" | grep -E 'ERROR SUMMARY|RACECHECK SUMMARY' | tail -1) $(echo "$out" | grep -o 'ok [a-z]*' | tail -1)"
   echo "$out" | grep -E "Error|Thread \(" | sort | uniq -c | head -6
 }
-for tool in racecheck memcheck; do
+for tool in racecheck memcheck synccheck; do
   run "T fused" "" $tool python tools/few_T.py c2
   run "T wide" "SPOCK_T_UNFUSED=1 SPOCK_T_WIDE=1" $tool python tools/few_T.py c2
   run "T stages" "SPOCK_T_UNFUSED=1 SPOCK_T_WIDE=0" $tool python tools/few_T.py c2
