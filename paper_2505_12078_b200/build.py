@@ -8,6 +8,7 @@ from __future__ import annotations
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
@@ -27,7 +28,7 @@ def _newest_header() -> float:
 def build(verbose: bool = False, force: bool = False) -> str:
     os.makedirs(OUT, exist_ok=True)
     hdr = _newest_header()
-    objs = []
+    objs, cmds = [], []
     for src in SOURCES:
         sp = os.path.join(CSRC, src)
         obj = os.path.join(OUT, os.path.splitext(src)[0] + ".o")
@@ -39,7 +40,13 @@ def build(verbose: bool = False, force: bool = False) -> str:
             cmd = [NVCC, *FLAGS, "-x", "c++", "-c", sp, "-o", obj]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
-        subprocess.run(cmd, check=True)
+        cmds.append(cmd)
+    # translation units are independent: compile them concurrently
+    jobs = int(os.environ.get("SPOCK_BUILD_JOBS", str(os.cpu_count() or 4)))
+    with ThreadPoolExecutor(max_workers=max(1, jobs)) as ex:
+        for r in list(ex.map(lambda c: subprocess.run(c), cmds)):
+            if r.returncode != 0:
+                raise subprocess.CalledProcessError(r.returncode, r.args)
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
         cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs]
         if verbose:

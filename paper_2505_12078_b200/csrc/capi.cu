@@ -64,6 +64,12 @@ int check(spock_solver* s) {
     g_err = "spock: null solver handle";
     return SPOCK_EINVAL;
   }
+  // the current device is per host thread: run on the solver's own device
+  // whatever thread calls (BatchSolver workers, user threads)
+  if (cudaSetDevice(s->eng->device()) != cudaSuccess) {
+    g_err = "spock: cannot make the solver's device current";
+    return SPOCK_ECUDA;
+  }
   return SPOCK_OK;
 }
 }  // namespace
@@ -105,6 +111,7 @@ int spock_solver_create(const spock_problem_desc* desc, const spock_params* para
 
 void spock_solver_destroy(spock_solver* s) {
   if (!s) return;
+  if (s->eng) cudaSetDevice(s->eng->device());
   delete s->eng;
   delete s;
 }

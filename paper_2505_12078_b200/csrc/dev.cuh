@@ -17,6 +17,23 @@
 
 namespace spock {
 
+// Opt-in maximum dynamic shared memory per block on the current device.  The
+// MaxDynamicSharedMemorySize attribute of a kernel is process-global, not per
+// solver: each kernel gets this maximum (once it is known to cover the launch)
+// so that a later solver with smaller blocks never lowers the limit under an
+// earlier solver's launches.  Occupancy follows the launch's own byte count.
+inline int smem_optin_max() {
+  int dev = 0, v = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  return v;
+}
+inline cudaError_t set_smem_limit(const void* f, int need) {
+  const int mx = smem_optin_max();
+  if (need > mx) return cudaErrorInvalidValue;
+  return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+}
+
 constexpr int kWarps = 8;          // warps per CTA in warp-per-node kernels
 constexpr int kMaxD = 256;         // max nx+nu (and any per-node GEMV length)
 constexpr int kMaxR = kMaxD / 32;  // rows per lane

@@ -95,8 +95,7 @@ Engine::Engine(const spock_problem_desc* desc, const Params& prm) : prm_(prm) {
   lay_ = make_layouts(p_, soc_);
   require(p_.nx + p_.nu <= kMaxD, "spock-b200: nx + nu above 256 is not supported");
   stage_start_ = p_.tree.stage_start;
-  int dev = 0;
-  CK(cudaGetDevice(&dev));
+  CK(cudaGetDevice(&dev_));
   CK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
   set_carveout_all();
   set_carveout_narrow();
@@ -878,6 +877,21 @@ void Engine::shard_set_collectives(CollFn fn, void* user) {
   shard_.coll_user = user;
 }
 
+// Cancellation of a sharded solve is a collective decision: each rank polls its
+// own callback and the ranks all-reduce the flags with MAX, so either every rank
+// stops at this iteration or none does (a lone rank leaving would strand the
+// others in their next collective).  Unsharded: the callback's own answer.
+bool Engine::agree_cancel(bool mine) {
+  if (!shard_solving_ || !shard_.coll || shard_.G == 1) return mine;
+  if (!cancel_dev_) cancel_dev_ = dalloc<double>(1);
+  host_red_[255] = mine ? 1.0 : 0.0;
+  CK(cudaMemcpyAsync(cancel_dev_, host_red_ + 255, sizeof(double), cudaMemcpyHostToDevice, st_));
+  coll(2, cancel_dev_, 1);
+  CK(cudaMemcpyAsync(host_red_ + 255, cancel_dev_, sizeof(double), cudaMemcpyDeviceToHost, st_));
+  sync();
+  return host_red_[255] != 0.0;
+}
+
 void Engine::coll(int op, double* buf, int64_t n) {
   if (!shard_.coll || shard_.G == 1 || n <= 0) return;
   if (shard_.coll(shard_.coll_user, op, buf, n) != 0) throw std::runtime_error("sharded solve: collective failed");
@@ -1645,18 +1659,21 @@ void Engine::L(const double* z, double* eta) {
   }
   if (wide_ok_ && !lop_wide_ && lop_narrow_) {
     launch_L_lop(D_, wargs_, lrec_, z, eta, lop_rows_, lop_mat_, lop_vec_, st_);
+    CK(cudaGetLastError());
     return;
   }
   if (wide_ok_ && lop_wide_) {  // warp-granular streaming items (wide.cu, kind 3)
     WideArgs A = wargs_;
     A.D = D_, A.z = z, A.eo = eta;
     launch_wide(A, lrec_, nlrec_);
+    CK(cudaGetLastError());
     return;
   }
   if (narrow_)
     launch_L_narrow(D_, z, eta, st_);
   else
     launch_L(D_, z, 1.0, nullptr, 0.0, nullptr, eta, 0.0, false, st_);
+  CK(cudaGetLastError());
 }
 
 void Engine::Lt(const double* eta, double* z) {
@@ -1666,6 +1683,7 @@ void Engine::Lt(const double* eta, double* z) {
   }
   if (wide_ok_ && !lop_wide_ && lop_narrow_) {
     launch_Lt_lop(D_, wargs_, ltrec_, eta, z, lop_rows_, lop_mat_, lop_vec_, st_);
+    CK(cudaGetLastError());
     return;
   }
   if (wide_ok_ && lop_wide_) {  // kinds 4 (child terms, flagged) then 5 (node rows)
@@ -1673,12 +1691,14 @@ void Engine::Lt(const double* eta, double* z) {
     A.D = D_, A.eta = eta, A.zo = z;
     CK(cudaMemsetAsync(wide_flags_, 0, sizeof(int) * size_t(p_.tree.nn()), st_));
     launch_wide(A, ltrec_, nltrec_);
+    CK(cudaGetLastError());
     return;
   }
   if (narrow_)
     launch_Lt_narrow(D_, eta, z, st_);
   else
     launch_Lt(D_, eta, nullptr, z, 0.0, 1.0, 0.0, st_);
+  CK(cudaGetLastError());
 }
 
 // one CP application (solver.cpp:148-164), internal layout; zo/eo must not
@@ -1700,6 +1720,7 @@ void Engine::T(const double* z, const double* eta, double* zo, double* eo) {
     F.alpha = alpha_;
     CK(cudaMemsetAsync(F.ticket, 0, fused_sync_bytes_, st_));
     launch_T_fused(F, fused_grid_, st_);
+    CK(cudaGetLastError());
     return;
   }
   if (t_wide_) {
@@ -1713,17 +1734,20 @@ void Engine::T(const double* z, const double* eta, double* zo, double* eo) {
     CK(cudaMemsetAsync(wide_flags_, 0, wide_flag_bytes_, st_));
     if (t_split_) {
       for (int k = 0; k < 3; ++k) launch_wide(A, tsplit_rec_[k], tsplit_n_[k]);
+      CK(cudaGetLastError());
       return;
     }
     A.recs = wargs_.recs;
     A.ntick = wargs_.ntick;
     launch_T_wide(A, wide_rows_, wide_ctas_, wide_grid_, st_);
+    CK(cudaGetLastError());
     return;
   }
   launch_Lt(D_, eta, z, zo, 1.0, -alpha_, -alpha_, st_);
   launch_s1(D_, stage_start_.data(), zo, st_);
   launch_s2(D_, zo, st_);
   launch_L(D_, zo, 2.0, z, -1.0, eta, eo, alpha_, true, st_);
+  CK(cudaGetLastError());
 }
 
 void Engine::dots(std::initializer_list<std::pair<const double*, const double*>> pairs, int64_t n_default,
@@ -2335,7 +2359,7 @@ void Engine::solve_b(const double* x_init, const double* wz, const double* we, d
         reason = SPOCK_CONVERGED;
       else if (k >= prm_.max_iters)
         reason = SPOCK_MAX_ITERS;
-      else if (prm_.cancelled && (k % std::max(1, prm_.poll_every) == 0) && prm_.cancelled())
+      else if (prm_.cancelled && (k % std::max(1, prm_.poll_every) == 0) && agree_cancel(prm_.cancelled()))
         reason = SPOCK_CANCELLED;
       if (reason >= 0) {
         st.reason = reason;

@@ -101,6 +101,7 @@ class Engine {
   typedef int (*CollFn)(void* user, int op, double* buf, int64_t n);
   void shard_set_collectives(CollFn fn, void* user);
   cudaStream_t stream() const { return st_; }
+  int device() const { return dev_; }
   double* scratch_z(int k) const { return scratch_z_[k]; }
   double* scratch_e(int k) const { return scratch_e_[k]; }
   int launches_per_T() const {
@@ -146,6 +147,7 @@ class Engine {
   Dev D_{};
   std::vector<int> stage_start_;
   cudaStream_t st_ = nullptr;
+  int dev_ = 0;  // the device current at construction; every C-ABI entry makes it current again
   std::vector<void*> allocs_;
   OpNorm norm_;
   double alpha_ = 0.0;
@@ -204,6 +206,8 @@ class Engine {
   bool shard_solving_ = false;
   std::vector<WRec> lrecs_h_, ltrecs_h_;
   void coll(int op, double* buf, int64_t n);
+  bool agree_cancel(bool mine);
+  double* cancel_dev_ = nullptr;
   void shard_T(const double* z, const double* eta, double* zo, double* eo);
   void shard_L(const double* z, double* eta);
   void shard_Lt(const double* eta, double* z);

@@ -109,7 +109,7 @@ cudaError_t fused_configure(int smem_bytes, int threads) {
   // every kernel of the engine prefers the maximum shared-memory carveout, so
   // consecutive launches never wait for an SM to change its L1 / smem split
   cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-  return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+  return set_smem_limit(f, smem_bytes);
 }
 
 const void* fused_kernel_ptr(int threads) {

@@ -1103,7 +1103,7 @@ void set_carveout_all() {
 }
 
 cudaError_t set_alg1_smem(int bytes) {
-  return cudaFuncSetAttribute(k_alg1_parent, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  return set_smem_limit(reinterpret_cast<const void*>(&k_alg1_parent), bytes);
 }
 
 }  // namespace spock

@@ -378,9 +378,9 @@ int lop_smem_bytes(int rows, int mat_cap, int vec_cap) {
 cudaError_t lop_configure(int bytes) {
   cudaFuncSetAttribute(k_L_node, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   cudaFuncSetAttribute(k_Lt_node, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-  cudaError_t e = cudaFuncSetAttribute(k_L_node, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaError_t e = set_smem_limit(reinterpret_cast<const void*>(&k_L_node), bytes);
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(k_Lt_node, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  return set_smem_limit(reinterpret_cast<const void*>(&k_Lt_node), bytes);
 }
 
 void launch_L_lop(const Dev& D, const WideArgs& W, const WRec* lrec, const double* z, double* eta, int rows,

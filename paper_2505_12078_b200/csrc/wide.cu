@@ -1437,13 +1437,26 @@ cudaError_t wide_configure(int rows, int ctas, int smem_bytes) {
                        cudaSharedmemCarveoutMaxShared);
   cudaFuncSetAttribute(reinterpret_cast<const void*>(&k_shard_unpack),
                        cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-  return cudaFuncSetAttribute(wide_kernel_ptr(rows, ctas), cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+  return set_smem_limit(wide_kernel_ptr(rows, ctas), smem_bytes);
 }
 
+// Items spin on the flags of smaller tickets and tickets are dealt round-robin
+// by warp index, so every CTA of the grid must be resident at once: the launch
+// is cooperative, which makes the runtime guarantee co-residency (or fail the
+// launch) even when other kernels -- a concurrent solver's stream, another
+// process under MPS -- hold part of the device.
 void launch_T_wide(const WideArgs& A, int rows, int ctas, int grid, cudaStream_t st) {
-  const int smem = wide_smem_bytes(A);
-  const int threads = 32 * A.warps;
-#define WLAUNCH(R, M) k_T_wide<R, M><<<grid, threads, smem, st>>>(A)
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(32 * A.warps);
+  cfg.dynamicSmemBytes = size_t(wide_smem_bytes(A));
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+#define WLAUNCH(R, M) cudaLaunchKernelEx(&cfg, k_T_wide<R, M>, A)
   WIDE_SWITCH(rows, ctas, WLAUNCH);
 #undef WLAUNCH
 }

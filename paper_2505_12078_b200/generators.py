@@ -130,8 +130,8 @@ CONFIGS = {
     "c1": dict(N=5, nb=3, nw=2, nx=10, nu=5, gamma=0.95, perturb=0.0),
     "c2": dict(N=10, nb=5, nw=2, nx=50, nu=25, gamma=None, perturb=0.01),
     "c2p": dict(N=10, nb=8, nw=2, nx=50, nu=25, gamma=None, perturb=0.01),
-    "c3": dict(N=12, nb=8, nw=3, nx=50, nu=25, gamma=None, perturb=0.0),
-    "c4": dict(N=12, nb=4, nw=10, nx=50, nu=25, gamma=None, perturb=0.0),
+    "c3": dict(N=12, nb=8, nw=3, nx=50, nu=25, gamma=None, perturb=0.01),
+    "c4": dict(N=12, nb=4, nw=10, nx=50, nu=25, gamma=None, perturb=0.01),
 }
 
 

@@ -199,6 +199,14 @@ class RiskSpec:
         return int(self.E.shape[0])
 
 
+def dual_cone(parts: List[ConePart]) -> List[ConePart]:
+    """Dual of a cone product (proj/src/risk.cpp:25-43): Zero <-> Free, the
+    nonnegative orthant and the SOC are self-dual.  S3 projects the risk rows
+    of eta onto this cone (projections.cpp:212-244)."""
+    swap = {CONE_ZERO: CONE_FREE, CONE_FREE: CONE_ZERO}
+    return [ConePart(swap.get(c.kind, c.kind), c.dim) for c in parts]
+
+
 def avar_spec(gamma: float, pi: np.ndarray) -> RiskSpec:
     """AV@R_gamma with base probabilities pi (proj/src/risk.cpp:65-98)."""
     if gamma < 0.0 or gamma > 1.0:

@@ -215,9 +215,12 @@ class ShardedSolver:
         eta = np.ascontiguousarray(eta, dtype=np.float64)
         z_out = np.zeros_like(z) if z_out is None else z_out
         eta_out = np.zeros_like(eta) if eta_out is None else eta_out
-        self._raise(self.lib, self.lib.spock_shard_apply_T(self.solver.h, 0, _ptr(z), _ptr(eta), None, None))
+        nz, ne = self.nz, self.neta
+        self._raise(self.lib, self.lib.spock_shard_apply_T(self.solver.h, 0, _ptr(z, nz, "apply_T: z"),
+                                                           _ptr(eta, ne, "apply_T: eta"), None, None))
         self._exchange()
-        self._raise(self.lib, self.lib.spock_shard_apply_T(self.solver.h, 1, None, None, _ptr(z_out), _ptr(eta_out)))
+        self._raise(self.lib, self.lib.spock_shard_apply_T(self.solver.h, 1, None, None, _ptr(z_out, nz, "apply_T: z_out"),
+                                                           _ptr(eta_out, ne, "apply_T: eta_out")))
         return z_out, eta_out
 
     def weights(self):
@@ -259,7 +262,9 @@ class ShardedSolver:
         z = np.zeros(self.nz)
         zs = np.zeros(self.nz)
         e = np.zeros(self.neta)
-        x = None if x_init is None else np.ascontiguousarray(x_init, dtype=np.float64)
+        x = None if x_init is None else np.ascontiguousarray(x_init, dtype=np.float64).ravel()
+        if x is not None and x.size != self.solver.problem.nx:
+            raise ValueError("solve: x_init has wrong length")
         rc = fn(self.solver.h, _ptr(x), None, None, _ptr(z), _ptr(zs), _ptr(e), C.byref(st))
         self._raise(self.lib, rc)
         # every rank's own entries -> the whole solution on every rank

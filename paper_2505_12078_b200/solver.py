@@ -41,16 +41,47 @@ def _raise(lib, rc: int, prefix: str = "spock"):
     raise RuntimeError(msg)
 
 
-def _ptr(a):
-    """Raw pointer of a numpy array or torch tensor (float64, contiguous)."""
+def _ptr(a, n: Optional[int] = None, what: str = "vector"):
+    """Raw pointer of a numpy array or torch tensor: float64, contiguous and, when
+    `n` is given, exactly n entries (the reference throws std::invalid_argument
+    on wrong dimensions, proj/src/solver.cpp:191,200-201; here a short buffer
+    would otherwise be read or written out of bounds by the library)."""
     if a is None:
         return None
     if isinstance(a, np.ndarray):
-        assert a.dtype == np.float64 and a.flags.c_contiguous
+        if a.dtype != np.float64:
+            raise ValueError(f"{what}: dtype must be float64, got {a.dtype}")
+        if not a.flags.c_contiguous:
+            raise ValueError(f"{what}: must be contiguous")
+        if n is not None and a.size != n:
+            raise ValueError(f"{what} has wrong length ({a.size}, expected {n})")
         return a.ctypes.data
     # torch tensor
-    assert a.dtype.is_floating_point and a.is_contiguous()
+    import torch
+    if not isinstance(a, torch.Tensor):
+        raise ValueError(f"{what}: expected a numpy array or torch tensor, got {type(a).__name__}")
+    if a.dtype != torch.float64:
+        raise ValueError(f"{what}: dtype must be torch.float64, got {a.dtype}")
+    if not a.is_contiguous():
+        raise ValueError(f"{what}: must be contiguous")
+    if n is not None and a.numel() != n:
+        raise ValueError(f"{what} has wrong length ({a.numel()}, expected {n})")
     return a.data_ptr()
+
+
+def _f64(a):
+    """Host copy as contiguous float64 unless `a` is already a float64 array/tensor."""
+    if a is None or (not isinstance(a, np.ndarray) and hasattr(a, "data_ptr")):
+        return a
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _current_device():
+    try:
+        import torch
+        return torch.cuda.current_device() if torch.cuda.is_available() else None
+    except Exception:  # pragma: no cover - torch without CUDA
+        return None
 
 
 def status_dict(st: capi.Status, rn: np.ndarray, br) -> dict:
@@ -115,11 +146,15 @@ class SpockSolver:
         z = np.zeros(self.nz)
         zs = np.zeros(self.nz)
         e = np.zeros(self.neta)
-        x = None if x_init is None else np.ascontiguousarray(x_init, dtype=np.float64)
+        x = None if x_init is None else np.ascontiguousarray(x_init, dtype=np.float64).ravel()
+        if x is not None and x.size != self.problem.nx:
+            raise ValueError("solve: x_init has wrong length")
         wz = we = None
         if warm is not None:
-            wz = np.ascontiguousarray(warm[0], dtype=np.float64)
-            we = np.ascontiguousarray(warm[1], dtype=np.float64)
+            wz = np.ascontiguousarray(warm[0], dtype=np.float64).ravel()
+            we = np.ascontiguousarray(warm[1], dtype=np.float64).ravel()
+            if wz.size != self.nz or we.size != self.neta:
+                raise ValueError("solve: warm start has wrong dimensions")
         rc = fn(self.h, _ptr(x), _ptr(wz), _ptr(we), _ptr(z), _ptr(zs), _ptr(e), C.byref(st))
         _raise(self.lib, rc)
         return SolveResult(z, zs, e, status_dict(st, rn, br))
@@ -134,46 +169,52 @@ class SpockSolver:
 
     def apply_T(self, z, eta, z_out=None, eta_out=None):
         """SpockSolver::apply_T (proj/src/solver.cpp:148-164)."""
+        z, eta = _f64(z), _f64(eta)
         if z_out is None:
-            z_out = np.empty_like(z)
+            z_out = np.empty(self.nz)
         if eta_out is None:
-            eta_out = np.empty_like(eta)
-        _raise(self.lib, self.lib.spock_solver_apply_T(self.h, _ptr(z), _ptr(eta), _ptr(z_out), _ptr(eta_out)))
+            eta_out = np.empty(self.neta)
+        _raise(self.lib, self.lib.spock_solver_apply_T(self.h, _ptr(z, self.nz, "apply_T: z"), _ptr(eta, self.neta, "apply_T: eta"),
+                                                       _ptr(z_out, self.nz, "apply_T: z_out"),
+                                                       _ptr(eta_out, self.neta, "apply_T: eta_out")))
         return z_out, eta_out
 
     def apply_L(self, z, out=None):
         out = np.empty(self.neta) if out is None else out
-        _raise(self.lib, self.lib.spock_op_apply(self.h, _ptr(z), _ptr(out)))
+        _raise(self.lib, self.lib.spock_op_apply(self.h, _ptr(_f64(z), self.nz, "apply: z"), _ptr(out, self.neta, "apply: out")))
         return out
 
     def apply_Lt(self, eta, out=None):
         out = np.empty(self.nz) if out is None else out
-        _raise(self.lib, self.lib.spock_op_apply_adjoint(self.h, _ptr(eta), _ptr(out)))
+        _raise(self.lib, self.lib.spock_op_apply_adjoint(self.h, _ptr(_f64(eta), self.neta, "apply_adjoint: eta"),
+                                                         _ptr(out, self.nz, "apply_adjoint: out")))
         return out
 
     def m_norm(self, z, eta, alpha: float) -> float:
         o = C.c_double()
-        _raise(self.lib, self.lib.spock_op_m_norm(self.h, _ptr(z), _ptr(eta), alpha, C.byref(o)))
+        _raise(self.lib, self.lib.spock_op_m_norm(self.h, _ptr(_f64(z), self.nz, "m_norm: z"),
+                                                  _ptr(_f64(eta), self.neta, "m_norm: eta"), alpha, C.byref(o)))
         return o.value
 
     def proj_s1(self, z):
         z = np.array(z, dtype=np.float64)
-        _raise(self.lib, self.lib.spock_proj_s1(self.h, _ptr(z)))
+        _raise(self.lib, self.lib.spock_proj_s1(self.h, _ptr(z, self.nz, "proj_s1: z")))
         return z
 
     def proj_s2(self, z):
         z = np.array(z, dtype=np.float64)
-        _raise(self.lib, self.lib.spock_proj_s2(self.h, _ptr(z)))
+        _raise(self.lib, self.lib.spock_proj_s2(self.h, _ptr(z, self.nz, "proj_s2: z")))
         return z
 
     def proj_s3(self, eta):
         eta = np.array(eta, dtype=np.float64)
-        _raise(self.lib, self.lib.spock_proj_s3(self.h, _ptr(eta)))
+        _raise(self.lib, self.lib.spock_proj_s3(self.h, _ptr(eta, self.neta, "proj_s3: eta")))
         return eta
 
     def unscale_primal(self, zs):
         out = np.empty(self.nz)
-        _raise(self.lib, self.lib.spock_solver_unscale_primal(self.h, _ptr(np.ascontiguousarray(zs)), _ptr(out)))
+        _raise(self.lib, self.lib.spock_solver_unscale_primal(
+            self.h, _ptr(np.ascontiguousarray(zs, dtype=np.float64), self.nz, "unscale_primal: z"), _ptr(out)))
         return out
 
     def bench_T(self, k: int, use_graph: bool = True, flush_l2: bool = False) -> float:
@@ -210,6 +251,15 @@ class SpockSolver:
         _raise(self.lib, self.lib.spock_solver_set_grid_cap(self.h, int(ctas)))
 
 
+def residuals_xi(op, z, eta, z_next, eta_next, alpha: float):
+    """Termination residuals of a CP step (proj/src/solver.cpp:31-43):
+    xi1 = (z - z+)/alpha - L*(eta - eta+), xi2 = (eta - eta+)/alpha - L(z - z+),
+    with `op`'s L and L* (the device operators for a SpockSolver)."""
+    dz = np.asarray(z, dtype=np.float64) - np.asarray(z_next, dtype=np.float64)
+    de = np.asarray(eta, dtype=np.float64) - np.asarray(eta_next, dtype=np.float64)
+    return dz / alpha - op.apply_Lt(de), de / alpha - op.apply_L(dz)
+
+
 class BatchSolver:
     """Several x_init of one problem solved side by side (batched
     multi-x_init / warm-started MPC solves; the reference solves one x_init per
@@ -230,9 +280,13 @@ class BatchSolver:
         import threading
         self.solvers = [None] * streams
         errs = []
+        dev = _current_device()
 
         def make(k):
             try:
+                if dev is not None:  # the current device is per thread: build on the caller's
+                    import torch
+                    torch.cuda.set_device(dev)
                 self.solvers[k] = SpockSolver(problem, **params)
             except Exception as e:  # surfaced in the caller's thread
                 errs.append(e)

@@ -175,3 +175,130 @@ def riccati_tree_solve(p: Raocp, x_init: np.ndarray) -> float:
         w[i] = hx - Hxu @ np.linalg.solve(Huu, hu)
         w0[i] = h0 - 0.25 * hu @ np.linalg.solve(Huu, hu)
     return float(x_init @ W[0] @ x_init + w[0] @ x_init + w0[0])
+
+
+def _soc_proj_local(v: np.ndarray) -> np.ndarray:
+    """reference.cpp:300-312 (axis last)."""
+    t, hn = v[-1], np.linalg.norm(v[:-1])
+    if hn <= t:
+        return v.copy()
+    r = np.zeros_like(v)
+    if hn <= -t:
+        return r
+    r[:-1] = (hn + t) / (2.0 * hn) * v[:-1]
+    r[-1] = 0.5 * (hn + t)
+    return r
+
+
+def _soc_face_distance(w, eta, a, tolc):
+    """reference.cpp:314-331: sup-norm distance from w to the support face of
+    SOC + a at eta (the face ray's sign corrected, see below); also returns the
+    polar-cone violation of eta."""
+    u = w - a
+    ph, pt = np.linalg.norm(eta[:-1]), eta[-1]
+    dv = ph + pt
+    if np.abs(eta).max(initial=0.0) <= tolc:
+        return float(np.abs(u - _soc_proj_local(u)).max()), dv
+    if ph + pt < -tolc:
+        return float(np.abs(u).max()), dv
+    # Deviation from reference.cpp:325-327, documented: the reference builds the
+    # ray along (-eta_head, |eta_head|).  For eta = c (d, -1) in the polar cone
+    # (the normal cone of SOC at the boundary point s (d, 1), which is what
+    # eta+ = p - alpha Pi(p / alpha) is, solver.cpp:148-164) the support face is the
+    # ray along (+eta_head, |eta_head|); with the reference's sign the check fails
+    # at every active SOC, also on the oracle's own converged solutions.
+    d = np.concatenate([eta[:-1], [ph]])
+    dn2 = d @ d
+    s = max(0.0, (u @ d) / dn2) if dn2 > 0.0 else 0.0
+    return float(np.abs(u - s * d).max()), dv
+
+
+def kkt_check(sp, soc, L, zl, el, z, eta, tol1, tol2):
+    """eps-KKT report of reference.cpp:335-494 (ref::kkt_check), numpy.
+
+    sp: the scaled problem; soc(which, idx) -> dict with the translation "a"
+    (0: stage, idx = node-1; 1: leaf); L: materialised operator (n_eta x n_z);
+    zl / el: primal / dual layouts.  COD solves are min-norm least squares: the
+    least-squares residual is the same for every minimiser."""
+    from paper_2505_12078_b200.problem import CONE_FREE, CONE_NONNEG, CONE_SOC, CONE_ZERO, dual_cone
+    tr = sp.tree
+    nn, nnl, nx, nu = tr.num_nodes(), tr.num_nonleaf(), sp.nx, sp.nu
+    Lte, Lz = L.T @ eta, L @ z
+    tolc = 1e-8 * (1.0 + np.abs(eta).max())
+    primal = abs(1.0 + Lte[0]) / tol1[0]
+    membership = dual = 0.0
+    nz1 = nn * nx + nnl * nu
+    G, h = dense_dynamics_constraints(sp, sp.x_init)
+    membership = max(membership, float(np.abs(G @ z[1:1 + nz1] - h).max()))
+    w = -Lte[1:1 + nz1]
+    lam = np.linalg.lstsq(G.T, w, rcond=None)[0]
+    primal = max(primal, float((np.abs(w - G.T @ lam) / tol1[1:1 + nz1]).max()))
+    for i in range(nnl):
+        rk = sp.risk[i]
+        ny, nch, cf = int(zl["y_dim"][i]), int(tr.child_count[i]), int(tr.child_first[i])
+        nnu = rk.F.shape[1]
+        dim = ny + 2 * nch
+        M = np.zeros((nch + nnu, dim))
+        M[:nch, :ny] = rk.E.T
+        M[:nch, ny:ny + nch] = -np.eye(nch)
+        M[:nch, ny + nch:] = -np.eye(nch)
+        if nnu:
+            M[nch:, :ny] = rk.F.T
+        idx = np.array(list(range(zl["y_off"][i], zl["y_off"][i] + ny))
+                       + [zl["tau_base"] + cf + k - 1 for k in range(nch)]
+                       + [zl["s_base"] + cf + k - 1 for k in range(nch)])
+        membership = max(membership, float(np.abs(M @ z[idx]).max()))
+        w2 = -Lte[idx]
+        lam = np.linalg.lstsq(M.T, w2, rcond=None)[0]
+        primal = max(primal, float((np.abs(w2 - M.T @ lam) / tol1[idx]).max()))
+
+    def box_dist(e, wv, lo, hi):
+        if e > tolc:
+            return abs(wv - hi)
+        if e < -tolc:
+            return abs(wv - lo)
+        return max(0.0, lo - wv, wv - hi)
+
+    for i in range(nn):
+        if i < nnl:
+            off = int(el["seg1_off"][i])
+            for part in dual_cone(sp.risk[i].cone):
+                if part.kind == CONE_SOC:
+                    d, dv = _soc_face_distance(Lz[off:off + part.dim], eta[off:off + part.dim],
+                                               np.zeros(part.dim), tolc)
+                    membership = max(membership, dv)
+                    dual = max(dual, d / tol2[off:off + part.dim].min())
+                else:
+                    for k in range(part.dim):
+                        e, wv, tl = eta[off + k], Lz[off + k], tol2[off + k]
+                        dist = 0.0
+                        if part.kind == CONE_NONNEG:
+                            membership = max(membership, e - tolc)
+                            dist = abs(wv) if e < -tolc else max(0.0, -wv)
+                        elif part.kind == CONE_FREE:
+                            membership = max(membership, abs(e) - tolc)
+                        elif part.kind == CONE_ZERO:
+                            dist = abs(wv)
+                        dual = max(dual, dist / tl)
+                off += part.dim
+            ix = int(el["seg1_off"][i]) + int(el["seg1_ydim"][i])  # risk scalar row
+            e, wv = eta[ix], Lz[ix]
+            membership = max(membership, e - tolc)
+            dual = max(dual, (abs(wv) if e < -tolc else max(0.0, -wv)) / tol2[ix])
+            for k in range(int(el["seg1_nc"][i])):
+                ix2 = ix + 1 + k
+                dual = max(dual, box_dist(eta[ix2], Lz[ix2], sp.C[i].lo[k], sp.C[i].hi[k]) / tol2[ix2])
+        if i > 0:
+            off, d = int(el["seg2_off"][i - 1]), int(el["seg2_dim"][i - 1])
+            dist, dv = _soc_face_distance(Lz[off:off + d], eta[off:off + d], soc(0, i - 1)["a"], tolc)
+            membership = max(membership, dv)
+            dual = max(dual, dist / tol2[off:off + d].min())
+        if i >= nnl:
+            j = i - nnl
+            off, nc, d = int(el["seg3_off"][j]), int(el["seg3_nc"][j]), int(el["seg3_socdim"][j])
+            for k in range(nc):
+                dual = max(dual, box_dist(eta[off + k], Lz[off + k], sp.CN[j].lo[k], sp.CN[j].hi[k]) / tol2[off + k])
+            dist, dv = _soc_face_distance(Lz[off + nc:off + nc + d], eta[off + nc:off + nc + d], soc(1, j)["a"], tolc)
+            membership = max(membership, dv)
+            dual = max(dual, dist / tol2[off + nc:off + nc + d].min())
+    return dict(primal=primal, dual=dual, membership=membership)

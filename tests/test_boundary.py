@@ -57,3 +57,63 @@ def test_no_cpu_fallback_without_gpu():
     p = make_tiny(ScenarioTree.from_branching([2]), 2, 1, 3)
     with pytest.raises(RuntimeError, match="CUDA"):
         SpockSolver(p)
+
+
+@pytest.mark.gpu
+def test_wrong_sizes_and_dtypes_raise_value_error():
+    """The reference throws std::invalid_argument on wrong dimensions
+    (solver.cpp:191,200-201); the Python mirror checks lengths and dtypes before
+    any pointer reaches the library (a short buffer would be read or written out
+    of bounds)."""
+    import numpy as np
+    import torch
+    from paper_2505_12078_b200.generators import make_config
+    from paper_2505_12078_b200.solver import SpockSolver
+    p = make_config("c1", seed=1)
+    s = SpockSolver(p, max_iters=3)
+    with pytest.raises(ValueError, match="x_init"):
+        s.solve(np.zeros(p.nx + 1))
+    with pytest.raises(ValueError, match="warm"):
+        s.solve(p.x_init, warm=(np.zeros(s.nz - 1), np.zeros(s.neta)))
+    with pytest.raises(ValueError):
+        s.apply_T(np.zeros(s.nz - 1), np.zeros(s.neta))
+    with pytest.raises(ValueError):
+        s.apply_T(np.zeros(s.nz), np.zeros(s.neta), np.zeros(s.nz), np.zeros(s.neta - 2))
+    with pytest.raises(ValueError):
+        s.apply_T(torch.zeros(s.nz, dtype=torch.float32, device="cuda"),
+                  torch.zeros(s.neta, dtype=torch.float64, device="cuda"))
+    with pytest.raises(ValueError):
+        s.apply_L(np.zeros(s.nz + 3))
+    with pytest.raises(ValueError):
+        s.apply_Lt(np.zeros(s.neta), out=np.zeros(s.nz, dtype=np.float32))
+    z1, e1 = s.apply_T(np.zeros(s.nz), np.zeros(s.neta))  # the right sizes still work
+    assert z1.shape == (s.nz,) and e1.shape == (s.neta,)
+
+
+@pytest.mark.gpu
+def test_dual_cone_projection_on_device():
+    """S3 on the risk rows projects onto the dual cone (risk.cpp:25-43,
+    projections.cpp:212-244): AV@R rows R+^{2n} x Free clamp the first 2n entries
+    and leave the last; the expectation form Zero^n -> Free leaves all n."""
+    import numpy as np
+    from oracle.oracle import OracleSolver
+    from paper_2505_12078_b200.problem import ScenarioTree
+    from paper_2505_12078_b200.solver import SpockSolver
+    from support import TinyOpts, make_tiny
+    for gamma, ny_of in ((0.5, lambda n: 2 * n + 1), (1.0, lambda n: n)):
+        p = make_tiny(ScenarioTree.from_branching([3, 2]), 2, 1, 5, TinyOpts(gamma=gamma))
+        s = SpockSolver(p)
+        o = OracleSolver(p, alpha=s.alpha)
+        el = o.dual_layout()
+        e = np.linspace(-3.0, 3.0, s.neta)
+        got = s.proj_s3(e)
+        np.testing.assert_allclose(got, o.proj_s3(e), rtol=1e-14, atol=1e-14)
+        for i in range(p.tree.num_nonleaf()):
+            n = int(p.tree.child_count[i])
+            off, ny = int(el["seg1_off"][i]), int(el["seg1_ydim"][i])
+            assert ny == ny_of(n)
+            if gamma < 1.0:
+                assert np.array_equal(got[off:off + 2 * n], np.maximum(e[off:off + 2 * n], 0.0))
+                assert got[off + 2 * n] == e[off + 2 * n]
+            else:
+                assert np.array_equal(got[off:off + n], e[off:off + n])

@@ -300,3 +300,54 @@ def test_invalid_params_raise(impl):  # solver.cpp:9-19 error kinds
                 dict(max_iters=0)):
         with pytest.raises(ValueError):
             make_solver(impl, p, **bad)
+
+
+def test_termination_residuals(impl):  # test_solver.cpp:226-245
+    from paper_2505_12078_b200.solver import residuals_xi
+    p = make_tiny(ScenarioTree.from_branching([2]), 2, 1, 27)
+    s = make_solver(impl, p)
+    rng = Philox(28)
+    z, e = random_vec(rng, s.nz), random_vec(rng, s.neta)
+    x1, x2 = residuals_xi(s, z, e, z, e, 0.5)
+    assert np.abs(x1).max() == 0.0 and np.abs(x2).max() == 0.0
+    zn, en = random_vec(rng, s.nz), random_vec(rng, s.neta)
+    x1, x2 = residuals_xi(s, z, e, zn, en, 0.5)
+    h1, h2 = residuals_xi(s, z, e, zn, en, 0.25)
+    assert np.abs(h1 - (x1 + (z - zn) / 0.5)).max() < 1e-12
+    assert np.abs(h2 - (x2 + (e - en) / 0.5)).max() < 1e-12
+
+
+def test_epsilon_kkt_at_convergence(impl):  # test_solver.cpp:429-456, oracle reference.cpp:335-494
+    """The one check of a solver's solution that does not go through the oracle's
+    iteration: the eps-KKT inclusions of the scaled problem at (z, eta)."""
+    # Deviation, documented: with the restated make_tiny (Philox pinned by the
+    # published Random123 vectors, tests/test_kats.py) three of the reference's
+    # four instances draw |x_init| > 1 = the box half-width at the root, an
+    # infeasible problem on which neither SuperMann nor CP can converge (xi2
+    # stalls at exactly |x_init|_inf - 1).  They are skipped by that data-derived
+    # predicate, and further instances from a second seed stream keep >= 3 checks.
+    from support import kkt_check
+    checked = 0
+    cases = []
+    for seed in (36, 37):
+        rng = Philox(seed)
+        for tree in small_trees():
+            if tree.num_nodes() > 12:
+                continue
+            cases.append(make_tiny(tree, 2, 1, rng.next_u64(), TinyOpts(gamma=0.5, box_halfwidth=1.0)))
+    for p in cases:
+        if np.abs(p.x_init).max() > 1.0:
+            continue
+        s = make_solver(impl, p, eps_abs=1e-7, eps_rel=1e-7, max_iters=200000)
+        r = s.solve()
+        assert r.status["reason"] == "converged"
+        o = oracle.OracleSolver(p)
+        sp = _scaled_problem(o, p)
+        L = materialize(s.nz, s.apply_L)
+        rep = kkt_check(sp, o.soc, L, o.primal_layout(), o.dual_layout(), r.z_scaled, r.eta,
+                        np.full(s.nz, 10.0 * 1e-7), np.full(s.neta, 10.0 * 1e-7))
+        assert rep["primal"] <= 1.0, rep
+        assert rep["dual"] <= 1.0, rep
+        assert rep["membership"] < 1e-6, rep
+        checked += 1
+    assert checked >= 3
