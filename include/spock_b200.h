@@ -237,7 +237,9 @@ int spock_shard_masks(spock_solver* s, uint8_t* z_mask, uint8_t* eta_mask);
  * exchanges; every reduction over the rank's entries, completed by the host's
  * collectives on device buffers, enqueued on spock_solver_stream's stream:
  * op 0 all-gather of the n-double exchange buffer (equal slices per rank),
- * op 1 all-reduce sum, op 2 all-reduce max; return 0 on success).  Outputs
+ * op 1 all-reduce sum, op 2 all-reduce max, op 3 all-gather of n doubles per
+ * rank in place -- dev_buf holds world * n, this rank's at [rank n, (rank+1) n),
+ * used for the double-double Anderson Gram; return 0 on success).  Outputs
  * are valid on spock_shard_masks' entries. */
 typedef int (*spock_collective_fn)(void* user, int32_t op, double* dev_buf, int64_t n);
 /* spock_shard_weights: spock_shard_masks restricted to one rank per entry (the
@@ -246,6 +248,14 @@ typedef int (*spock_collective_fn)(void* user, int32_t op, double* dev_buf, int6
 int spock_shard_weights(spock_solver* s, uint8_t* z_w, uint8_t* eta_w);
 int spock_shard_set_collectives(spock_solver* s, spock_collective_fn fn, void* user);
 void* spock_solver_stream(const spock_solver* s);
+
+/* The least-squares step of AndersonAccelerator::direction
+ * (proj/src/solver.cpp:67-76: ColPivHouseholderQR(M_d).setThreshold(1e-12)
+ * .solve(r)) as the solver computes it on device: Gram M_d'M_d and M_d'r in
+ * double-double, column-pivoted Cholesky with Eigen's pivot order and rank
+ * rules (aa.cuh).  Host-only (no device needed): M_d column-major rows x cols,
+ * cols <= 64. */
+int spock_anderson_lstsq(const double* Md, int64_t rows, int32_t cols, const double* r, double* kappa);
 
 #ifdef __cplusplus
 }

@@ -64,6 +64,7 @@ def lib() -> C.CDLL:
         L.oracle_aa_create.restype = V
         L.oracle_aa_destroy.argtypes = [V]
         L.oracle_aa_direction.argtypes = [V, V, I, V]
+        L.oracle_colpiv_qr_solve.argtypes = [V, I, I, V, V]
         L.oracle_estimate_norm_identity.argtypes = [I]
         L.oracle_estimate_norm_identity.restype = D
         L.oracle_philox_normals.argtypes = [C.c_uint64, I, V]
@@ -284,6 +285,16 @@ class Anderson:
         if getattr(self, "h", None):
             self.L.oracle_aa_destroy(self.h)
             self.h = None
+
+
+def colpiv_qr_solve(A, b) -> np.ndarray:
+    """Eigen ColPivHouseholderQR(A).setThreshold(1e-12).solve(b) as restated
+    (orc_la.cpp; the reference's Anderson least squares, solver.cpp:73-75)."""
+    A = np.asfortranarray(A, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    x = np.zeros(A.shape[1])
+    lib().oracle_colpiv_qr_solve(A.ctypes.data, A.shape[0], A.shape[1], b.ctypes.data, x.ctypes.data)
+    return x
 
 
 def estimate_norm_identity(n: int) -> float:

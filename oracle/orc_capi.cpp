@@ -396,6 +396,15 @@ void oracle_aa_direction(void* a, const double* r, int n, double* psi) {
   Vec o = static_cast<Anderson*>(a)->direction(Vec(r, r + n));
   std::memcpy(psi, o.data(), sizeof(double) * n);
 }
+// The Anderson least squares alone (solver.cpp:73-75): Eigen's ColPivHouseholderQR
+// solve with threshold 1e-12 on a column-major rows x cols matrix
+void oracle_colpiv_qr_solve(const double* A, int rows, int cols, const double* b, double* x) {
+  Mat M(rows, cols);
+  for (int c = 0; c < cols; ++c)
+    for (int i = 0; i < rows; ++i) M(i, c) = A[size_t(c) * rows + i];
+  const Vec k = colpiv_qr_solve(M, Vec(b, b + rows), 1e-12);
+  std::memcpy(x, k.data(), sizeof(double) * cols);
+}
 // Power iteration on an identity operator of size n (test_oper.cpp:159-163)
 double oracle_estimate_norm_identity(int n) {
   auto ident = [](const Vec& v, Vec& o) { o = v; };

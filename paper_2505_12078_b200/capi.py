@@ -240,6 +240,7 @@ def load_library() -> C.CDLL:
     lib.spock_solver_set_grid_cap.argtypes = [C.c_void_p, C.c_int32]
     lib.spock_solver_grid.argtypes = [C.c_void_p]
     lib.spock_solver_grid.restype = C.c_int32
+    lib.spock_anderson_lstsq.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p]
     _LIB = lib
     return lib
 
@@ -251,5 +252,19 @@ EXPORTED_SYMBOLS = [
     "spock_proj_s1", "spock_proj_s2", "spock_proj_s3", "spock_solver_unscale_primal", "spock_bench_T",
     "spock_bench_kernels", "spock_traffic_model", "spock_solver_t_path", "spock_shard_setup", "spock_shard_apply_T",
     "spock_shard_bench", "spock_shard_masks", "spock_shard_weights", "spock_shard_set_collectives",
-    "spock_solver_stream", "spock_solver_set_grid_cap", "spock_solver_grid",
+    "spock_solver_stream", "spock_solver_set_grid_cap", "spock_solver_grid", "spock_anderson_lstsq",
 ]
+
+
+def anderson_lstsq(Md, r):
+    """The solver's Anderson least squares (spock_anderson_lstsq): kappa =
+    argmin ||M_d kappa - r|| with the reference's rank rules, double-double Gram."""
+    import numpy as np
+    lib = load_library()
+    A = np.asfortranarray(Md, dtype=np.float64)
+    b = np.ascontiguousarray(r, dtype=np.float64)
+    k = np.zeros(A.shape[1])
+    rc = lib.spock_anderson_lstsq(A.ctypes.data, A.shape[0], A.shape[1], b.ctypes.data, k.ctypes.data)
+    if rc != SPOCK_OK:
+        raise ValueError(lib.spock_last_error().decode())
+    return k

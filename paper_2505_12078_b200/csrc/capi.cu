@@ -4,6 +4,7 @@
 // -> SPOCK_ERUNTIME, CUDA failures -> SPOCK_ECUDA.
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "../../include/spock_b200.h"
 #include "engine.hpp"
@@ -259,6 +260,27 @@ const char* spock_solver_t_path(const spock_solver* s) { return (s && s->eng) ? 
 int spock_solver_set_grid_cap(spock_solver* s, int32_t ctas) {
   if (int rc = check(s)) return rc;
   return guard([&] { s->eng->set_grid_cap(ctas); });
+}
+
+int spock_anderson_lstsq(const double* Md, int64_t rows, int32_t cols, const double* r, double* kappa) {
+  return guard([&] {
+    if (!Md || !r || !kappa || rows < 1 || cols < 1 || cols > spock::kAaHostMax)
+      throw std::invalid_argument("spock_anderson_lstsq: bad arguments");
+    std::vector<spock::dd> G(size_t(cols) * cols, spock::dd{0.0, 0.0}), g(size_t(cols), spock::dd{0.0, 0.0});
+    for (int a = 0; a < cols; ++a) {
+      const double* x = Md + size_t(a) * rows;
+      for (int b = a; b < cols; ++b) {
+        const double* y = Md + size_t(b) * rows;
+        spock::dd s{0.0, 0.0};
+        for (int64_t i = 0; i < rows; ++i) s = spock::dd_fma(s, x[i], y[i]);
+        G[a + size_t(b) * cols] = G[b + size_t(a) * cols] = s;
+      }
+      spock::dd s{0.0, 0.0};
+      for (int64_t i = 0; i < rows; ++i) s = spock::dd_fma(s, x[i], r[i]);
+      g[a] = s;
+    }
+    spock::aa_kappa_dd<spock::kAaHostMax>(G.data(), g.data(), cols, rows, kappa);
+  });
 }
 
 int32_t spock_solver_grid(const spock_solver* s) { return (s && s->eng) ? s->eng->fused_grid() : 0; }

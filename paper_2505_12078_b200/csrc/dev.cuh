@@ -29,7 +29,10 @@ inline int smem_optin_max() {
   return v;
 }
 inline cudaError_t set_smem_limit(const void* f, int need) {
-  const int mx = smem_optin_max();
+  cudaFuncAttributes fa{};
+  const cudaError_t e = cudaFuncGetAttributes(&fa, f);
+  if (e != cudaSuccess) return e;
+  const int mx = smem_optin_max() - int(fa.sharedSizeBytes);  // dynamic + static <= opt-in
   if (need > mx) return cudaErrorInvalidValue;
   return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
 }

@@ -7,6 +7,7 @@
 //   Engine::T            <- SpockSolver::apply_T       proj/src/solver.cpp:148-164
 //   Engine::solve_b      <- SpockSolver::run           proj/src/solver.cpp:189-350
 #include "engine.hpp"
+#include "aa.cuh"
 
 #include <chrono>
 #include <climits>
@@ -54,7 +55,7 @@ void Params::validate() const {  // proj/src/solver.cpp:9-19
     throw std::invalid_argument("SpockParams: beta, sigma must be in (0, 1)");
   if (lambda <= 0.0 || lambda >= 2.0) throw std::invalid_argument("SpockParams: lambda must be in (0, 2)");
   if (max_iters < 1 || max_backtracks < 1) throw std::invalid_argument("SpockParams: bad iteration caps");
-  if (aa_memory > 15) throw std::invalid_argument("SpockParams: aa_memory above 15 is not supported on device");
+  if (aa_memory > kAaHostMax) throw std::invalid_argument("SpockParams: aa_memory above 64 is not supported on device");
 }
 
 template <class Ty>
@@ -877,6 +878,49 @@ void Engine::shard_set_collectives(CollFn fn, void* user) {
   shard_.coll_user = user;
 }
 
+// Host-loop Gram of the Anderson difference history by position (newest 0),
+// double-double: shift every entry one position, then row / column 0 from this
+// iteration's update dots (launch_gram_dd, chunks of kLoopMaxMem columns:
+// [<dnew, D_b> | <D_b, r>] as (hi, lo) pairs per chunk).  Sharded: the ranks'
+// partial sums are all-gathered and added in rank order, so the double-double
+// precision survives the cross-rank sum (an all-reduce of hi and lo would not).
+void Engine::gram_update(int cols, bool sharded) {
+  const int n = 4 * cols;
+  const double* src = gram_out_;
+  int G = 1;
+  if (sharded && shard_.coll && shard_.G > 1) {
+    G = shard_.G;
+    if (!gram_gather_) gram_gather_ = dalloc<double>(size_t(G) * 4 * kAaHostMax);
+    CK(cudaMemcpyAsync(gram_gather_ + size_t(shard_.rank) * n, gram_out_, sizeof(double) * n,
+                       cudaMemcpyDeviceToDevice, st_));
+    coll(3, gram_gather_, n);
+    src = gram_gather_;
+  }
+  std::vector<double> h(size_t(G) * n);
+  CK(cudaMemcpyAsync(h.data(), src, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, st_));
+  sync();
+  std::vector<dd> nd(cols, dd{0.0, 0.0}), rd(cols, dd{0.0, 0.0});
+  for (int g = 0; g < G; ++g) {
+    const double* q = h.data() + size_t(g) * n;
+    for (int c0 = 0; c0 < cols; c0 += kLoopMaxMem) {
+      const int cc = std::min(kLoopMaxMem, cols - c0);
+      const double* z = q + 4 * c0;
+      for (int b = 0; b < cc; ++b) {
+        nd[c0 + b] = dd_add(nd[c0 + b], dd{z[2 * b], z[2 * b + 1]});
+        rd[c0 + b] = dd_add(rd[c0 + b], dd{z[2 * (cc + b)], z[2 * (cc + b) + 1]});
+      }
+    }
+  }
+  constexpr int K = kAaHostMax;
+  const int m = prm_.aa_memory;
+  for (int a = m - 1; a >= 1; --a)
+    for (int b = m - 1; b >= 1; --b) gram_h_[a + b * K] = gram_h_[(a - 1) + (b - 1) * K];
+  for (int b = 0; b < cols; ++b) {
+    gram_h_[b * K] = gram_h_[b] = nd[b];
+    gram_r_[b] = rd[b];
+  }
+}
+
 // Cancellation of a sharded solve is a collective decision: each rank polls its
 // own callback and the ranks all-reduce the flags with MAX, so either every rank
 // stops at this iteration or none does (a lone rank leaving would strand the
@@ -884,12 +928,12 @@ void Engine::shard_set_collectives(CollFn fn, void* user) {
 bool Engine::agree_cancel(bool mine) {
   if (!shard_solving_ || !shard_.coll || shard_.G == 1) return mine;
   if (!cancel_dev_) cancel_dev_ = dalloc<double>(1);
-  host_red_[255] = mine ? 1.0 : 0.0;
-  CK(cudaMemcpyAsync(cancel_dev_, host_red_ + 255, sizeof(double), cudaMemcpyHostToDevice, st_));
+  host_red_[511] = mine ? 1.0 : 0.0;
+  CK(cudaMemcpyAsync(cancel_dev_, host_red_ + 511, sizeof(double), cudaMemcpyHostToDevice, st_));
   coll(2, cancel_dev_, 1);
-  CK(cudaMemcpyAsync(host_red_ + 255, cancel_dev_, sizeof(double), cudaMemcpyDeviceToHost, st_));
+  CK(cudaMemcpyAsync(host_red_ + 511, cancel_dev_, sizeof(double), cudaMemcpyDeviceToHost, st_));
   sync();
-  return host_red_[255] != 0.0;
+  return host_red_[511] != 0.0;
 }
 
 void Engine::coll(int op, double* buf, int64_t n) {
@@ -1451,8 +1495,12 @@ void Engine::upload() {
     d2_ = dupload(d2);
   }
   partial_ = dalloc<double>(size_t(4) * kRedRegion);
-  red_out_ = dalloc<double>(256);
-  CK(cudaMallocHost(&host_red_, 256 * sizeof(double)));
+  red_out_ = dalloc<double>(512);
+  gram_partial_ = dalloc<double>(size_t(kGramRegion));
+  gram_out_ = dalloc<double>(size_t(4 * kAaHostMax));
+  gram_h_.assign(size_t(kAaHostMax) * kAaHostMax, dd{0.0, 0.0});
+  gram_r_.assign(size_t(kAaHostMax), dd{0.0, 0.0});
+  CK(cudaMallocHost(&host_red_, 512 * sizeof(double)));
   for (int t = 0; t < 3; ++t) {
     scratch_z_[t] = dalloc<double>(lay_.nz);
     scratch_e_[t] = dalloc<double>(lay_.neta);
@@ -1923,54 +1971,6 @@ void Engine::unscale_b(const double* zs, double* z) {  // solver.cpp:116-130
 }
 
 // ---------------------------------------------------------------------------
-// Anderson least squares min ||M_d kappa - r|| from the Gram matrix G = M_d'M_d
-// and gr = M_d'r: column-pivoted Cholesky of G is the R factor of the
-// column-pivoted QR of M_d (same pivot order: largest remaining column norm),
-// and R' c = P'gr gives c = Q'r.  Pivots at or below 64 eps of the largest
-// Gram diagonal are treated as zero (the Gram form cannot resolve the QR's
-// 1e-12 threshold below sqrt(eps)); the remaining ones use the reference's
-// 1e-12 relative threshold (solver.cpp:73-75).  R is indexed by original column.
-std::vector<double> aa_kappa(const std::vector<double>& G, const std::vector<double>& gr, int cols) {
-  std::vector<int> piv(cols);
-  for (int a = 0; a < cols; ++a) piv[a] = a;
-  std::vector<double> W = G, Rm(size_t(cols) * cols, 0.0), cv(cols, 0.0);
-  auto R = [&](int s, int c) -> double& { return Rm[size_t(s) + size_t(c) * cols]; };
-  double maxd = 0.0;
-  for (int a = 0; a < cols; ++a) maxd = std::max(maxd, G[a + a * cols]);
-  const double floor_rel = 64.0 * std::numeric_limits<double>::epsilon();
-  int rank = 0;
-  double maxpiv = 0.0;
-  for (int t = 0; t < cols; ++t) {
-    int best = t;
-    for (int a = t + 1; a < cols; ++a)
-      if (W[piv[a] + piv[a] * cols] > W[piv[best] + piv[best] * cols]) best = a;
-    std::swap(piv[t], piv[best]);
-    const int pt = piv[t];
-    const double dd = W[pt + pt * cols];
-    if (!(dd > floor_rel * maxd)) break;
-    const double rkk = std::sqrt(dd);
-    R(t, pt) = rkk;
-    maxpiv = std::max(maxpiv, rkk);
-    for (int a = t + 1; a < cols; ++a) R(t, piv[a]) = W[pt + piv[a] * cols] / rkk;
-    double ct = gr[pt];
-    for (int s = 0; s < t; ++s) ct -= R(s, pt) * cv[s];
-    cv[t] = ct / rkk;
-    for (int a = t + 1; a < cols; ++a)
-      for (int b = t + 1; b < cols; ++b) W[piv[a] + piv[b] * cols] -= R(t, piv[a]) * R(t, piv[b]);
-    ++rank;
-  }
-  int np = 0;
-  for (int t = 0; t < rank; ++t) np += (R(t, piv[t]) > 1e-12 * maxpiv) ? 1 : 0;
-  std::vector<double> kap(cols, 0.0);
-  for (int t = np - 1; t >= 0; --t) {
-    double s = cv[t];
-    for (int a = t + 1; a < np; ++a) s -= R(t, piv[a]) * kap[piv[a]];
-    kap[piv[t]] = s / R(t, piv[t]);
-  }
-  return kap;
-}
-
-// ---------------------------------------------------------------------------
 // Device-resident loop (loop.cu): one CUDA graph per solve.
 //   WHILE(h_loop) {
 //     L*(r_eta), xi norms, [history push, Gram]      -> k_begin (termination,
@@ -2139,7 +2139,7 @@ void Engine::build_loop_graph(GraphLoop& G, bool supermann) {
     launch_xi(X, partial_ + kRedRegion, red_out_ + 4, st_);
     if (supermann) {
       loop_push(A, st_);
-      loop_gram(A, partial_ + 2 * kRedRegion, red_out_ + 8, st_);
+      loop_gram(A, gram_partial_, red_out_ + 8, st_);
     }
     loop_begin(A, st_);
     if (supermann) loop_psi(A, st_);
@@ -2289,6 +2289,8 @@ void Engine::solve_b(const double* x_init, const double* wz, const double* we, d
   };
   int aa_k = 0;  // Anderson call counter
   int aa_cols = 0;
+  std::fill(gram_h_.begin(), gram_h_.end(), dd{0.0, 0.0});
+  std::fill(gram_r_.begin(), gram_r_.end(), dd{0.0, 0.0});
   try {
     refresh(V, TV, R, Lrz);
     queue_mnorm(R, Lrz, 0);
@@ -2304,8 +2306,8 @@ void Engine::solve_b(const double* x_init, const double* wz, const double* we, d
       X.alpha = alpha;
       if (sharded) X.w[0] = shard_.mz, X.w[1] = shard_.me;
       launch_xi(X, partial_ + kRedRegion, red_out_ + 4, st_);
-      // Anderson push (solver.cpp:57-63) and Gram of the differences
-      int ngram = 0;
+      // Anderson push (solver.cpp:57-63) and the Gram update of the newest
+      // difference in double-double (aa.cuh; Gram kept by history position)
       if (supermann) {
         std::rotate(RH.begin(), RH.end() - 1, RH.end());
         std::rotate(DH.begin(), DH.end() - 1, DH.end());
@@ -2315,30 +2317,20 @@ void Engine::solve_b(const double* x_init, const double* wz, const double* we, d
         else
           launch_axpby(int(nv), 1.0, RH[0], -1.0, RH[1], DH[0], st_);
         aa_cols = std::min(aa_cols + 1, m);
-        if (aa_k > m) {
-          // Gram of the differences and M_d' r, in chunks of kMaxDots dots
-          std::vector<std::pair<const double*, const double*>> prs;
-          for (int a = 0; a < aa_cols; ++a)
-            for (int b = a; b < aa_cols; ++b) prs.push_back({DH[a], DH[b]});
-          for (int a = 0; a < aa_cols; ++a) prs.push_back({DH[a], R});
-          for (size_t c0 = 0; c0 < prs.size(); c0 += kMaxDots) {
-            DotArgs A{};
-            int j = 0;
-            for (size_t q = c0; q < prs.size() && j < kMaxDots; ++q, ++j) {
-              A.x[j] = prs[q].first, A.y[j] = prs[q].second, A.n[j] = int(nv), A.w[j] = w_v;
-            }
-            A.ndots = j;
-            launch_dots(A, partial_ + 2 * kRedRegion, red_out_ + 8 + c0, st_);
-          }
-          ngram = int(prs.size());
+        for (int c0 = 0; c0 < aa_cols; c0 += kLoopMaxMem) {
+          GramArgs A{};
+          A.dnew = DH[0], A.r = R, A.w = w_v, A.n = nv;
+          A.cols = std::min(kLoopMaxMem, aa_cols - c0);
+          for (int b = 0; b < A.cols; ++b) A.D[b] = DH[c0 + b];
+          launch_gram_dd(A, gram_partial_, gram_out_ + 4 * c0, st_);
         }
       }
       if (sharded) {  // this iteration's fresh partials, summed (max for xi) over the ranks
         if (!have_omega) coll(1, red_out_, 3);
         coll(2, red_out_ + 4, 2);
-        if (ngram) coll(1, red_out_ + 8, ngram);
       }
-      fetch(8 + ngram);
+      fetch(8);
+      if (supermann) gram_update(aa_cols, sharded);
       if (!have_omega) {
         omega = mnorm_of(host_red_);
         have_omega = true;
@@ -2388,15 +2380,11 @@ void Engine::solve_b(const double* x_init, const double* wz, const double* we, d
         // kappa = argmin ||M_d kappa - r|| by column-pivoted Cholesky of the
         // Gram matrix (the R factor of a column-pivoted QR of M_d)
         const int cols = aa_cols;
-        std::vector<double> G(cols * cols), gr(cols);
-        int j = 0;
+        std::vector<dd> G(size_t(cols) * cols);
         for (int a = 0; a < cols; ++a)
-          for (int b = a; b < cols; ++b) {
-            G[a + b * cols] = G[b + a * cols] = host_red_[8 + j];
-            ++j;
-          }
-        for (int a = 0; a < cols; ++a) gr[a] = host_red_[8 + j++];
-        const std::vector<double> kap = aa_kappa(G, gr, cols);
+          for (int b = 0; b < cols; ++b) G[a + b * cols] = gram_h_[a + b * kAaHostMax];
+        std::vector<double> kap(cols);
+        aa_kappa_dd<kAaHostMax>(G.data(), gram_r_.data(), cols, nv, kap.data());
         // psi = -r - sum_j kappa_j (M_r - M_d)_j, (M_r - M_d)_j = r_{k-1-j} = RH[j+1]
         LinCombArgs A{};
         A.x[0] = R;

@@ -10,6 +10,7 @@
 #include <string>
 #include <vector>
 
+#include "aa.cuh"
 #include "dev.cuh"
 #include "fused.hpp"
 #include "kernels.hpp"
@@ -207,6 +208,11 @@ class Engine {
   std::vector<WRec> lrecs_h_, ltrecs_h_;
   void coll(int op, double* buf, int64_t n);
   bool agree_cancel(bool mine);
+  void gram_update(int cols, bool sharded);
+  double* gram_partial_ = nullptr;  // block partials of the double-double Gram update
+  double* gram_out_ = nullptr;      // its (hi, lo) results (host loop)
+  double* gram_gather_ = nullptr;   // sharded: every rank's results
+  std::vector<dd> gram_h_, gram_r_;  // host loop: Gram by history position, M_d' r
   double* cancel_dev_ = nullptr;
   void shard_T(const double* z, const double* eta, double* zo, double* eo);
   void shard_L(const double* z, double* eta);

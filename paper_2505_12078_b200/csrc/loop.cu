@@ -15,9 +15,12 @@
 
 #include "../../include/spock_b200.h"
 #include "kernels.hpp"
+#include "aa.cuh"
 #include "loop.hpp"
 
 namespace spock {
+
+static_assert(kGramRegion == 4 * kLoopMaxMem * kRedBlocks + 2, "Gram partial region");
 
 namespace {
 
@@ -26,50 +29,6 @@ __device__ __forceinline__ void set_cond(unsigned long long h, unsigned int v) {
 }
 
 __device__ __forceinline__ int ring(int i, int n) { return ((i % n) + n) % n; }
-
-// Anderson least squares from the Gram matrix by column-pivoted Cholesky (the
-// R factor of the column-pivoted QR of M_d), as Engine's host aa_kappa.
-__device__ void aa_kappa_dev(const double* G, const double* gr, int cols, double* kap) {
-  constexpr int M = kLoopMaxMem;
-  int piv[M];
-  double W[M * M], Rm[M * M], cv[M];
-  for (int a = 0; a < cols; ++a) piv[a] = a;
-  for (int e = 0; e < cols * cols; ++e) W[e] = G[e], Rm[e] = 0.0;
-  double maxd = 0.0;
-  for (int a = 0; a < cols; ++a) maxd = fmax(maxd, G[a + a * cols]);
-  const double floor_rel = 64.0 * 2.220446049250313e-16;
-  int rank = 0;
-  double maxpiv = 0.0;
-  for (int t = 0; t < cols; ++t) {
-    int best = t;
-    for (int a = t + 1; a < cols; ++a)
-      if (W[piv[a] + piv[a] * cols] > W[piv[best] + piv[best] * cols]) best = a;
-    const int tmp = piv[t];
-    piv[t] = piv[best];
-    piv[best] = tmp;
-    const int pt = piv[t];
-    const double dd = W[pt + pt * cols];
-    if (!(dd > floor_rel * maxd)) break;
-    const double rkk = sqrt(dd);
-    Rm[t + pt * cols] = rkk;
-    maxpiv = fmax(maxpiv, rkk);
-    for (int a = t + 1; a < cols; ++a) Rm[t + piv[a] * cols] = W[pt + piv[a] * cols] / rkk;
-    double ct = gr[pt];
-    for (int s = 0; s < t; ++s) ct -= Rm[s + pt * cols] * cv[s];
-    cv[t] = ct / rkk;
-    for (int a = t + 1; a < cols; ++a)
-      for (int b = t + 1; b < cols; ++b) W[piv[a] + piv[b] * cols] -= Rm[t + piv[a] * cols] * Rm[t + piv[b] * cols];
-    ++rank;
-  }
-  int np = 0;
-  for (int t = 0; t < rank; ++t) np += (Rm[t + piv[t] * cols] > 1e-12 * maxpiv) ? 1 : 0;
-  for (int a = 0; a < cols; ++a) kap[a] = 0.0;
-  for (int t = np - 1; t >= 0; --t) {
-    double s = cv[t];
-    for (int a = t + 1; a < np; ++a) s -= Rm[t + piv[a] * cols] * kap[piv[a]];
-    kap[piv[t]] = s / Rm[t + piv[t] * cols];
-  }
-}
 
 // history push for iteration k (solver.cpp:57-63): newest slot hn = h + 1
 __global__ void k_push(const __grid_constant__ LoopArgs A) {
@@ -86,53 +45,101 @@ __global__ void k_push(const __grid_constant__ LoopArgs A) {
   }
 }
 
-// Gram of the difference columns and M_d' r: pairs (a <= b) row-major, then a
-__global__ void __launch_bounds__(kRedThreads) k_gram(const __grid_constant__ LoopArgs A, double* __restrict__ partial,
-                                                      double* out) {
-  constexpr int MD = kLoopMaxMem * (kLoopMaxMem + 1) / 2 + kLoopMaxMem;
-  __shared__ double sm[MD][kRedThreads / 32];
-  const LoopState& S = *A.st;
-  const int m = A.P.m, hn = S.h + 1, cols = min(S.aa_cols + 1, m);
-  const double* X[MD];
-  const double* Y[MD];
-  int nd = 0;
-  for (int a = 0; a < cols; ++a)
-    for (int b = a; b < cols; ++b) {
-      X[nd] = A.DH[ring(hn - a, m)];
-      Y[nd] = A.DH[ring(hn - b, m)];
-      ++nd;
-    }
-  for (int a = 0; a < cols; ++a) {
-    X[nd] = A.DH[ring(hn - a, m)];
-    Y[nd] = A.R;
-    ++nd;
-  }
-  double acc[MD];
+// Gram update of the Anderson history in double-double (aa.cuh): per thread,
+// error-free products accumulated by two-sum; per block, a fixed-order warp and
+// warp-to-warp reduction; the last block to arrive sums the block partials in
+// block order.  Outputs (hi, lo) of <dnew, D[b]> (b < cols), then <D[b], r>.
+__device__ __forceinline__ dd warp_sum_dd(dd v) {
 #pragma unroll
-  for (int j = 0; j < MD; ++j) acc[j] = 0.0;
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < A.nv; i += stride) {
-#pragma unroll
-    for (int j = 0; j < MD; ++j)
-      if (j < nd) acc[j] += X[j][i] * Y[j][i];
+  for (int o = 16; o > 0; o >>= 1) {
+    const dd u = {__shfl_xor_sync(0xffffffffu, v.hi, o), __shfl_xor_sync(0xffffffffu, v.lo, o)};
+    v = (threadIdx.x & o) ? dd_add(u, v) : dd_add(v, u);  // same operand order on both lanes
   }
-  const int w = threadIdx.x >> 5;
-#pragma unroll
-  for (int j = 0; j < MD; ++j) {
-    double v = acc[j];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if ((threadIdx.x & 31) == 0) sm[j][w] = v;
-  }
-  __syncthreads();
-  if (threadIdx.x < MD) {
-    double s = 0.0;
-    for (int k = 0; k < kRedThreads / 32; ++k) s += sm[threadIdx.x][k];
-    partial[size_t(threadIdx.x) * gridDim.x + blockIdx.x] = s;
-  }
-  grid_finalize<false>(partial, MD, out, red_counter(partial));
+  return v;
 }
 
+__device__ void gram_dd_body(const double* __restrict__ dnew, const double* __restrict__ r,
+                             const double* const* D, const double* __restrict__ w, int cols, int64_t n,
+                             double* __restrict__ partial, double* out) {
+  constexpr int M = kLoopMaxMem;
+  constexpr int NW = kRedThreads / 32;
+  __shared__ double sh[2 * M][NW], sl[2 * M][NW];
+  __shared__ int last;
+  dd acc[2 * M];
+#pragma unroll
+  for (int j = 0; j < 2 * M; ++j) acc[j] = {0.0, 0.0};
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += stride) {
+    double x = dnew[i], rr = r[i];
+    if (w) {
+      const double wi = w[i];
+      x *= wi;
+      rr *= wi;
+    }
+#pragma unroll
+    for (int b = 0; b < M; ++b)
+      if (b < cols) {
+        const double db = D[b][i];
+        acc[b] = dd_fma(acc[b], x, db);
+        acc[M + b] = dd_fma(acc[M + b], db, rr);
+      }
+  }
+  const int wp = threadIdx.x >> 5, nd = 2 * cols;
+#pragma unroll
+  for (int j = 0; j < 2 * M; ++j) {
+    const dd v = warp_sum_dd(acc[j]);
+    if ((threadIdx.x & 31) == 0) sh[j][wp] = v.hi, sl[j][wp] = v.lo;
+  }
+  __syncthreads();
+  const int nb = gridDim.x;
+  if (threadIdx.x < nd) {
+    const int j = threadIdx.x < cols ? threadIdx.x : M + threadIdx.x - cols;
+    dd s = {sh[j][0], sl[j][0]};
+    for (int k = 1; k < NW; ++k) s = dd_add(s, {sh[j][k], sl[j][k]});
+    partial[size_t(2 * threadIdx.x) * nb + blockIdx.x] = s.hi;
+    partial[size_t(2 * threadIdx.x + 1) * nb + blockIdx.x] = s.lo;
+  }
+  // last block: partials in block order (thread-strided, warp tree, warps in order)
+  unsigned int* counter = reinterpret_cast<unsigned int*>(partial + size_t(4 * M) * kRedBlocks);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == unsigned(nb - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int j = 0; j < nd; ++j) {
+    dd s = {0.0, 0.0};
+    for (int k = threadIdx.x; k < nb; k += blockDim.x)
+      s = dd_add(s, {__ldcg(partial + size_t(2 * j) * nb + k), __ldcg(partial + size_t(2 * j + 1) * nb + k)});
+    s = warp_sum_dd(s);
+    if ((threadIdx.x & 31) == 0) sh[0][wp] = s.hi, sl[0][wp] = s.lo;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      dd o = {sh[0][0], sl[0][0]};
+      for (int k = 1; k < NW; ++k) o = dd_add(o, {sh[0][k], sl[0][k]});
+      out[2 * j] = o.hi;
+      out[2 * j + 1] = o.lo;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *counter = 0u;
+}
+
+// graph loop: the history columns come from the device ring (head hn = h + 1)
+__global__ void __launch_bounds__(kRedThreads) k_gram(const __grid_constant__ LoopArgs A, double* __restrict__ partial,
+                                                      double* out) {
+  const LoopState& S = *A.st;
+  const int m = A.P.m, hn = S.h + 1, cols = min(S.aa_cols + 1, m);
+  const double* D[kLoopMaxMem];
+#pragma unroll
+  for (int b = 0; b < kLoopMaxMem; ++b) D[b] = A.DH[ring(hn - min(b, cols - 1), m)];
+  gram_dd_body(D[0], A.R, D, nullptr, cols, A.nv, partial, out);
+}
+
+__global__ void __launch_bounds__(kRedThreads) k_gram_args(const __grid_constant__ GramArgs G, double* __restrict__ partial,
+                                                           double* out) {
+  gram_dd_body(G.dnew, G.r, G.D, G.w, G.cols, G.n, partial, out);
+}
 
 // top of iteration k (solver.cpp:233-290): M-norm, xi thresholds, termination,
 // Anderson direction coefficients, K0 test; selects the branch body
@@ -189,17 +196,26 @@ __global__ void k_begin(const __grid_constant__ LoopArgs A) {
   const int kk = S.aa_k++;
   S.cpsi[0] = -1.0;
   S.ncpsi = 1;
+  // Gram ring update: row / column of the newest difference (slot of head h)
+  const int cols = S.aa_cols, m = P.m, s0 = ring(S.h, m);
+  for (int b = 0; b < cols; ++b) {
+    const int sb = ring(S.h - b, m);
+    const double hi = red[8 + 2 * b], lo = red[8 + 2 * b + 1];
+    S.gh[s0 + sb * kLoopMaxMem] = S.gh[sb + s0 * kLoopMaxMem] = hi;
+    S.gl[s0 + sb * kLoopMaxMem] = S.gl[sb + s0 * kLoopMaxMem] = lo;
+  }
   if (kk > P.m) {
-    const int cols = S.aa_cols;
-    double G[kLoopMaxMem * kLoopMaxMem], gr[kLoopMaxMem], kap[kLoopMaxMem];
-    int j = 0;
-    for (int a = 0; a < cols; ++a)
-      for (int b = a; b < cols; ++b) {
-        G[a + b * cols] = G[b + a * cols] = red[8 + j];
-        ++j;
+    dd G[kLoopMaxMem * kLoopMaxMem], gr[kLoopMaxMem];
+    double kap[kLoopMaxMem];
+    for (int a = 0; a < cols; ++a) {
+      const int sa = ring(S.h - a, m);
+      for (int b = 0; b < cols; ++b) {
+        const int sb = ring(S.h - b, m);
+        G[a + b * cols] = {S.gh[sa + sb * kLoopMaxMem], S.gl[sa + sb * kLoopMaxMem]};
       }
-    for (int a = 0; a < cols; ++a) gr[a] = red[8 + j++];
-    aa_kappa_dev(G, gr, cols, kap);
+      gr[a] = {red[8 + 2 * (cols + a)], red[8 + 2 * (cols + a) + 1]};
+    }
+    aa_kappa_dd<kLoopMaxMem>(G, gr, cols, A.nv, kap);
     for (int c = 0; c < cols; ++c) S.cpsi[c + 1] = -kap[c];
     S.ncpsi = cols + 1;
   }
@@ -342,6 +358,9 @@ inline int vec_blocks(int64_t n) { return int(std::min<int64_t>((n + 255) / 256,
 void loop_push(const LoopArgs& A, cudaStream_t st) { k_push<<<vec_blocks(A.nv), 256, 0, st>>>(A); }
 void loop_gram(const LoopArgs& A, double* partial, double* out, cudaStream_t st) {
   k_gram<<<kRedBlocks, kRedThreads, 0, st>>>(A, partial, out);
+}
+void launch_gram_dd(const GramArgs& A, double* partial, double* out, cudaStream_t st) {
+  k_gram_args<<<kRedBlocks, kRedThreads, 0, st>>>(A, partial, out);
 }
 void loop_begin(const LoopArgs& A, cudaStream_t st) { k_begin<<<1, 1, 0, st>>>(A); }
 void loop_psi(const LoopArgs& A, cudaStream_t st) { k_psi<<<vec_blocks(A.nv), 256, 0, st>>>(A); }

@@ -12,7 +12,11 @@
 
 namespace spock {
 
-constexpr int kLoopMaxMem = 4;  // Anderson memory handled by the graph loop (Gram in one dot launch)
+constexpr int kLoopMaxMem = 10;  // Anderson memory handled by the graph loop (the Gram update in one launch)
+constexpr int kAaHostMax = 64;   // Anderson memory of the host-driven loop (Gram update in chunks)
+// double-double Gram update: 2 * cols dots of (hi, lo) per block, then the
+// arrival counter of the last-block finalize
+constexpr int kGramRegion = 4 * kLoopMaxMem * 296 + 2;
 
 // solve state in device memory (read back by the host at the end)
 struct LoopState {
@@ -28,6 +32,8 @@ struct LoopState {
   double xi1, xi2;
   double cpsi[kLoopMaxMem + 1];  // psi = cpsi[0] r + sum_j cpsi[j+1] r_{k-1-j}
   int ncpsi;
+  // Gram of the difference history in double-double, indexed by ring slot
+  double gh[kLoopMaxMem * kLoopMaxMem], gl[kLoopMaxMem * kLoopMaxMem];
 };
 
 struct LoopParams {
@@ -38,7 +44,8 @@ struct LoopParams {
 struct LoopArgs {
   LoopState* st;
   LoopParams P;
-  const double* red;  // reduction results: [0..3) M-norm dots, [3..5) <r~, M psi>, [4..6) xi norms, [8..) Gram
+  const double* red;  // reduction results: [0..3) M-norm dots, [3..5) <r~, M psi>, [4..6) xi norms,
+                      // [8..) Gram update as (hi, lo) pairs: <d_new, d_b>, then <d_b, r>, b = 0..cols-1
   double* rnorm;      // per-iteration ||r||_M
   char* branch;       // per-iteration branch character
   int cap;            // capacity of rnorm / branch
@@ -56,7 +63,7 @@ struct LoopArgs {
 
 // kernels launched (and captured) by Engine::solve_graph
 void loop_push(const LoopArgs& A, cudaStream_t st);                       // history push (before Gram)
-void loop_gram(const LoopArgs& A, double* partial, double* out, cudaStream_t st);  // Gram of the differences
+void loop_gram(const LoopArgs& A, double* partial, double* out, cudaStream_t st);  // Gram update (double-double)
 void loop_begin(const LoopArgs& A, cudaStream_t st);                      // termination, Anderson, branch
 void loop_psi(const LoopArgs& A, cudaStream_t st);                        // psi from the device coefficients
 void loop_axpy_tau(const LoopArgs& A, cudaStream_t st);                   // C = V + tau psi
@@ -65,5 +72,18 @@ void loop_k2(const LoopArgs& A, cudaStream_t st);                         // V -
 void loop_end(const LoopArgs& A, cudaStream_t st);                        // bookkeeping, loop condition
 void loop_ls_init(const LoopArgs& A, cudaStream_t st);                    // arm the line-search WHILE
 void loop_copy(double* dst, const double* src, int64_t n, cudaStream_t st);
+
+// The host-driven loop's Gram update: (hi, lo) of <dnew, D[b]> for b < cols,
+// then <D[b], r>, with optional 0/1 weights w (sharded solve: the entries this
+// rank counts); cols <= kLoopMaxMem per launch.
+struct GramArgs {
+  const double* dnew;
+  const double* r;
+  const double* D[kLoopMaxMem];
+  const double* w;
+  int cols;
+  int64_t n;
+};
+void launch_gram_dd(const GramArgs& A, double* partial, double* out, cudaStream_t st);
 
 }  // namespace spock
