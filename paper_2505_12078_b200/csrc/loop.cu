@@ -70,12 +70,9 @@ __device__ void gram_dd_body(const double* __restrict__ dnew, const double* __re
   for (int j = 0; j < 2 * M; ++j) acc[j] = {0.0, 0.0};
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += stride) {
-    double x = dnew[i], rr = r[i];
-    if (w) {
-      const double wi = w[i];
-      x *= wi;
-      rr *= wi;
-    }
+    // entries with weight 0 may hold anything (another rank computes them): skipped, not multiplied
+    if (w && w[i] == 0.0) continue;
+    const double x = dnew[i], rr = r[i];
 #pragma unroll
     for (int b = 0; b < M; ++b)
       if (b < cols) {

@@ -240,12 +240,13 @@ class ShardedSolver:
             if op == 3:  # all-gather of n doubles per rank, in place (rank r's at [r n, (r + 1) n))
                 w, r = self.plan.world, self.plan.rank
                 t = torch.as_tensor(_DevArray(ptr, n * w), device="cuda")
-                own = t[r * n:(r + 1) * n].clone()
                 if dist.get_backend(self.group) == "nccl":
-                    with torch.cuda.stream(self.stream):
+                    with torch.cuda.stream(self.stream):  # ordered after the library's writes
+                        own = t[r * n:(r + 1) * n].clone()
                         dist.all_gather_into_tensor(t, own, group=self.group)
                 else:
                     self.stream.synchronize()
+                    own = t[r * n:(r + 1) * n].clone()
                     parts = [torch.empty(n, dtype=torch.float64) for _ in range(w)]
                     dist.all_gather(parts, own.cpu(), group=self.group)
                     t.copy_(torch.cat(parts).to(t.device))
