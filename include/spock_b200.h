@@ -199,6 +199,11 @@ int spock_bench_T(spock_solver* s, int32_t k, int32_t use_graph, int32_t flush_l
 int spock_bench_kernels(spock_solver* s, int32_t k, int32_t flush_l2, double* ms5);
 int spock_traffic_model(spock_solver* s, double* bytes5, int32_t* launches_per_T);
 const char* spock_solver_t_path(const spock_solver* s);
+/* Which loop spock_solver_solve / _solve_cp run (extension): "small" -- the
+ * whole solve in one CTA (trees whose CP application streams <= 2 MB),
+ * "graph" -- one CUDA graph with conditional nodes per solve, "host" -- the
+ * host-driven loop (cancellation callback, Anderson memory > 10, sharded). */
+const char* spock_solver_loop_path(const spock_solver* s);
 
 /* Concurrent solves (batched multi-x_init; no reference
  * counterpart -- the reference solves one x_init at a time, solver.hpp:104-105).

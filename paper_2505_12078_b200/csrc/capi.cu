@@ -257,6 +257,8 @@ void* spock_solver_stream(const spock_solver* s) {
 
 const char* spock_solver_t_path(const spock_solver* s) { return (s && s->eng) ? s->eng->t_path() : ""; }
 
+const char* spock_solver_loop_path(const spock_solver* s) { return (s && s->eng) ? s->eng->loop_path() : ""; }
+
 int spock_solver_set_grid_cap(spock_solver* s, int32_t ctas) {
   if (int rc = check(s)) return rc;
   return guard([&] { s->eng->set_grid_cap(ctas); });

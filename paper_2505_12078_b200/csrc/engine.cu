@@ -1971,6 +1971,112 @@ void Engine::unscale_b(const double* zs, double* z) {  // solver.cpp:116-130
 }
 
 // ---------------------------------------------------------------------------
+// CTA-resident loop for small trees (small.cuh): the whole solve in one CTA,
+// operator phases separated by __syncthreads, the graph loop's controller on a
+// shared-memory state.  Chosen when a CP application streams little enough
+// that one SM's L1 holds the blocks (Engine::traffic <= kSmallBytes) and the
+// per-stage operator kernels cover the shape.  SPOCK_SMALL=0 disables it,
+// SPOCK_SMALL=1 forces it (tests).
+bool Engine::small_eligible() const {
+  const char* env = std::getenv("SPOCK_SMALL");
+  const char* genv = std::getenv("SPOCK_SOLVE_GRAPH");  // 0: the host-driven loop (no device-resident loop)
+  if ((env && env[0] == '0') || (genv && genv[0] == '0')) return false;
+  if (prm_.cancelled || prm_.aa_memory > kLoopMaxMem) return false;
+  if (env && env[0] == '1') return true;
+  double b[5];
+  traffic(b);
+  return b[4] <= kSmallBytes && p_.tree.nn() <= 4096;
+}
+
+const char* Engine::loop_path() const {
+  if (shard_.on && shard_.coll) return "host";
+  if (small_eligible()) return "small";
+  const char* env = std::getenv("SPOCK_SOLVE_GRAPH");
+  if (prm_.cancelled || prm_.aa_memory > kLoopMaxMem || (env && env[0] == '0')) return "host";
+  return "graph";
+}
+
+bool Engine::solve_small(const double* x_init, const double* wz, const double* we, double* oz, double* ozs,
+                         double* oe, bool supermann, Status& st) {
+  if (!small_eligible()) return false;
+  const int m = prm_.aa_memory;
+  const int64_t nz = lay_.nz, ne = lay_.neta, nv = nz + ne;
+  set_xinit(x_init ? x_init : raw_.x_init.data());
+  SmallArgs& A = small_;
+  if (!A.L.V) {  // buffers, built once per engine
+    auto pair = [&]() { return dalloc<double>(size_t(nv)); };
+    A.L.V = pair(), A.L.TV = pair(), A.L.R = pair(), A.L.C = pair(), A.L.CR = pair(), A.L.PSI = pair();
+    A.TC = pair(), A.PV = pair();
+    A.Lrz = dalloc<double>(size_t(ne));
+    A.cLrz = dalloc<double>(size_t(ne));
+    A.Lsre = dalloc<double>(size_t(nz));
+    A.tmpz = dalloc<double>(size_t(nz));
+    A.tmpe = dalloc<double>(size_t(ne));
+    for (int j = 0; j < kLoopMaxMem + 1; ++j) A.L.RH[j] = pair();
+    for (int j = 0; j < kLoopMaxMem; ++j) A.L.DH[j] = pair();
+    A.L.st = dalloc<LoopState>(1);
+    A.stage_start = dupload(stage_start_);
+    small_cap_ = 0;
+  }
+  const int cap = prm_.max_iters + 2;
+  if (small_cap_ < cap) {
+    A.L.rnorm = dalloc<double>(size_t(cap));
+    A.L.branch = dalloc<char>(size_t(cap));
+    small_cap_ = cap;
+  }
+  A.L.P = LoopParams{prm_.eps_abs, prm_.eps_rel, prm_.c0, prm_.c1, prm_.c2, prm_.beta, prm_.sigma, prm_.lambda,
+                     alpha_, prm_.max_iters, prm_.max_backtracks, m, supermann ? 1 : 0};
+  A.L.cap = cap;
+  A.L.nz = nz;
+  A.L.nv = nv;
+  A.D = D_;
+  A.d1 = d1_;
+  A.d2 = d2_;
+  A.supermann = supermann ? 1 : 0;
+  double* V = A.L.V;
+  CK(cudaMemsetAsync(V, 0, sizeof(double) * nv, st_));
+  if (wz || we) {
+    if (!wz || !we) throw std::invalid_argument("solve: warm start has wrong dimensions");
+    copy_in_z(wz, V);
+    to_internal_eta(we, V + nz);
+  }
+  LoopState S0{};
+  S0.reason = -1;
+  S0.n_T = 1;
+  S0.n_L = 1;
+  S0.k_stop = prm_.max_iters + 1;
+  CK(cudaMemcpyAsync(A.L.st, &S0, sizeof(S0), cudaMemcpyHostToDevice, st_));
+  launch_small_solve(A, st_);
+  CK(cudaGetLastError());
+  LoopState Sh{};
+  CK(cudaMemcpyAsync(&Sh, A.L.st, sizeof(Sh), cudaMemcpyDeviceToHost, st_));
+  CK(cudaStreamSynchronize(st_));
+  if (Sh.reason == -2) throw std::runtime_error("spock: negative M-norm radicand (alpha too large)");
+  const int iters = Sh.k;
+  std::vector<double> rn(size_t(std::max(iters, 1)));
+  std::vector<char> br(size_t(std::max(iters, 1)));
+  if (iters > 0) {
+    CK(cudaMemcpy(rn.data(), A.L.rnorm, sizeof(double) * iters, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(br.data(), A.L.branch, size_t(iters), cudaMemcpyDeviceToHost));
+  }
+  st.iterations = iters;
+  st.reason = Sh.reason < 0 ? SPOCK_MAX_ITERS : Sh.reason;
+  st.xi1 = Sh.xi1;
+  st.xi2 = Sh.xi2;
+  st.k0 = Sh.k0, st.k1 = Sh.k1, st.k2 = Sh.k2, st.stalled = Sh.stalled;
+  st.n_T = Sh.n_T, st.n_L = Sh.n_L, st.n_Lt = Sh.n_Lt;
+  st.rnorm.assign(rn.begin(), rn.begin() + iters);
+  st.branches.assign(br.begin(), br.begin() + iters);
+  if (prm_.progress)  // replayed after the kernel (as for the graph loop)
+    for (int k = 0; k < iters; ++k) prm_.progress(k, rn[k], br[k]);
+  if (ozs) copy_out(A.L.TV, ozs, nz);
+  if (oe) from_internal_eta(A.L.TV + nz, oe);
+  sync();
+  if (oz) unscale_b(A.L.TV, oz);
+  return true;
+}
+
+// ---------------------------------------------------------------------------
 // Device-resident loop (loop.cu): one CUDA graph per solve.
 //   WHILE(h_loop) {
 //     L*(r_eta), xi norms, [history push, Gram]      -> k_begin (termination,
@@ -2222,6 +2328,7 @@ void Engine::solve_b(const double* x_init, const double* wz, const double* we, d
   const double* w_z = sharded ? shard_.wz : nullptr;
   const double* w_e = sharded ? shard_.we : nullptr;
   const double* w_v = sharded ? shard_.wv : nullptr;
+  if (!sharded && solve_small(x_init, wz, we, oz, ozs, oe, supermann, st)) return;
   if (!sharded && solve_graph(x_init, wz, we, oz, ozs, oe, supermann, st)) return;
   const int64_t nz = lay_.nz, ne = lay_.neta, nv = nz + ne;
   set_xinit(x_init ? x_init : raw_.x_init.data());

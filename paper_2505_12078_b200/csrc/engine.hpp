@@ -84,6 +84,15 @@ class Engine {
     double* Lrz = nullptr;
   };
   GraphLoop gloop_[2];  // CP, SuperMann
+  // CTA-resident loop for small trees (small.cuh)
+  static constexpr double kSmallBytes = 2.0e6;  // algorithmic bytes per T at most (one SM's L1 / L2 share)
+  bool small_eligible() const;
+  // which loop a solve runs: "small" (CTA-resident), "graph" (device-resident graph) or "host"
+  const char* loop_path() const;
+  bool solve_small(const double* x_init, const double* wz, const double* we, double* oz, double* ozs, double* oe,
+                   bool supermann, Status& st);
+  SmallArgs small_{};
+  int small_cap_ = 0;
   void build_loop_graph(GraphLoop& G, bool supermann);
   double bench_T(int k, bool graph, bool flush);
   void bench_kernels(int k, bool flush, double* ms);

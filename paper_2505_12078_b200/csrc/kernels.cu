@@ -30,6 +30,7 @@
 
 #include "dev.cuh"
 #include "kernels.hpp"
+#include "loop_ctl.cuh"
 
 namespace spock {
 
@@ -118,16 +119,10 @@ __device__ void ycone_project(const Dev& D, int i, double* t, int ny) {
 // ---------------------------------------------------------------------------
 // L* part 1: per non-root child c, adj_c = H_c' head_c - rsum/2 qk_c and the
 // tau slot (tree_operator.cpp:80-88).
-__global__ void __launch_bounds__(32 * kWarps) k_Lt_child(Dev D, const double* __restrict__ eta,
-                                                         const double* __restrict__ zin, double* __restrict__ zout,
-                                                         double a, double b) {
-  __shared__ double sh[kWarps][kMaxD];
-  const int w = threadIdx.x >> 5, l = lane_id();
-  const int k = blockIdx.x * kWarps + w;
-  if (k >= D.nr) return;
+__device__ __forceinline__ void lt_child_body(const Dev& D, int k, const double* __restrict__ eta, const double* __restrict__ zin, double* __restrict__ zout, double a, double b, double* __restrict__ xs) {
+  const int l = lane_id();
   const int px = D.px[k], pu = D.pu[k], p = px + pu;
   const double* seg = eta + D.s2_off[k];
-  double* xs = sh[w];
   for (int r = l; r < p; r += 32) xs[r] = seg[r];
   const double rsum = seg[p] + seg[p + 1];
   __syncwarp();
@@ -163,17 +158,21 @@ __global__ void __launch_bounds__(32 * kWarps) k_Lt_child(Dev D, const double* _
   }
 }
 
+__global__ void __launch_bounds__(32 * kWarps) k_Lt_child(Dev D, const double* __restrict__ eta,
+                                                         const double* __restrict__ zin, double* __restrict__ zout,
+                                                         double a, double b) {
+  __shared__ double sh[kWarps][kMaxD];
+  const int w = threadIdx.x >> 5;
+  const int k = blockIdx.x * kWarps + w;
+  if (k >= D.nr) return;
+  lt_child_body(D, k, eta, zin, zout, a, b, sh[w]);
+}
+
 // L* part 2: per node, own segments + ascending sum of the children's adj
 // (tree_operator.cpp:75-79,89-113).  zout = a*zin + b*L*eta (+c0 at s0).
-__global__ void __launch_bounds__(32 * kWarps) k_Lt_node(Dev D, const double* __restrict__ eta,
-                                                        const double* __restrict__ zin, double* __restrict__ zout,
-                                                        double a, double b, double c0) {
-  __shared__ double sh[kWarps][kMaxD];
-  const int w = threadIdx.x >> 5, l = lane_id();
-  const int i = blockIdx.x * kWarps + w;
-  if (i >= D.nn) return;
+__device__ __forceinline__ void lt_node_body(const Dev& D, int i, const double* __restrict__ eta, const double* __restrict__ zin, double* __restrict__ zout, double a, double b, double c0, double* __restrict__ xs) {
+  const int l = lane_id();
   const int nx = D.nx, nu = D.nu;
-  double* xs = sh[w];
   auto emit = [&](int idx, double lt) { zout[idx] = (a == 0.0 ? 0.0 : a * zin[idx]) + b * lt; };
   double acc[kMaxR];
   if (i < D.nnl) {
@@ -275,21 +274,24 @@ __global__ void __launch_bounds__(32 * kWarps) k_Lt_node(Dev D, const double* __
   }
 }
 
+__global__ void __launch_bounds__(32 * kWarps) k_Lt_node(Dev D, const double* __restrict__ eta,
+                                                        const double* __restrict__ zin, double* __restrict__ zout,
+                                                        double a, double b, double c0) {
+  __shared__ double sh[kWarps][kMaxD];
+  const int w = threadIdx.x >> 5;
+  const int i = blockIdx.x * kWarps + w;
+  if (i >= D.nn) return;
+  lt_node_body(D, i, eta, zin, zout, a, b, c0, sh[w]);
+}
+
 // ---------------------------------------------------------------------------
 // L applied to w = a1*z1 + a2*z2.  PLAIN: eta_out = L w.  DUAL: the CP dual
 // half with the S3 projection fused: p = eta + alpha L w, eta_out =
 // p - alpha Pi_S3(p/alpha)  (solver.cpp:159-163).
 template <bool DUAL>
-__global__ void __launch_bounds__(32 * kWarps) k_L(Dev D, const double* __restrict__ z1, double a1,
-                                                  const double* __restrict__ z2, double a2,
-                                                  const double* __restrict__ eta_in, double* __restrict__ eta_out,
-                                                  double alpha) {
-  __shared__ double sh[kWarps][kMaxD];
-  const int w = threadIdx.x >> 5, l = lane_id();
-  const int i = blockIdx.x * kWarps + w;
-  if (i >= D.nn) return;
+__device__ __forceinline__ void L_node_body(const Dev& D, int i, const double* __restrict__ z1, double a1, const double* __restrict__ z2, double a2, const double* __restrict__ eta_in, double* __restrict__ eta_out, double alpha, double* __restrict__ xs) {
+  const int l = lane_id();
   const int nx = D.nx, nu = D.nu;
-  double* xs = sh[w];
   auto W = [&](int idx) { return z2 ? a1 * z1[idx] + a2 * z2[idx] : a1 * z1[idx]; };
   auto fin = [&](int idx, double val) -> double {  // before projection
     return DUAL ? eta_in[idx] + alpha * val : val;
@@ -480,11 +482,21 @@ __global__ void __launch_bounds__(32 * kWarps) k_L(Dev D, const double* __restri
   }
 }
 
-// Standalone S3 projection in place (proj_s3, projections.cpp:212-244).
-__global__ void __launch_bounds__(32 * kWarps) k_s3(Dev D, double* __restrict__ eta) {
-  const int w = threadIdx.x >> 5, l = lane_id();
+template <bool DUAL>
+__global__ void __launch_bounds__(32 * kWarps) k_L(Dev D, const double* __restrict__ z1, double a1,
+                                                  const double* __restrict__ z2, double a2,
+                                                  const double* __restrict__ eta_in, double* __restrict__ eta_out,
+                                                  double alpha) {
+  __shared__ double sh[kWarps][kMaxD];
+  const int w = threadIdx.x >> 5;
   const int i = blockIdx.x * kWarps + w;
   if (i >= D.nn) return;
+  L_node_body<DUAL>(D, i, z1, a1, z2, a2, eta_in, eta_out, alpha, sh[w]);
+}
+
+// Standalone S3 projection in place (proj_s3, projections.cpp:212-244).
+__device__ __forceinline__ void s3_node_body(const Dev& D, int i, double* __restrict__ eta, double* __restrict__ xs) {
+  const int l = lane_id();
   double acc[kMaxR];
   if (i < D.nnl) {
     const int ny = D.y_dim[i], so = D.s1_off[i];
@@ -540,15 +552,19 @@ __global__ void __launch_bounds__(32 * kWarps) k_s3(Dev D, double* __restrict__ 
   }
 }
 
+__global__ void __launch_bounds__(32 * kWarps) k_s3(Dev D, double* __restrict__ eta) {
+  __shared__ double sh[kWarps][kMaxD];
+  const int w = threadIdx.x >> 5;
+  const int i = blockIdx.x * kWarps + w;
+  if (i >= D.nn) return;
+  s3_node_body(D, i, eta, sh[w]);
+}
+
 // ---------------------------------------------------------------------------
 // S1 backward, one launch per stage (nodes [b, e)), in place on z's (x, u).
-__global__ void __launch_bounds__(32 * kWarps) k_s1_back(Dev D, int b, int e, const double* __restrict__ z) {
-  __shared__ double sh[kWarps][kMaxD];
-  const int w = threadIdx.x >> 5, l = lane_id();
-  const int i = b + blockIdx.x * kWarps + w;
-  if (i >= e) return;
+__device__ __forceinline__ void s1_back_body(const Dev& D, int i, const double* __restrict__ z, double* __restrict__ xs) {
+  const int l = lane_id();
   const int nx = D.nx, nu = D.nu;
-  double* xs = sh[w];
   double q[kMaxR];
   const double* xb = z + 1 + size_t(i) * nx;
   if (D.cc[i] == 0) {
@@ -624,15 +640,19 @@ __global__ void __launch_bounds__(32 * kWarps) k_s1_back(Dev D, int b, int e, co
   }
 }
 
-// S1 forward, one launch per stage: x_c = [Abar B][x_anc; d_anc] + c_c,
-// u_c = K_c x_c + d_c (projections.cpp:176-186).
-__global__ void __launch_bounds__(32 * kWarps) k_s1_fwd(Dev D, int b, int e, double* __restrict__ z) {
+__global__ void __launch_bounds__(32 * kWarps) k_s1_back(Dev D, int b, int e, const double* __restrict__ z) {
   __shared__ double sh[kWarps][kMaxD];
-  const int w = threadIdx.x >> 5, l = lane_id();
+  const int w = threadIdx.x >> 5;
   const int i = b + blockIdx.x * kWarps + w;
   if (i >= e) return;
+  s1_back_body(D, i, z, sh[w]);
+}
+
+// S1 forward, one launch per stage: x_c = [Abar B][x_anc; d_anc] + c_c,
+// u_c = K_c x_c + d_c (projections.cpp:176-186).
+__device__ __forceinline__ void s1_fwd_body(const Dev& D, int i, double* __restrict__ z, double* __restrict__ xs) {
+  const int l = lane_id();
   const int nx = D.nx, nu = D.nu;
-  double* xs = sh[w];
   double x[kMaxR];
   if (i == 0) {
 #pragma unroll
@@ -684,13 +704,18 @@ __global__ void __launch_bounds__(32 * kWarps) k_s1_fwd(Dev D, int b, int e, dou
   }
 }
 
+__global__ void __launch_bounds__(32 * kWarps) k_s1_fwd(Dev D, int b, int e, double* __restrict__ z) {
+  __shared__ double sh[kWarps][kMaxD];
+  const int w = threadIdx.x >> 5;
+  const int i = b + blockIdx.x * kWarps + w;
+  if (i >= e) return;
+  s1_fwd_body(D, i, z, sh[w]);
+}
+
 // ---------------------------------------------------------------------------
 // S2: projection of (y_i, tau_[i], s_[i]) onto ker [E' -I -I] per non-leaf.
-__global__ void __launch_bounds__(32 * kWarps) k_s2(Dev D, double* __restrict__ z) {
-  __shared__ double sh[kWarps][kMaxD];
-  const int w = threadIdx.x >> 5, l = lane_id();
-  const int i = blockIdx.x * kWarps + w;
-  if (i >= D.nnl) return;
+__device__ __forceinline__ void s2_node_body(const Dev& D, int i, double* __restrict__ z, double* __restrict__ xs) {
+  const int l = lane_id();
   const int n = D.cc[i], c0 = D.cf[i], ny = D.y_dim[i];
   double* y = z + D.y_off[i];
   double* tau = z + D.tau_base + (c0 - 1);
@@ -698,7 +723,6 @@ __global__ void __launch_bounds__(32 * kWarps) k_s2(Dev D, double* __restrict__ 
   const int kind = D.s2_kind[i];
   if (kind == S2_DENSE) {
     const int dim = ny + 2 * n;
-    double* xs = sh[w];
     for (int r = l; r < ny; r += 32) xs[r] = y[r];
     for (int r = l; r < n; r += 32) {
       xs[ny + r] = tau[r];
@@ -765,6 +789,14 @@ __global__ void __launch_bounds__(32 * kWarps) k_s2(Dev D, double* __restrict__ 
     else
       y[n] = ylast - lsum;
   }
+}
+
+__global__ void __launch_bounds__(32 * kWarps) k_s2(Dev D, double* __restrict__ z) {
+  __shared__ double sh[kWarps][kMaxD];
+  const int w = threadIdx.x >> 5;
+  const int i = blockIdx.x * kWarps + w;
+  if (i >= D.nnl) return;
+  s2_node_body(D, i, z, sh[w]);
 }
 
 // ---------------------------------------------------------------------------
@@ -1007,6 +1039,8 @@ __global__ void k_alg1_child_abar(Alg1Args P) {
   }
 }
 
+#include "small.cuh"
+
 }  // namespace
 
 // ===========================================================================
@@ -1047,6 +1081,11 @@ void launch_s2(const Dev& D, double* z, cudaStream_t st) {
 
 void launch_s3(const Dev& D, double* eta, cudaStream_t st) {
   k_s3<<<blocks_for(D.nn, kWarps), 32 * kWarps, 0, st>>>(D, eta);
+}
+
+void launch_small_solve(const SmallArgs& A, cudaStream_t st) {
+  static_assert(kSmallThreads == kSmallThreadsHost, "small solve block size");
+  k_small_solve<<<1, kSmallThreads, 0, st>>>(A);
 }
 
 void launch_axpby(int n, double a, const double* x, double b, const double* y, double* out, cudaStream_t st) {

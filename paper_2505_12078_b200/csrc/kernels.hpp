@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include "dev.cuh"
+#include "loop.hpp"
 
 namespace spock {
 
@@ -69,6 +70,18 @@ struct Alg1Args {
   double* Abar_out;  // optional per non-root
   int* err;
 };
+
+// CTA-resident SuperMann / CP solve for small trees (small.cuh)
+struct SmallArgs {
+  LoopArgs L;  // state (device copy of the initial LoopState), parameters, history rings, V TV R C CR PSI
+  Dev D;
+  const int* stage_start;  // [N + 2]
+  double *TC, *PV, *Lrz, *cLrz, *Lsre, *tmpz, *tmpe;
+  const double *d1, *d2;  // termination scalings
+  int supermann;
+};
+void launch_small_solve(const SmallArgs& A, cudaStream_t st);
+constexpr int kSmallThreadsHost = 256;
 
 void launch_Lt(const Dev& D, const double* eta, const double* zin, double* zout, double a, double b, double c0,
                cudaStream_t st);

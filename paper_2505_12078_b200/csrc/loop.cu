@@ -17,6 +17,7 @@
 #include "kernels.hpp"
 #include "aa.cuh"
 #include "loop.hpp"
+#include "loop_ctl.cuh"
 
 namespace spock {
 
@@ -24,11 +25,6 @@ static_assert(kGramRegion == 4 * kLoopMaxMem * kRedBlocks + 2, "Gram partial reg
 
 namespace {
 
-__device__ __forceinline__ void set_cond(unsigned long long h, unsigned int v) {
-  cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(h), v);
-}
-
-__device__ __forceinline__ int ring(int i, int n) { return ((i % n) + n) % n; }
 
 // history push for iteration k (solver.cpp:57-63): newest slot hn = h + 1
 __global__ void k_push(const __grid_constant__ LoopArgs A) {
@@ -138,102 +134,6 @@ __global__ void __launch_bounds__(kRedThreads) k_gram_args(const __grid_constant
   gram_dd_body(G.dnew, G.r, G.D, G.w, G.cols, G.n, partial, out);
 }
 
-// top of iteration k (solver.cpp:233-290): M-norm, xi thresholds, termination,
-// Anderson direction coefficients, K0 test; selects the branch body
-__global__ void k_begin(const __grid_constant__ LoopArgs A) {
-  LoopState& S = *A.st;
-  const LoopParams& P = A.P;
-  const double* red = A.red;
-  if (P.supermann) {
-    S.h += 1;
-    S.aa_cols = min(S.aa_cols + 1, P.m);
-  }
-  int reason = -1;
-  if (!S.have_omega) {
-    const double rad = red[0] - 2.0 * P.alpha * red[1] + red[2];
-    if (rad < -1e-12 * fmax(1.0, red[0] + red[2])) reason = -2;  // solver.cpp:171-172
-    S.omega = sqrt(fmax(0.0, rad));
-    if (S.k == 0) S.zeta = S.omega_safe = S.omega;
-  }
-  const double n1 = red[4], n2 = red[5];
-  if (S.k == 0) {
-    S.th1 = fmax(P.eps_abs, P.eps_rel * n1);
-    S.th2 = fmax(P.eps_abs, P.eps_rel * n2);
-  }
-  S.xi1 = n1;
-  S.xi2 = n2;
-  ++S.n_Lt;
-  if (reason < 0) {
-    if (!isfinite(n1) || !isfinite(n2) || !isfinite(S.omega))
-      reason = SPOCK_STALLED;
-    else if (n1 <= S.th1 && n2 <= S.th2)
-      reason = SPOCK_CONVERGED;
-    else if (S.k >= P.max_iters)
-      reason = SPOCK_MAX_ITERS;
-  }
-  if (reason != -1) {
-    S.reason = reason;
-    S.sw = 0;
-    S.refresh = 0;
-    set_cond(A.h_sw, 0);
-    set_cond(A.h_ref, 0);
-    set_cond(A.h_loop, 0);
-    return;
-  }
-  if (S.k < A.cap) A.rnorm[S.k] = S.omega;
-  if (!P.supermann) {  // CP: v <- T(v)
-    S.sw = 3;
-    S.refresh = 1;
-    S.act = 'K';
-    set_cond(A.h_sw, 3);
-    set_cond(A.h_ref, 1);
-    return;
-  }
-  // Anderson direction (solver.cpp:64-76)
-  const int kk = S.aa_k++;
-  S.cpsi[0] = -1.0;
-  S.ncpsi = 1;
-  // Gram ring update: row / column of the newest difference (slot of head h)
-  const int cols = S.aa_cols, m = P.m, s0 = ring(S.h, m);
-  for (int b = 0; b < cols; ++b) {
-    const int sb = ring(S.h - b, m);
-    const double hi = red[8 + 2 * b], lo = red[8 + 2 * b + 1];
-    S.gh[s0 + sb * kLoopMaxMem] = S.gh[sb + s0 * kLoopMaxMem] = hi;
-    S.gl[s0 + sb * kLoopMaxMem] = S.gl[sb + s0 * kLoopMaxMem] = lo;
-  }
-  if (kk > P.m) {
-    dd G[kLoopMaxMem * kLoopMaxMem], gr[kLoopMaxMem];
-    double kap[kLoopMaxMem];
-    for (int a = 0; a < cols; ++a) {
-      const int sa = ring(S.h - a, m);
-      for (int b = 0; b < cols; ++b) {
-        const int sb = ring(S.h - b, m);
-        G[a + b * cols] = {S.gh[sa + sb * kLoopMaxMem], S.gl[sa + sb * kLoopMaxMem]};
-      }
-      gr[a] = {red[8 + 2 * (cols + a)], red[8 + 2 * (cols + a) + 1]};
-    }
-    aa_kappa_dd<kLoopMaxMem>(G, gr, cols, A.nv, kap);
-    for (int c = 0; c < cols; ++c) S.cpsi[c + 1] = -kap[c];
-    S.ncpsi = cols + 1;
-  }
-  if (S.omega <= P.c0 * S.zeta) {  // K0
-    S.zeta = S.omega;
-    S.act = '0';
-    ++S.k0;
-    S.sw = 1;
-    S.refresh = 1;
-    set_cond(A.h_sw, 1);
-    set_cond(A.h_ref, 1);
-  } else {  // line search with M psi (solver.cpp:287-290)
-    ++S.n_Lt;
-    ++S.n_L;
-    S.tau = 1.0;
-    S.backtracks = 0;
-    S.sw = 2;
-    set_cond(A.h_sw, 2);
-  }
-}
-
 // first kernel of the line-search branch: arm its WHILE (the handle lives in
 // that branch's body graph)
 __global__ void k_ls_init(const __grid_constant__ LoopArgs A) { set_cond(A.h_ls, 1); }
@@ -268,84 +168,14 @@ __global__ void k_axpy_tau(const __grid_constant__ LoopArgs A) {  // C = V + tau
     A.C[i] = A.V[i] + tau * A.PSI[i];
 }
 
-// line-search trial decision (solver.cpp:295-338)
-__global__ void k_ls(const __grid_constant__ LoopArgs A) {
-  LoopState& S = *A.st;
-  const LoopParams& P = A.P;
-  const double* red = A.red;
-  ++S.n_T;
-  ++S.n_L;
-  const double rad = red[0] - 2.0 * P.alpha * red[1] + red[2];
-  if (rad < -1e-12 * fmax(1.0, red[0] + red[2])) {
-    S.reason = -2;
-    S.act = 'S';
-    S.sw = 0;
-    set_cond(A.h_ls, 0);
-    set_cond(A.h_act, 0);
-    set_cond(A.h_ref, 0);
-    set_cond(A.h_loop, 0);
-    return;
-  }
-  const double omt = sqrt(fmax(0.0, rad));
-  S.omt = omt;
-  if ((S.omega <= S.omega_safe && omt <= P.c1 * S.omega) || omt == 0.0) {  // K1
-    S.omega_safe = omt + pow(P.c2, double(S.k));
-    S.act = '1';
-    ++S.k1;
-    S.omega = omt;  // carried to the next iteration
-    S.have_omega = 1;
-    S.refresh = 0;
-    set_cond(A.h_ls, 0);
-    set_cond(A.h_act, 1);
-    set_cond(A.h_ref, 0);
-    return;
-  }
-  const double rho = omt * omt - S.tau * (red[3] + red[4]);
-  if (rho >= P.sigma * omt * S.omega) {  // K2
-    S.coef = P.lambda * rho / (omt * omt);
-    S.act = '2';
-    ++S.k2;
-    S.refresh = 1;
-    set_cond(A.h_ls, 0);
-    set_cond(A.h_act, 2);
-    set_cond(A.h_ref, 1);
-    return;
-  }
-  S.tau *= P.beta;
-  if (++S.backtracks > P.max_backtracks) {  // KM fallback
-    S.act = 'S';
-    ++S.stalled;
-    S.refresh = 1;
-    set_cond(A.h_ls, 0);
-    set_cond(A.h_act, 3);
-    set_cond(A.h_ref, 1);
-    return;
-  }
-  set_cond(A.h_ls, 1);
-  set_cond(A.h_act, 0);
-}
+__global__ void k_begin(const __grid_constant__ LoopArgs A) { ctl_begin<true>(A); }
+__global__ void k_ls(const __grid_constant__ LoopArgs A) { ctl_ls<true>(A); }
+__global__ void k_end(const __grid_constant__ LoopArgs A) { ctl_end<true>(A); }
 
 __global__ void k_k2(const __grid_constant__ LoopArgs A) {  // v <- v - coef r~
   const double coef = A.st->coef;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < A.nv; i += int64_t(gridDim.x) * blockDim.x)
     A.V[i] -= coef * A.CR[i];
-}
-
-// end of iteration k: branch record, refresh bookkeeping, loop condition
-__global__ void k_end(const __grid_constant__ LoopArgs A) {
-  LoopState& S = *A.st;
-  if (S.reason != -1) {
-    set_cond(A.h_loop, 0);
-    return;
-  }
-  if (S.k < A.cap) A.branch[S.k] = char(S.act);
-  if (S.refresh) {
-    S.have_omega = 0;
-    ++S.n_T;
-    ++S.n_L;
-  }
-  ++S.k;
-  set_cond(A.h_loop, S.k < S.k_stop ? 1 : 0);
 }
 
 inline int vec_blocks(int64_t n) { return int(std::min<int64_t>((n + 255) / 256, 4 * 148)); }

@@ -28,6 +28,7 @@ struct LoopState {
   int backtracks;
   int n_T, n_L, n_Lt, k0, k1, k2, stalled;
   int sw, act, refresh;  // branch decisions (mirrors of the conditional handles)
+  int ls_more;           // line search continues (mirror of the line-search WHILE handle)
   double omega, zeta, omega_safe, th1, th2, tau, omt, coef;
   double xi1, xi2;
   double cpsi[kLoopMaxMem + 1];  // psi = cpsi[0] r + sum_j cpsi[j+1] r_{k-1-j}

@@ -205,16 +205,12 @@ __device__ __forceinline__ void refill_lane0(Ring& R) {
   }
 }
 
-// acc[k] += sum_{c < cc} A[(lane + 32k) + c*rows] x[c], A in shared memory.
-// Even and odd columns accumulate into separate registers (two independent DFMA
-// chains per row block: the chain latency, not the shared-memory bandwidth,
-// bounds a warp here), summed once per chunk in a fixed order.
+// acc[k] += sum_{c < cc} A[(lane + 32k) + c*rows] x[c], A in shared memory
+// (a second, interleaved accumulator chain measured no faster: the warp is not
+// bound by the DFMA chain but by the instructions around it)
 template <int RR>
 __device__ __forceinline__ void gemv_cols(const double* A, int rows, int cc, const double* x, double (&acc)[RR]) {
   const int l = lane_id();
-  double a1[RR];
-#pragma unroll
-  for (int k = 0; k < RR; ++k) a1[k] = 0.0;
   int c = 0;
   for (; c + 4 <= cc; c += 4) {
     const double x0 = x[c], x1 = x[c + 1], x2 = x[c + 2], x3 = x[c + 3];
@@ -224,9 +220,9 @@ __device__ __forceinline__ void gemv_cols(const double* A, int rows, int cc, con
       const int r = l + 32 * k;
       if (r < rows) {
         acc[k] = fma(a[r], x0, acc[k]);
-        a1[k] = fma(a[r + rows], x1, a1[k]);
+        acc[k] = fma(a[r + rows], x1, acc[k]);
         acc[k] = fma(a[r + 2 * rows], x2, acc[k]);
-        a1[k] = fma(a[r + 3 * rows], x3, a1[k]);
+        acc[k] = fma(a[r + 3 * rows], x3, acc[k]);
       }
     }
   }
@@ -239,8 +235,6 @@ __device__ __forceinline__ void gemv_cols(const double* A, int rows, int cc, con
       if (r < rows) acc[k] = fma(a[r], xc, acc[k]);
     }
   }
-#pragma unroll
-  for (int k = 0; k < RR; ++k) acc[k] += a1[k];
 }
 
 // consume the chunks of the item's next streamed matrix (record order): acc += M x

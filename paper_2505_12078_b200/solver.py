@@ -242,6 +242,11 @@ class SpockSolver:
         return out, n.value
 
     @property
+    def loop_path(self) -> str:
+        """Loop a solve runs: 'small' (one CTA), 'graph' (CUDA graph) or 'host'."""
+        return self.lib.spock_solver_loop_path(self.h).decode()
+
+    @property
     def grid(self) -> int:
         """CTAs of the fused T launch (0 when T runs on another schedule)."""
         return int(self.lib.spock_solver_grid(self.h))

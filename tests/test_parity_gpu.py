@@ -130,3 +130,63 @@ def test_long_supermann_trace_matches_oracle(cfg):
           f"oracle {b.status['k0_steps']}/{b.status['k1_steps']}/{b.status['k2_steps']}")
     assert d >= need, f"branch strings diverge at iteration {d}"
     assert h >= horizon, f"||r||_M traces differ by more than 1e-6 from iteration {h}"
+
+
+def _with_env(env, fn):
+    import os
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        return fn()
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+SMALL_CASES = [
+    ("binary-2x2", lambda: make_tiny(ScenarioTree.from_branching([2, 2]), 2, 1, 31, TinyOpts(gamma=0.5, box_halfwidth=1.0))),
+    ("mixed-3-1-2", lambda: make_tiny(ScenarioTree.from_branching([3, 1, 2]), 3, 2, 5, TinyOpts(gamma=0.3))),
+    ("c1", None),
+]
+
+
+@pytest.mark.parametrize("name,mk", SMALL_CASES, ids=[c[0] for c in SMALL_CASES])
+@pytest.mark.parametrize("method", ["solve", "solve_cp"])
+def test_small_loop_matches_graph_loop(name, mk, method):
+    """The CTA-resident loop (small.cuh: the whole solve in one CTA) runs the
+    graph loop's algorithm on the per-stage operator kernels' arithmetic: over
+    a few dozen iterations the branch strings and counters agree and the traces
+    and iterates agree to rounding."""
+    from paper_2505_12078_b200.generators import make_config
+    from paper_2505_12078_b200.solver import SpockSolver
+    p = make_config("c1", seed=1) if mk is None else mk()
+    s = SpockSolver(p, max_iters=40, eps_abs=1e-14, eps_rel=1e-14)
+    assert s.loop_path == "small"
+    g = _with_env({"SPOCK_SMALL": "0"}, lambda: SpockSolver(p, max_iters=40, eps_abs=1e-14, eps_rel=1e-14,
+                                                              alpha=s.alpha))
+    assert g.loop_path == "graph"
+    a = getattr(s, method)(p.x_init)
+    b = getattr(g, method)(p.x_init)
+    assert a.status["branches"] == b.status["branches"]
+    for key in ("iterations", "n_T", "n_L", "n_Lt", "k0_steps", "k1_steps", "k2_steps", "stalled_steps", "reason"):
+        assert a.status[key] == b.status[key], key
+    np.testing.assert_allclose(a.status["rnorm_history"], b.status["rnorm_history"], rtol=1e-9, atol=1e-12)
+    for x, y in ((a.z_scaled, b.z_scaled), (a.eta, b.eta)):
+        assert float(np.abs(x - y).max()) <= 1e-8 * max(1.0, float(np.abs(y).max()))
+
+
+def test_small_loop_bitwise_deterministic_and_warm_start():
+    from paper_2505_12078_b200.generators import make_config
+    from paper_2505_12078_b200.solver import SpockSolver
+    p = make_config("c1", seed=1)
+    s = SpockSolver(p, max_iters=300)
+    a, b = s.solve(), s.solve()
+    assert np.array_equal(a.z, b.z) and np.array_equal(a.status["rnorm_history"], b.status["rnorm_history"])
+    w = SpockSolver(p, max_iters=50000, eps_abs=1e-6, eps_rel=1e-6)
+    cold = w.solve_cp()
+    warm = w.solve_cp(p.x_init, warm=(cold.z_scaled, cold.eta))
+    assert cold.status["reason"] == warm.status["reason"] == "converged"
+    assert warm.status["iterations"] <= 2
