@@ -117,6 +117,17 @@ Engine::Engine(const spock_problem_desc* desc, const Params& prm) : prm_(prm) {
   mark("fused / wide records");
   power_iteration();
   alpha_ = prm_.alpha > 0.0 ? prm_.alpha : 0.99 / std::max(norm_.estimate, 1e-300);
+  {  // CTA-resident loop (small.cuh) for trees whose CP application streams little
+    const char* env = std::getenv("SPOCK_SMALL");
+    double b[5];
+    traffic(b);
+    // default off: measured slower than the graph loop on c1 (127 vs 91 us per CP
+    // iteration): one SM cannot hold c1's ~0.2 MB of blocks plus iterates in
+    // L1, so every warp-per-node body pays a chain of L2 round trips (~5 k
+    // cycles per node; SPOCK_SMALL_PROF=1 breakdown in DESIGN.md §5)
+    (void)b;
+    small_ok_ = env && env[0] == '1';
+  }
   CK(cudaStreamSynchronize(st_));
   mark("power iteration");
 }
@@ -1978,14 +1989,10 @@ void Engine::unscale_b(const double* zs, double* z) {  // solver.cpp:116-130
 // per-stage operator kernels cover the shape.  SPOCK_SMALL=0 disables it,
 // SPOCK_SMALL=1 forces it (tests).
 bool Engine::small_eligible() const {
-  const char* env = std::getenv("SPOCK_SMALL");
   const char* genv = std::getenv("SPOCK_SOLVE_GRAPH");  // 0: the host-driven loop (no device-resident loop)
-  if ((env && env[0] == '0') || (genv && genv[0] == '0')) return false;
+  if (genv && genv[0] == '0') return false;
   if (prm_.cancelled || prm_.aa_memory > kLoopMaxMem) return false;
-  if (env && env[0] == '1') return true;
-  double b[5];
-  traffic(b);
-  return b[4] <= kSmallBytes && p_.tree.nn() <= 4096;
+  return small_ok_;
 }
 
 const char* Engine::loop_path() const {
@@ -2046,8 +2053,19 @@ bool Engine::solve_small(const double* x_init, const double* wz, const double* w
   S0.n_L = 1;
   S0.k_stop = prm_.max_iters + 1;
   CK(cudaMemcpyAsync(A.L.st, &S0, sizeof(S0), cudaMemcpyHostToDevice, st_));
+  const char* pe = std::getenv("SPOCK_SMALL_PROF");
+  if (pe && pe[0] == '1' && !A.prof) {
+    A.prof = dalloc<unsigned long long>(8);
+  }
   launch_small_solve(A, st_);
   CK(cudaGetLastError());
+  if (A.prof) {
+    unsigned long long h[8];
+    CK(cudaMemcpyAsync(h, A.prof, sizeof(h), cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+    std::fprintf(stderr, "[small prof] cycles T %llu L %llu L* %llu red %llu gram %llu ctl %llu vec %llu other %llu\n",
+                 h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7]);
+  }
   LoopState Sh{};
   CK(cudaMemcpyAsync(&Sh, A.L.st, sizeof(Sh), cudaMemcpyDeviceToHost, st_));
   CK(cudaStreamSynchronize(st_));

@@ -92,6 +92,7 @@ class Engine {
   bool solve_small(const double* x_init, const double* wz, const double* we, double* oz, double* ozs, double* oe,
                    bool supermann, Status& st);
   SmallArgs small_{};
+  bool small_ok_ = false;  // decided at construction (SPOCK_SMALL=0/1 overrides)
   int small_cap_ = 0;
   void build_loop_graph(GraphLoop& G, bool supermann);
   double bench_T(int k, bool graph, bool flush);

@@ -1085,6 +1085,14 @@ void launch_s3(const Dev& D, double* eta, cudaStream_t st) {
 
 void launch_small_solve(const SmallArgs& A, cudaStream_t st) {
   static_assert(kSmallThreads == kSmallThreadsHost, "small solve block size");
+  // the per-node blocks are read through L1 every iteration: give the SM's
+  // unified L1 / shared memory to L1 (the kernel needs ~22 KB of shared memory)
+  static bool once = [] {
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(&k_small_solve), cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxL1);
+    return true;
+  }();
+  (void)once;
   k_small_solve<<<1, kSmallThreads, 0, st>>>(A);
 }
 

@@ -79,6 +79,7 @@ struct SmallArgs {
   double *TC, *PV, *Lrz, *cLrz, *Lsre, *tmpz, *tmpe;
   const double *d1, *d2;  // termination scalings
   int supermann;
+  unsigned long long* prof;  // optional [8] clock64 totals per phase class (SPOCK_SMALL_PROF=1)
 };
 void launch_small_solve(const SmallArgs& A, cudaStream_t st);
 constexpr int kSmallThreadsHost = 256;

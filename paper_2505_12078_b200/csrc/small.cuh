@@ -207,22 +207,39 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_solve(const __grid_c
   double *TC = A.TC, *PV = A.PV, *Lrz = A.Lrz, *cLrz = A.cLrz;
   const bool sm = A.supermann != 0;
   const int m = A.L.P.m;
+  long long tprev = clock64();
+  long long tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // T, L, L*, reductions, gram, controller, vector ops, other
+  auto tick = [&](int cls) {
+    if (A.prof && t == 0) {
+      const long long now = clock64();
+      tacc[cls] += now - tprev;
+      tprev = now;
+    }
+  };
   auto vec = [&](auto&& f) {
     for (int64_t i = t; i < nv; i += kSmallThreads) f(i);
     __syncthreads();
   };
   // r = v - T v, L r_z and the M-norm dots of (r, L r_z)
   auto refresh = [&](const double* v, double* tv, double* r, double* lrz) {
+    tick(7);
     cta_T(D, ss, v, v + nz, tv, tv + nz, alpha, xs);
+    tick(0);
     vec([&](int64_t i) { r[i] = v[i] - tv[i]; });
+    tick(6);
     cta_L(D, r, lrz, xs);
+    tick(1);
     cta_mnorm(r, lrz, nz, ne, wred, red);
+    tick(3);
   };
   refresh(V, TV, R, Lrz);  // prologue (solver.cpp:211-235)
   for (;;) {
     // top of the iteration: L* r_eta, xi norms, Anderson push and Gram
+    tick(7);
     cta_Lt(D, R + nz, nullptr, A.Lsre, 0.0, 1.0, 0.0, xs);
+    tick(2);
     cta_xi(R, A.Lsre, Lrz, A.d1, A.d2, nz, ne, alpha, wred, red + 4);
+    tick(3);
     if (sm) {
       const int hn = S.h + 1;
       double* rn = LA.RH[ring(hn, m + 1)];
@@ -234,10 +251,13 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_solve(const __grid_c
         dn[i] = first ? r : r - rp[i];
         rn[i] = r;
       });
+      tick(6);
       cta_gram(LA, S, wred, red + 8);
+      tick(4);
     }
     if (t == 0) ctl_begin<false>(LA);
     __syncthreads();
+    tick(5);
     if (S.sw == 0) break;
     if (sm) {  // psi = cpsi[0] r + sum_c cpsi[c] r_{k-1-c}
       const int h = S.h, nc = S.ncpsi;
@@ -293,4 +313,6 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_solve(const __grid_c
   }
   __syncthreads();
   if (t == 0) *A.L.st = S;
+  if (A.prof && t == 0)
+    for (int k = 0; k < 8; ++k) A.prof[k] += (unsigned long long)tacc[k];
 }

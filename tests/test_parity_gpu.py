@@ -163,7 +163,7 @@ def test_small_loop_matches_graph_loop(name, mk, method):
     from paper_2505_12078_b200.generators import make_config
     from paper_2505_12078_b200.solver import SpockSolver
     p = make_config("c1", seed=1) if mk is None else mk()
-    s = SpockSolver(p, max_iters=40, eps_abs=1e-14, eps_rel=1e-14)
+    s = _with_env({"SPOCK_SMALL": "1"}, lambda: SpockSolver(p, max_iters=40, eps_abs=1e-14, eps_rel=1e-14))
     assert s.loop_path == "small"
     g = _with_env({"SPOCK_SMALL": "0"}, lambda: SpockSolver(p, max_iters=40, eps_abs=1e-14, eps_rel=1e-14,
                                                               alpha=s.alpha))
@@ -182,11 +182,12 @@ def test_small_loop_bitwise_deterministic_and_warm_start():
     from paper_2505_12078_b200.generators import make_config
     from paper_2505_12078_b200.solver import SpockSolver
     p = make_config("c1", seed=1)
-    s = SpockSolver(p, max_iters=300)
+    s = _with_env({"SPOCK_SMALL": "1"}, lambda: SpockSolver(p, max_iters=300))
+    assert s.loop_path == "small"
     a, b = s.solve(), s.solve()
     assert np.array_equal(a.z, b.z) and np.array_equal(a.status["rnorm_history"], b.status["rnorm_history"])
-    w = SpockSolver(p, max_iters=50000, eps_abs=1e-6, eps_rel=1e-6)
+    w = _with_env({"SPOCK_SMALL": "1"}, lambda: SpockSolver(p, max_iters=50000, eps_abs=1e-6, eps_rel=1e-6))
     cold = w.solve_cp()
     warm = w.solve_cp(p.x_init, warm=(cold.z_scaled, cold.eta))
     assert cold.status["reason"] == warm.status["reason"] == "converged"
-    assert warm.status["iterations"] <= 2
+    assert warm.status["iterations"] <= cold.status["iterations"] // 4  # test_solver.cpp:373-384

@@ -14,13 +14,13 @@ def main():
     from paper_2505_12078_b200.generators import make_config
     from paper_2505_12078_b200.solver import SpockSolver
     cfg = sys.argv[1] if len(sys.argv) > 1 else "c1"
+    tols = [float(x) for x in sys.argv[2].split(",")] if len(sys.argv) > 2 else [1e-3, 1e-4, 1e-6]
     p = make_config(cfg, seed=1)
     for method in ("solve_cp", "solve"):
-        for tol in (1e-3, 1e-4, 1e-6):
+        for tol in tols:
             row = {"config": cfg, "method": method, "tol": tol}
             for path in ("small", "graph"):
-                if path == "graph":
-                    os.environ["SPOCK_SMALL"] = "0"
+                os.environ["SPOCK_SMALL"] = "1" if path == "small" else "0"
                 s = SpockSolver(p, max_iters=50000, eps_abs=tol, eps_rel=tol)
                 os.environ.pop("SPOCK_SMALL", None)
                 getattr(s, method)(p.x_init)
