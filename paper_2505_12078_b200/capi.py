@@ -184,6 +184,10 @@ def pack_problem(p: Raocp) -> PackedProblem:
 
 
 def _lib_path() -> str:
+    # SPOCK_LIB: an alternative in-tree build of the same library (tools/ A/B runs)
+    alt = os.environ.get("SPOCK_LIB")
+    if alt:
+        return alt
     here = os.path.dirname(os.path.abspath(__file__))
     return os.path.join(here, "_build", "libspock_b200.so")
 

@@ -8,6 +8,7 @@
 //   Engine::solve_b      <- SpockSolver::run           proj/src/solver.cpp:189-350
 #include "engine.hpp"
 #include "aa.cuh"
+#include "setup_dev.hpp"
 
 #include <chrono>
 #include <climits>
@@ -86,18 +87,27 @@ Engine::Engine(const spock_problem_desc* desc, const Params& prm) : prm_(prm) {
     t0 = t1;
   };
   prm_.validate();
-  raw_ = problem_from_desc(desc);
-  p_ = raw_;
+  p_ = problem_from_desc(desc);
+  raw_xinit_ = p_.x_init;  // the unscaled initial state (the solve default)
   mark("problem_from_desc");
   pc_ = prm_.use_preconditioner ? precondition_inplace(p_) : identity_precond(p_);
   mark("precondition");
-  soc_ = soc_epigraph_data(p_);
-  mark("soc_epigraph_data");
-  lay_ = make_layouts(p_, soc_);
   require(p_.nx + p_.nu <= kMaxD, "spock-b200: nx + nu above 256 is not supported");
-  stage_start_ = p_.tree.stage_start;
   CK(cudaGetDevice(&dev_));
   CK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+  {
+    // SOC epigraph data on the device (SPOCK_HOST_SOC=1: the host restatement)
+    const char* hs = std::getenv("SPOCK_HOST_SOC");
+    soc_dev_ = !(hs && hs[0] == '1') && p_.nx <= kEigMaxN && p_.tree.nn() > 1;
+    if (soc_dev_) {
+      soc_device_ranks();
+    } else {
+      soc_ = soc_epigraph_data(p_);
+    }
+  }
+  mark(soc_dev_ ? "soc ranks (device)" : "soc_epigraph_data");
+  lay_ = make_layouts(p_, soc_);
+  stage_start_ = p_.tree.stage_start;
   set_carveout_all();
   set_carveout_narrow();
   mark("layouts + stream");
@@ -666,6 +676,9 @@ void Engine::setup_wide(bool force) {
   if (occ < 1) return;
   // every CTA must be resident (items spin on flags of smaller tickets)
   wide_grid_ = occ * sms;
+  if (std::getenv("SPOCK_DEBUG_SETUP"))
+    std::fprintf(stderr, "[wide] rows %d ctas %d warps %d slots %d chunk %d vrec %d vecd %d smem %d B occ %d grid %d\n",
+                 wide_rows_, wide_ctas_, A.warps, A.slots, A.chunk, A.vrec, A.vecd, bytes, occ, wide_grid_);
   // latency configuration for launches with about one item per warp (standalone
   // L / L* on narrow trees): one CTA per SM, few warps, 16-slot rings so a
   // warp's whole item is requested at once instead of one chunk per round trip
@@ -1132,6 +1145,192 @@ Engine::~Engine() {
 }
 
 // ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------
+// Device-side SOC epigraph data (soc_data_quadlin, proj/src/problem.cpp:113-161,
+// per block of blkdiag(Q, R) as the host restatement soc_block in model.cpp).
+// Pass 1 (before the layouts): eigendecompositions of every Q_k, R_k, QN_j
+// (one CTA each) and, per node, the ranks, lambda_max and the merged row order
+// the boundary permutation needs.  Pass 2 (upload): S'MS, its square root by a
+// second eigendecomposition, the head maps H and H', q_kernel and the
+// translation a, written into the per-node layout.
+namespace {
+template <class Ty>
+Ty* tmp_alloc(std::vector<void*>& owned, size_t n) {
+  void* p = nullptr;
+  CK(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(Ty)));
+  owned.push_back(p);
+  return static_cast<Ty*>(p);
+}
+template <class Ty>
+Ty* tmp_upload(std::vector<void*>& owned, const Ty* h, size_t n, cudaStream_t st) {
+  Ty* d = tmp_alloc<Ty>(owned, n);
+  if (n) CK(cudaMemcpyAsync(d, h, n * sizeof(Ty), cudaMemcpyHostToDevice, st));
+  return d;
+}
+}  // namespace
+
+void Engine::soc_device_ranks() {
+  const Tree& tr = p_.tree;
+  const int nn = tr.nn(), nr = nn - 1, nl = tr.nl(), nx = p_.nx, nu = p_.nu;
+  SocScratch& S = socs_;
+  auto& own = S.owned;
+  S.Q = tmp_upload(own, p_.Q.data(), p_.Q.size(), st_);
+  S.R = tmp_upload(own, p_.R.data(), p_.R.size(), st_);
+  S.q = tmp_upload(own, p_.q.data(), p_.q.size(), st_);
+  S.r = tmp_upload(own, p_.r.data(), p_.r.size(), st_);
+  S.QN = tmp_upload(own, p_.QN.data(), p_.QN.size(), st_);
+  S.qN = tmp_upload(own, p_.qN.data(), p_.qN.size(), st_);
+  const int nbx = nr + nl;  // x blocks: stage Q_k, then terminal QN_j
+  S.Wx = tmp_alloc<double>(own, size_t(nbx) * nx);
+  S.Vx = tmp_alloc<double>(own, size_t(nbx) * nx * nx);
+  S.Wu = tmp_alloc<double>(own, size_t(nr) * nu);
+  S.Vu = tmp_alloc<double>(own, size_t(nr) * nu * nu);
+  CK(eig_configure(std::max(nx, nu)));
+  std::vector<EigJob> jx(static_cast<size_t>(nbx)), ju(static_cast<size_t>(nr));
+  for (int b = 0; b < nbx; ++b) {
+    const double* M = b < nr ? S.Q + size_t(b) * nx * nx : S.QN + size_t(b - nr) * nx * nx;
+    jx[b] = EigJob{M, S.Wx + size_t(b) * nx, S.Vx + size_t(b) * nx * nx, nx, 0};
+  }
+  for (int k = 0; k < nr; ++k) ju[k] = EigJob{S.R + size_t(k) * nu * nu, S.Wu + size_t(k) * nu,
+                                              S.Vu + size_t(k) * nu * nu, nu, 0};
+  std::vector<void*> jobs_own;
+  const EigJob* djx = tmp_upload(jobs_own, jx.data(), jx.size(), st_);
+  const EigJob* dju = tmp_upload(jobs_own, ju.data(), ju.size(), st_);
+  launch_sym_eig(djx, nbx, nx, st_);
+  CK(cudaGetLastError());
+  launch_sym_eig(dju, nr, nu, st_);
+  CK(cudaGetLastError());
+  // ranks, lambda_max, merged order
+  const int pw = nx + nu;
+  int* dpx = tmp_alloc<int>(jobs_own, size_t(nbx));
+  int* dpu = tmp_alloc<int>(jobs_own, size_t(nr));
+  int* dperm = tmp_alloc<int>(jobs_own, size_t(nbx) * pw);
+  double* dlm = tmp_alloc<double>(jobs_own, size_t(nbx));
+  int* derr = tmp_alloc<int>(jobs_own, 1);
+  CK(cudaMemsetAsync(derr, 0, sizeof(int), st_));
+  launch_soc_rank(SocRankArgs{S.Wx, S.Wu, nr, nx, nu, dpx, dpu, dperm, dlm, derr}, st_);
+  launch_soc_rank(SocRankArgs{S.Wx + size_t(nr) * nx, nullptr, nl, nx, nu, dpx + nr, nullptr,
+                              dperm + size_t(nr) * pw, dlm + nr, derr},
+                  st_);
+  CK(cudaGetLastError());
+  std::vector<int> hpx(nbx), hpu(std::max(nr, 1)), hperm(size_t(nbx) * pw);
+  std::vector<double> hlm(nbx);
+  int herr = 0;
+  CK(cudaMemcpyAsync(hpx.data(), dpx, sizeof(int) * nbx, cudaMemcpyDeviceToHost, st_));
+  if (nr) CK(cudaMemcpyAsync(hpu.data(), dpu, sizeof(int) * nr, cudaMemcpyDeviceToHost, st_));
+  CK(cudaMemcpyAsync(hperm.data(), dperm, sizeof(int) * hperm.size(), cudaMemcpyDeviceToHost, st_));
+  CK(cudaMemcpyAsync(hlm.data(), dlm, sizeof(double) * nbx, cudaMemcpyDeviceToHost, st_));
+  CK(cudaMemcpyAsync(&herr, derr, sizeof(int), cudaMemcpyDeviceToHost, st_));
+  CK(cudaStreamSynchronize(st_));
+  for (void* q : jobs_own) cudaFree(q);
+  require(herr == 0, "soc_data_quadlin: Q must be positive semidefinite");
+  soc_.stage.assign(static_cast<size_t>(nr), SocBlock{});
+  soc_.leaf.assign(static_cast<size_t>(nl), SocBlock{});
+  for (int k = 0; k < nr; ++k) {
+    SocBlock& b = soc_.stage[k];
+    b.px = hpx[k], b.pu = hpu[k], b.lambda_max = hlm[k];
+    b.perm.assign(hperm.begin() + size_t(k) * pw, hperm.begin() + size_t(k) * pw + b.px + b.pu);
+  }
+  for (int j = 0; j < nl; ++j) {
+    SocBlock& b = soc_.leaf[j];
+    b.px = hpx[nr + j], b.lambda_max = hlm[nr + j];
+    b.perm.resize(b.px);
+    for (int r = 0; r < b.px; ++r) b.perm[r] = r;
+  }
+}
+
+void Engine::soc_device_build(const std::vector<int64_t>& hxo, const std::vector<int64_t>& huo,
+                              const std::vector<int64_t>& ao, const std::vector<int64_t>& hno,
+                              const std::vector<int64_t>& aNo) {
+  const Tree& tr = p_.tree;
+  const int nn = tr.nn(), nr = nn - 1, nl = tr.nl(), nx = p_.nx, nu = p_.nu, pw = nx + nu;
+  SocScratch& S = socs_;
+  auto& own = S.owned;
+  const int nbx = nr + nl;
+  double* smsx = tmp_alloc<double>(own, size_t(nbx) * nx * nx);
+  double* u2x = tmp_alloc<double>(own, size_t(nbx) * nx * nx);
+  double* w2x = tmp_alloc<double>(own, size_t(nbx) * nx);
+  double* smsu = tmp_alloc<double>(own, size_t(nr) * nu * nu);
+  double* u2u = tmp_alloc<double>(own, size_t(nr) * nu * nu);
+  double* w2u = tmp_alloc<double>(own, size_t(nr) * nu);
+  double* wst = tmp_alloc<double>(own, size_t(nr) * pw);
+  double* wlf = tmp_alloc<double>(own, size_t(nl) * pw);
+  std::vector<SocBlockJob> jx(static_cast<size_t>(nbx)), ju(static_cast<size_t>(nr));
+  std::vector<EigJob> ex(static_cast<size_t>(nbx)), eu(static_cast<size_t>(nr));
+  for (int b = 0; b < nbx; ++b) {
+    SocBlockJob& J = jx[b];
+    const bool leaf = b >= nr;
+    const int k = leaf ? b - nr : b;
+    J.n = nx;
+    J.p = leaf ? soc_.leaf[k].px : soc_.stage[k].px;
+    J.M = leaf ? S.QN + size_t(k) * nx * nx : S.Q + size_t(k) * nx * nx;
+    J.v = leaf ? S.qN + size_t(k) * nx : S.q + size_t(k) * nx;
+    J.V = S.Vx + size_t(b) * nx * nx;
+    J.sms = smsx + size_t(b) * nx * nx;
+    J.U2 = u2x + size_t(b) * nx * nx;
+    J.W2 = w2x + size_t(b) * nx;
+    J.H = const_cast<double*>(leaf ? D_.HN + hno[k] : D_.Hx + hxo[k]);
+    J.HT = const_cast<double*>(leaf ? D_.HNT + hno[k] : D_.HxT + hxo[k]);
+    J.qk = const_cast<double*>(leaf ? D_.qkN + size_t(k) * nx : D_.qk + size_t(k) * pw);
+    J.w = leaf ? wlf + size_t(k) * pw : wst + size_t(k) * pw;
+    ex[b] = EigJob{J.sms, J.W2, J.U2, J.p, 0};
+  }
+  for (int k = 0; k < nr; ++k) {
+    SocBlockJob& J = ju[k];
+    J.n = nu;
+    J.p = soc_.stage[k].pu;
+    J.M = S.R + size_t(k) * nu * nu;
+    J.v = S.r + size_t(k) * nu;
+    J.V = S.Vu + size_t(k) * nu * nu;
+    J.sms = smsu + size_t(k) * nu * nu;
+    J.U2 = u2u + size_t(k) * nu * nu;
+    J.W2 = w2u + size_t(k) * nu;
+    J.H = const_cast<double*>(D_.Hu + huo[k]);
+    J.HT = const_cast<double*>(D_.HuT + huo[k]);
+    J.qk = const_cast<double*>(D_.qk + size_t(k) * pw + nx);
+    J.w = wst + size_t(k) * pw + nx;
+    eu[k] = EigJob{J.sms, J.W2, J.U2, J.p, 0};
+  }
+  const SocBlockJob* djx = tmp_upload(own, jx.data(), jx.size(), st_);
+  const SocBlockJob* dju = tmp_upload(own, ju.data(), ju.size(), st_);
+  const EigJob* dex = tmp_upload(own, ex.data(), ex.size(), st_);
+  const EigJob* deu = tmp_upload(own, eu.data(), eu.size(), st_);
+  launch_soc_sms(djx, nbx, nx, st_);
+  launch_soc_sms(dju, nr, nu, st_);
+  launch_sym_eig(dex, nbx, nx, st_);
+  launch_sym_eig(deu, nr, nu, st_);
+  launch_soc_build(djx, nbx, nx, st_);
+  launch_soc_build(dju, nr, nu, st_);
+  CK(cudaGetLastError());
+  // translations and |qk|^2 (analytic norm bound)
+  int* dpx = tmp_alloc<int>(own, size_t(nbx));
+  int* dpu = tmp_alloc<int>(own, size_t(std::max(nr, 1)));
+  {
+    std::vector<int> hpx(nbx), hpu(std::max(nr, 1));
+    for (int k = 0; k < nr; ++k) hpx[k] = soc_.stage[k].px, hpu[k] = soc_.stage[k].pu;
+    for (int j = 0; j < nl; ++j) hpx[nr + j] = soc_.leaf[j].px;
+    CK(cudaMemcpyAsync(dpx, hpx.data(), sizeof(int) * nbx, cudaMemcpyHostToDevice, st_));
+    CK(cudaMemcpyAsync(dpu, hpu.data(), sizeof(int) * hpu.size(), cudaMemcpyHostToDevice, st_));
+    CK(cudaStreamSynchronize(st_));  // host vectors go out of scope
+  }
+  const int64_t* dao = tmp_upload(own, ao.data(), ao.size(), st_);
+  const int64_t* daNo = tmp_upload(own, aNo.data(), aNo.size(), st_);
+  double* qk2 = tmp_alloc<double>(own, size_t(nbx));
+  launch_soc_tail(SocTailArgs{wst, dpx, dpu, dao, const_cast<double*>(D_.a), D_.qk, pw, qk2, nr, nx, nu}, st_);
+  launch_soc_tail(SocTailArgs{wlf, dpx + nr, nullptr, daNo, const_cast<double*>(D_.aN), D_.qkN, nx, qk2 + nr, nl,
+                              nx, nu},
+                  st_);
+  CK(cudaGetLastError());
+  std::vector<double> h2(nbx);
+  CK(cudaMemcpyAsync(h2.data(), qk2, sizeof(double) * nbx, cudaMemcpyDeviceToHost, st_));
+  CK(cudaStreamSynchronize(st_));
+  for (int k = 0; k < nr; ++k) soc_.stage[k].qk2 = h2[k];
+  for (int j = 0; j < nl; ++j) soc_.leaf[j].qk2 = h2[nr + j];
+  for (void* q : own) cudaFree(q);
+  own.clear();
+  S = SocScratch{};
+}
+
 void Engine::upload() {
   const Tree& tr = p_.tree;
   const int nn = tr.nn(), nnl = tr.nnl(), nl = tr.nl(), nr = nn - 1, nx = p_.nx, nu = p_.nu;
@@ -1155,6 +1354,7 @@ void Engine::upload() {
   D.s3_socdim = dupload(lay_.seg3_socdim);
 
   // stage-cost SOC data
+  std::vector<int64_t> shxo, shuo, sao;
   {
     std::vector<int> px(nr), pu(nr);
     std::vector<int64_t> hxo(nr), huo(nr), ao(nr);
@@ -1169,8 +1369,11 @@ void Engine::upload() {
       su += pad2(int64_t(pu[k]) * nu);
       sa += px[k] + pu[k] + 2;
     }
-    std::vector<double> Hx(sx), HxT(sx), Hu(su), HuT(su), qk(size_t(nr) * (nx + nu)), a(sa);
-    for (int k = 0; k < nr; ++k) {
+    std::vector<double> Hx, HxT, Hu, HuT, qk, a;
+    if (!soc_dev_) {
+      Hx.resize(sx), HxT.resize(sx), Hu.resize(su), HuT.resize(su), qk.resize(size_t(nr) * (nx + nu)), a.resize(sa);
+    }
+    for (int k = 0; k < nr && !soc_dev_; ++k) {
       const SocBlock& b = soc_.stage[k];
       for (int j = 0; j < nx; ++j)
         for (int r = 0; r < b.px; ++r) {
@@ -1191,13 +1394,23 @@ void Engine::upload() {
     D.pu = dupload(pu);
     D.hx_off = dupload(hxo);
     D.hu_off = dupload(huo);
-    D.Hx = dupload(Hx);
-    D.HxT = dupload(HxT);
-    D.Hu = dupload(Hu);
-    D.HuT = dupload(HuT);
-    D.qk = dupload(qk);
     D.a_off = dupload(ao);
-    D.a = dupload(a);
+    if (soc_dev_) {
+      D.Hx = dalloc<double>(sx);
+      D.HxT = dalloc<double>(sx);
+      D.Hu = dalloc<double>(su);
+      D.HuT = dalloc<double>(su);
+      D.qk = dalloc<double>(size_t(nr) * (nx + nu));
+      D.a = dalloc<double>(sa);
+    } else {
+      D.Hx = dupload(Hx);
+      D.HxT = dupload(HxT);
+      D.Hu = dupload(Hu);
+      D.HuT = dupload(HuT);
+      D.qk = dupload(qk);
+      D.a = dupload(a);
+    }
+    shxo = std::move(hxo), shuo = std::move(huo), sao = std::move(ao);
   }
   // terminal SOC data
   {
@@ -1211,8 +1424,9 @@ void Engine::upload() {
       sh += pad2(int64_t(pN[j]) * nx);
       sa += pN[j] + 2;
     }
-    std::vector<double> HN(sh), HNT(sh), qk(size_t(nl) * nx), a(sa);
-    for (int j = 0; j < nl; ++j) {
+    std::vector<double> HN, HNT, qk, a;
+    if (!soc_dev_) HN.resize(sh), HNT.resize(sh), qk.resize(size_t(nl) * nx), a.resize(sa);
+    for (int j = 0; j < nl && !soc_dev_; ++j) {
       const SocBlock& b = soc_.leaf[j];
       for (int c = 0; c < nx; ++c)
         for (int r = 0; r < b.px; ++r) {
@@ -1225,11 +1439,19 @@ void Engine::upload() {
     }
     D.pN = dupload(pN);
     D.hn_off = dupload(ho);
-    D.HN = dupload(HN);
-    D.HNT = dupload(HNT);
-    D.qkN = dupload(qk);
     D.aN_off = dupload(ao);
-    D.aN = dupload(a);
+    if (soc_dev_) {
+      D.HN = dalloc<double>(sh);
+      D.HNT = dalloc<double>(sh);
+      D.qkN = dalloc<double>(size_t(nl) * nx);
+      D.aN = dalloc<double>(sa);
+      soc_device_build(shxo, shuo, sao, ho, ao);
+    } else {
+      D.HN = dupload(HN);
+      D.HNT = dupload(HNT);
+      D.qkN = dupload(qk);
+      D.aN = dupload(a);
+    }
   }
   // boundary permutation of eta (stage SOC head rows)
   {
@@ -1247,27 +1469,30 @@ void Engine::upload() {
   }
   // constraints
   {
-    bool gdiag = true;
-    for (int i = 0; i < nnl && gdiag; ++i) {
+    std::vector<uint8_t> nd(static_cast<size_t>(std::max(nnl, 1)), 0);  // node i: [Gx Gu] not square diagonal
+    parallel_for(nnl, [&](int64_t ii) {
+      const int i = int(ii);
       if (p_.nc[i] != nx + nu) {
-        gdiag = false;
-        break;
+        nd[i] = 1;
+        return;
       }
       const size_t o = size_t(p_.g_off[i]);
       const int nc = p_.nc[i];
-      for (int c = 0; c < nx && gdiag; ++c)
+      for (int c = 0; c < nx; ++c)
         for (int r = 0; r < nc; ++r)
           if (r != c && p_.Gx[o * nx + r + size_t(c) * nc] != 0.0) {
-            gdiag = false;
-            break;
+            nd[i] = 1;
+            return;
           }
-      for (int c = 0; c < nu && gdiag; ++c)
+      for (int c = 0; c < nu; ++c)
         for (int r = 0; r < nc; ++r)
           if (r != nx + c && p_.Gu[o * nu + r + size_t(c) * nc] != 0.0) {
-            gdiag = false;
-            break;
+            nd[i] = 1;
+            return;
           }
-    }
+    });
+    bool gdiag = true;
+    for (int i = 0; i < nnl; ++i) gdiag = gdiag && !nd[i];
     D.g_diag = gdiag ? 1 : 0;
     const int64_t rows = p_.g_off[nnl];
     std::vector<int64_t> goff(p_.g_off.begin(), p_.g_off.end() - 1);
@@ -1276,12 +1501,13 @@ void Engine::upload() {
     D.hi = dupload(p_.C_hi);
     if (gdiag) {
       std::vector<double> gd(size_t(nnl) * (nx + nu));
-      for (int i = 0; i < nnl; ++i) {
+      parallel_for(nnl, [&](int64_t ii) {
+        const int i = int(ii);
         const size_t o = size_t(p_.g_off[i]);
         const int nc = p_.nc[i];
         for (int r = 0; r < nx; ++r) gd[size_t(i) * (nx + nu) + r] = p_.Gx[o * nx + r + size_t(r) * nc];
         for (int r = 0; r < nu; ++r) gd[size_t(i) * (nx + nu) + nx + r] = p_.Gu[o * nu + nx + r + size_t(r) * nc];
-      }
+      });
       D.gd = dupload(gd);
     } else {
       std::vector<double> GxT(size_t(rows) * nx), GuT(size_t(rows) * nu);
@@ -1516,7 +1742,7 @@ void Engine::upload() {
     scratch_z_[t] = dalloc<double>(lay_.nz);
     scratch_e_[t] = dalloc<double>(lay_.neta);
   }
-  set_xinit(raw_.x_init.data());
+  set_xinit(raw_xinit_.data());
 }
 
 void Engine::set_xinit(const double* x) {
@@ -1558,13 +1784,9 @@ void Engine::factorize() {
   tmp.push_back(derr);
   CK(cudaMemsetAsync(derr, 0, sizeof(int), st_));
   // leaves: P = I
-  {
-    std::vector<double> I(size_t(nn) * nx * nx, 0.0);
-    for (int j = tr.stage_start[N]; j < nn; ++j)
-      for (int k = 0; k < nx; ++k) I[size_t(j) * nx * nx + k + size_t(k) * nx] = 1.0;
-    CK(cudaMemcpyAsync(P, I.data(), sizeof(double) * I.size(), cudaMemcpyHostToDevice, st_));
-    CK(cudaStreamSynchronize(st_));
-  }
+  CK(cudaMemsetAsync(P, 0, sizeof(double) * size_t(nn) * nx * nx, st_));
+  launch_eye(P + size_t(tr.stage_start[N]) * nx * nx, nn - tr.stage_start[N], nx, st_);
+  CK(cudaGetLastError());
   // pointer arrays for batched GEMMs (rebuilt per stage)
   const size_t maxw = size_t(nr) + 1;
   const double** hA = new const double*[maxw];
@@ -1705,9 +1927,9 @@ void Engine::launch_wide(WideArgs A, const WRec* recs, int ntick) {
   A.ntick = ntick;
   if (ntick <= wide_grid_lat_ * wlat_.warps) {
     A.warps = wlat_.warps, A.slots = wlat_.slots;
-    launch_T_wide(A, wide_rows_, 1, std::min(wide_grid_lat_, (ntick + A.warps - 1) / A.warps), st_);
+    CK(launch_T_wide(A, wide_rows_, 1, std::min(wide_grid_lat_, (ntick + A.warps - 1) / A.warps), st_));
   } else {
-    launch_T_wide(A, wide_rows_, wide_ctas_, std::min(wide_grid_, (ntick + A.warps - 1) / A.warps), st_);
+    CK(launch_T_wide(A, wide_rows_, wide_ctas_, std::min(wide_grid_, (ntick + A.warps - 1) / A.warps), st_));
   }
 }
 
@@ -1798,7 +2020,7 @@ void Engine::T(const double* z, const double* eta, double* zo, double* eo) {
     }
     A.recs = wargs_.recs;
     A.ntick = wargs_.ntick;
-    launch_T_wide(A, wide_rows_, wide_ctas_, wide_grid_, st_);
+    CK(launch_T_wide(A, wide_rows_, wide_ctas_, wide_grid_, st_));
     CK(cudaGetLastError());
     return;
   }
@@ -2008,7 +2230,7 @@ bool Engine::solve_small(const double* x_init, const double* wz, const double* w
   if (!small_eligible()) return false;
   const int m = prm_.aa_memory;
   const int64_t nz = lay_.nz, ne = lay_.neta, nv = nz + ne;
-  set_xinit(x_init ? x_init : raw_.x_init.data());
+  set_xinit(x_init ? x_init : raw_xinit_.data());
   SmallArgs& A = small_;
   if (!A.L.V) {  // buffers, built once per engine
     auto pair = [&]() { return dalloc<double>(size_t(nv)); };
@@ -2114,7 +2336,7 @@ bool Engine::solve_graph(const double* x_init, const double* wz, const double* w
   const char* env = std::getenv("SPOCK_SOLVE_GRAPH");
   if (env && env[0] == '0') return false;
   const int64_t nz = lay_.nz, ne = lay_.neta, nv = nz + ne;
-  set_xinit(x_init ? x_init : raw_.x_init.data());
+  set_xinit(x_init ? x_init : raw_xinit_.data());
   GraphLoop& G = gloop_[supermann ? 1 : 0];
   if (!G.exec) build_loop_graph(G, supermann);
   const LoopArgs& A = G.A;
@@ -2349,7 +2571,7 @@ void Engine::solve_b(const double* x_init, const double* wz, const double* we, d
   if (!sharded && solve_small(x_init, wz, we, oz, ozs, oe, supermann, st)) return;
   if (!sharded && solve_graph(x_init, wz, we, oz, ozs, oe, supermann, st)) return;
   const int64_t nz = lay_.nz, ne = lay_.neta, nv = nz + ne;
-  set_xinit(x_init ? x_init : raw_.x_init.data());
+  set_xinit(x_init ? x_init : raw_xinit_.data());
   const int m = prm_.aa_memory;
   // pair buffers: [z | eta] contiguous so Anderson works on the stacked vector
   std::vector<double*> bufs;

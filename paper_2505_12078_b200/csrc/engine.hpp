@@ -129,6 +129,19 @@ class Engine {
 
  private:
   void upload();
+  // device-side SOC epigraph data (setup_dev.cu): eigenvalues,
+  // ranks and the merged row order first (the layouts need the ranks), then
+  // the head maps, kernel components and translations straight into D_
+  bool soc_dev_ = false;
+  struct SocScratch {
+    double *Q = nullptr, *R = nullptr, *q = nullptr, *r = nullptr, *QN = nullptr, *qN = nullptr;
+    double *Wx = nullptr, *Vx = nullptr, *Wu = nullptr, *Vu = nullptr;
+    std::vector<void*> owned;
+  } socs_;
+  void soc_device_ranks();
+  void soc_device_build(const std::vector<int64_t>& hxo, const std::vector<int64_t>& huo,
+                        const std::vector<int64_t>& ao, const std::vector<int64_t>& hno,
+                        const std::vector<int64_t>& aNo);
   void setup_fused();
   void setup_wide(bool force);
   void factorize();
@@ -151,7 +164,8 @@ class Engine {
   Ty* dupload(const std::vector<Ty>& h);
 
   Params prm_;
-  Problem raw_, p_;
+  Problem p_;
+  Vec raw_xinit_;
   Precond pc_;
   SocData soc_;
   Layouts lay_;

@@ -202,7 +202,20 @@ bool chol_pd(const double* M, int n) {
 void Problem::validate() const {  // proj/src/problem.cpp:39-86
   const int nn = tree.nn(), nnl = tree.nnl(), nl = tree.nl();
   require(nx > 0 && nu > 0, "Raocp: dimensions must be positive");
+  // per-node checks on host threads; the first failing node (in node order)
+  // raises the reference's exception on this thread
+  std::vector<uint8_t> bad(static_cast<size_t>(std::max(nn - 1, 1)), 0);
+  host_parallel(nn - 1, [&](int64_t k) {
+    try {
+      check_symmetric(&Q[size_t(k) * nx * nx], nx, "Raocp Q");
+      check_symmetric(&R[size_t(k) * nu * nu], nu, "Raocp R");
+      if (!chol_pd(&R[size_t(k) * nu * nu], nu)) bad[k] = 1;
+    } catch (const std::invalid_argument&) {
+      bad[k] = 1;
+    }
+  });
   for (int i = 1; i < nn; ++i) {
+    if (!bad[i - 1]) continue;
     check_symmetric(&Q[size_t(i - 1) * nx * nx], nx, "Raocp Q");
     check_symmetric(&R[size_t(i - 1) * nu * nu], nu, "Raocp R");
     require(chol_pd(&R[size_t(i - 1) * nu * nu], nu), "Raocp: R must be positive definite");
@@ -213,8 +226,16 @@ void Problem::validate() const {  // proj/src/problem.cpp:39-86
     for (int k = 0; k < nc[i]; ++k)
       require(C_lo[box_off[i] + k] <= C_hi[box_off[i] + k], "Box: lower bound above upper bound");
   }
+  std::vector<uint8_t> badN(static_cast<size_t>(std::max(nl, 1)), 0);
+  host_parallel(nl, [&](int64_t j) {
+    try {
+      check_symmetric(&QN[size_t(j) * nx * nx], nx, "Raocp QN");
+    } catch (const std::invalid_argument&) {
+      badN[j] = 1;
+    }
+  });
   for (int j = 0; j < nl; ++j) {
-    check_symmetric(&QN[size_t(j) * nx * nx], nx, "Raocp QN");
+    if (badN[j]) check_symmetric(&QN[size_t(j) * nx * nx], nx, "Raocp QN");
     for (int k = 0; k < ncN[j]; ++k)
       require(CN_lo[boxN_off[j] + k] <= CN_hi[boxN_off[j] + k], "Box: lower bound above upper bound");
   }
@@ -241,7 +262,14 @@ Problem problem_from_desc(const spock_problem_desc* d) {
   const size_t nx = P.nx, nu = P.nu, nr = nn - 1, nnl = t.nnl(), nl = t.nl();
   auto cp = [](const double* s, size_t n) {
     require(n == 0 || s != nullptr, "Raocp: missing data array");
-    return Vec(s, s + n);
+    Vec v(n);
+    // large per-node arrays (c4: GBs): copy in parallel slabs
+    const int64_t slab = int64_t(1) << 20;
+    host_parallel((int64_t(n) + slab - 1) / slab, [&](int64_t b) {
+      const size_t o = size_t(b) * slab;
+      std::memcpy(v.data() + o, s + o, sizeof(double) * std::min<size_t>(slab, n - o));
+    });
+    return v;
   };
   P.A = cp(d->A, nr * nx * nx);
   P.B = cp(d->B, nr * nx * nu);
@@ -380,56 +408,53 @@ Precond precondition_inplace(Problem& p) {  // proj/src/problem.cpp:249-326
       for (int r = 0; r < nx; ++r) Q[r + jj * nx] = isxN[r] * Q[r + jj * nx] * isxN[jj];
     for (int r = 0; r < nx; ++r) p.qN[size_t(j) * nx + r] *= isxN[r];
   }
-  // per non-leaf constraint row scaling by max(1, ||[Gx/sx Gu/su]||_2); the
-  // spectral norm is memoised by content (generators share G across nodes)
+  // per non-leaf constraint row scaling by max(1, ||[Gx/sx Gu/su]||_2), per node
+  // on host threads.  When every row of the scaled block has at most one
+  // nonzero (box selectors: every generated problem) the columns have disjoint
+  // supports, S'S is diagonal and the norm is the largest column norm; else
+  // the dense S'S and its largest eigenvalue
   pc.cstr_scale.assign(nnl, 1.0);
-  std::unordered_map<uint64_t, int> memo;
-  std::vector<int> rep(nnl);
-  for (int i = 0; i < nnl; ++i) {
-    const size_t o = size_t(p.g_off[i]);
-    uint64_t h = fnv(&p.Gx[o * nx], sizeof(double) * size_t(p.nc[i]) * nx, uint64_t(p.nc[i]) * 7919);
-    h = fnv(&p.Gu[o * nu], sizeof(double) * size_t(p.nc[i]) * nu, h);
-    auto it = memo.find(h);
-    if (it != memo.end() && p.nc[it->second] == p.nc[i] &&
-        std::memcmp(&p.Gx[size_t(p.g_off[it->second]) * nx], &p.Gx[o * nx], sizeof(double) * p.nc[i] * nx) == 0 &&
-        std::memcmp(&p.Gu[size_t(p.g_off[it->second]) * nu], &p.Gu[o * nu], sizeof(double) * p.nc[i] * nu) == 0) {
-      rep[i] = it->second;
-    } else {
-      memo[h] = i;
-      rep[i] = i;
-    }
-  }
   host_parallel(nnl, [&](int64_t ii) {
     const int i = int(ii);
-    if (rep[i] != i) return;
     const int nc = p.nc[i], m = nx + nu;
     const size_t o = size_t(p.g_off[i]);
-    Mat S(nc, m);
-    for (int j = 0; j < nx; ++j)
-      for (int r = 0; r < nc; ++r) S(r, j) = p.Gx[(o + 0) * nx + r + size_t(j) * nc] * isx[j];
-    for (int j = 0; j < nu; ++j)
-      for (int r = 0; r < nc; ++r) S(r, nx + j) = p.Gu[o * nu + r + size_t(j) * nc] * isu[j];
-    Mat G(m, m);
-    bool diag = true;
-    for (int j = 0; j < m; ++j)
-      for (int k = 0; k < m; ++k) {
-        double s = 0.0;
-        for (int r = 0; r < nc; ++r) s += S(r, j) * S(r, k);
-        G(j, k) = s;
-        if (j != k && s != 0.0) diag = false;
-      }
+    auto S = [&](int r, int j) {
+      return j < nx ? p.Gx[o * nx + r + size_t(j) * nc] * isx[j] : p.Gu[o * nu + r + size_t(j - nx) * nc] * isu[j - nx];
+    };
+    bool sel = true;
+    for (int r = 0; r < nc && sel; ++r) {
+      int nz = 0;
+      for (int j = 0; j < m; ++j) nz += S(r, j) != 0.0;
+      sel = nz <= 1;
+    }
     double emax = 0.0;
-    if (diag) {
-      for (int j = 0; j < m; ++j) emax = std::max(emax, G(j, j));
+    if (sel) {
+      for (int j = 0; j < m; ++j) {
+        double s2 = 0.0;
+        for (int r = 0; r < nc; ++r) s2 += S(r, j) * S(r, j);
+        emax = std::max(emax, s2);
+      }
     } else {
-      Vec w;
-      Mat V;
-      sym_eig(G, w, V);
-      emax = w.empty() ? 0.0 : w.back();
+      Mat G(m, m);
+      bool diag = true;
+      for (int j = 0; j < m; ++j)
+        for (int k = 0; k < m; ++k) {
+          double s2 = 0.0;
+          for (int r = 0; r < nc; ++r) s2 += S(r, j) * S(r, k);
+          G(j, k) = s2;
+          if (j != k && s2 != 0.0) diag = false;
+        }
+      if (diag) {
+        for (int j = 0; j < m; ++j) emax = std::max(emax, G(j, j));
+      } else {
+        Vec w;
+        Mat V;
+        sym_eig(G, w, V);
+        emax = w.empty() ? 0.0 : w.back();
+      }
     }
     pc.cstr_scale[i] = std::max(1.0, std::sqrt(std::max(0.0, emax)));
   });
-  for (int i = 0; i < nnl; ++i) pc.cstr_scale[i] = pc.cstr_scale[rep[i]];
   host_parallel(nnl, [&](int64_t ii) {
     const int i = int(ii), nc = p.nc[i];
     const size_t o = size_t(p.g_off[i]);
@@ -570,6 +595,8 @@ SocBlock soc_block(const double* Q, int nx, const double* R, int nu, const doubl
   return out;
 }
 
+void parallel_for(int64_t n, const std::function<void(int64_t)>& f) { host_parallel(n, f); }
+
 SocData soc_epigraph_data(const Problem& p) {  // proj/src/problem.cpp:216-236
   const int nn = p.tree.nn(), nnl = p.tree.nnl(), nl = p.tree.nl(), nx = p.nx, nu = p.nu;
   SocData d;
@@ -705,8 +732,11 @@ double analytic_norm_bound(const Problem& p, const SocData& soc) {
   const int nn = tr.nn(), nnl = tr.nnl(), nx = p.nx, nu = p.nu;
   int max_ch = 1;
   for (int i = 0; i < nnl; ++i) max_ch = std::max(max_ch, tr.child_count[i]);
-  double mx = 0.0;
-  for (int i = 0; i < nn; ++i) {
+  // per-node maxima on host threads, then one max (order-independent)
+  std::vector<double> per(static_cast<size_t>(nn), 0.0);
+  host_parallel(nn, [&](int64_t ii) {
+    const int i = int(ii);
+    double mx = 0.0;
     if (i < nnl) {
       mx = std::max(mx, 1.0);
       double bb = 0.0;
@@ -720,19 +750,28 @@ double analytic_norm_bound(const Problem& p, const SocData& soc) {
     }
     if (i > 0) {
       const auto& d = soc.stage[i - 1];
-      double qq = 0.0;
-      for (double v : d.qk) qq += v * v;
+      double qq = d.qk2;
+      if (qq < 0.0) {
+        qq = 0.0;
+        for (double v : d.qk) qq += v * v;
+      }
       mx = std::max(mx, std::sqrt(d.lambda_max + 0.5 * (1.0 + qq)));
     }
     if (i >= nnl) {
       const int j = i - nnl;
       const auto& d = soc.leaf[j];
       mx = std::max(mx, holder(&p.GN[size_t(p.gN_off[j]) * nx], p.ncN[j], nx));
-      double qq = 0.0;
-      for (double v : d.qk) qq += v * v;
+      double qq = d.qk2;
+      if (qq < 0.0) {
+        qq = 0.0;
+        for (double v : d.qk) qq += v * v;
+      }
       mx = std::max(mx, std::sqrt(d.lambda_max + 0.5 * (1.0 + qq)));
     }
-  }
+    per[size_t(i)] = mx;
+  });
+  double mx = 0.0;
+  for (double v : per) mx = std::max(mx, v);
   return std::sqrt(1.0 + double(max_ch)) * mx;
 }
 

@@ -19,6 +19,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <functional>
 #include <vector>
 
 #include "../../include/spock_b200.h"
@@ -94,6 +95,7 @@ struct SocBlock {
   Vec a;                    // translation, internal row order [x rows; u rows; 2]
   std::vector<int> perm;    // perm[k] = boundary row of internal head row k
   double lambda_max = 0.0;
+  double qk2 = -1.0;         // |qk|^2 when qk itself stays on the device (device-side setup)
 };
 SocBlock soc_block(const double* Q, int nx, const double* R, int nu, const double* q, const double* r);
 
@@ -101,6 +103,9 @@ struct SocData {
   std::vector<SocBlock> stage, leaf;
 };
 SocData soc_epigraph_data(const Problem& p);
+// parallel loop over [0, n) on host threads (setup only; every index must
+// write its own slot)
+void parallel_for(int64_t n, const std::function<void(int64_t)>& f);
 
 struct Layouts {
   // primal (layout.cpp:5-30)

@@ -109,7 +109,7 @@ cudaError_t wide_configure(int rows, int ctas, int smem_bytes) {
 // is cooperative, which makes the runtime guarantee co-residency (or fail the
 // launch) even when other kernels -- a concurrent solver's stream, another
 // process under MPS -- hold part of the device.
-void launch_T_wide(const WideArgs& A, int rows, int ctas, int grid, cudaStream_t st) {
+cudaError_t launch_T_wide(const WideArgs& A, int rows, int ctas, int grid, cudaStream_t st) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(32 * A.warps);
@@ -121,11 +121,11 @@ void launch_T_wide(const WideArgs& A, int rows, int ctas, int grid, cudaStream_t
   cfg.attrs = at;
   cfg.numAttrs = 1;
   switch (rows) {
-    case 1: wide_launch_r1(&cfg, ctas, A); break;
-    case 2: wide_launch_r2(&cfg, ctas, A); break;
-    case 3: wide_launch_r3(&cfg, ctas, A); break;
-    case 4: wide_launch_r4(&cfg, ctas, A); break;
-    default: wide_launch_r8(&cfg, ctas, A); break;
+    case 1: return wide_launch_r1(&cfg, ctas, A);
+    case 2: return wide_launch_r2(&cfg, ctas, A);
+    case 3: return wide_launch_r3(&cfg, ctas, A);
+    case 4: return wide_launch_r4(&cfg, ctas, A);
+    default: return wide_launch_r8(&cfg, ctas, A);
   }
 }
 

@@ -90,6 +90,6 @@ int wide_smem_bytes(const WideArgs& A);
 int wide_rows(const Dev& D, int max_nc);  // register row groups (template parameter)
 cudaError_t wide_configure(int rows, int ctas, int smem_bytes);
 const void* wide_kernel_ptr(int rows, int ctas);
-void launch_T_wide(const WideArgs& A, int rows, int ctas, int grid, cudaStream_t st);
+cudaError_t launch_T_wide(const WideArgs& A, int rows, int ctas, int grid, cudaStream_t st);
 
 }  // namespace spock
