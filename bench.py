@@ -495,7 +495,7 @@ def main():
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(args.config, {}).get("dram_bytes_per_launch")
+            traffic = json.load(open(tp)).get(args.config, {}).get("T")
         except Exception:
             traffic = None
     o = None

@@ -68,6 +68,11 @@ Ty* Engine::dalloc(size_t n) {
   allocs_.push_back(p);
   return static_cast<Ty*>(p);
 }
+double* Engine::dupload(const BigVec& h) {
+  double* d = dalloc<double>(h.size());
+  if (!h.empty()) CK(cudaMemcpyAsync(d, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice, st_));
+  return d;
+}
 template <class Ty>
 Ty* Engine::dupload(const std::vector<Ty>& h) {
   Ty* d = dalloc<Ty>(h.size());

@@ -162,6 +162,7 @@ class Engine {
   Ty* dalloc(size_t n);
   template <class Ty>
   Ty* dupload(const std::vector<Ty>& h);
+  double* dupload(const BigVec& h);
 
   Params prm_;
   Problem p_;

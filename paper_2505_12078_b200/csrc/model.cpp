@@ -241,6 +241,14 @@ void Problem::validate() const {  // proj/src/problem.cpp:39-86
   }
 }
 
+BigVec::BigVec(const double* src, size_t count) : p(count ? new double[count] : nullptr), n(count) {
+  const int64_t slab = int64_t(1) << 20;
+  host_parallel((int64_t(count) + slab - 1) / slab, [&](int64_t b) {
+    const size_t o = size_t(b) * slab;
+    std::memcpy(p.get() + o, src + o, sizeof(double) * std::min<size_t>(slab, count - o));
+  });
+}
+
 Problem problem_from_desc(const spock_problem_desc* d) {
   require(d != nullptr, "spock: null problem description");
   Problem P;
@@ -262,23 +270,20 @@ Problem problem_from_desc(const spock_problem_desc* d) {
   const size_t nx = P.nx, nu = P.nu, nr = nn - 1, nnl = t.nnl(), nl = t.nl();
   auto cp = [](const double* s, size_t n) {
     require(n == 0 || s != nullptr, "Raocp: missing data array");
-    Vec v(n);
-    // large per-node arrays (c4: GBs): copy in parallel slabs
-    const int64_t slab = int64_t(1) << 20;
-    host_parallel((int64_t(n) + slab - 1) / slab, [&](int64_t b) {
-      const size_t o = size_t(b) * slab;
-      std::memcpy(v.data() + o, s + o, sizeof(double) * std::min<size_t>(slab, n - o));
-    });
-    return v;
+    return Vec(s, s + n);
   };
-  P.A = cp(d->A, nr * nx * nx);
-  P.B = cp(d->B, nr * nx * nu);
+  auto big = [](const double* s, size_t n) {
+    require(n == 0 || s != nullptr, "Raocp: missing data array");
+    return BigVec(s, n);
+  };
+  P.A = big(d->A, nr * nx * nx);
+  P.B = big(d->B, nr * nx * nu);
   P.c = cp(d->c, nr * nx);
-  P.Q = cp(d->Q, nr * nx * nx);
-  P.R = cp(d->R, nr * nu * nu);
+  P.Q = big(d->Q, nr * nx * nx);
+  P.R = big(d->R, nr * nu * nu);
   P.q = cp(d->q, nr * nx);
   P.r = cp(d->r, nr * nu);
-  P.QN = cp(d->QN, nl * nx * nx);
+  P.QN = big(d->QN, nl * nx * nx);
   P.qN = cp(d->qN, nl * nx);
   P.nc.assign(d->nc, d->nc + nnl);
   P.ncN.assign(d->ncN, d->ncN + nl);
@@ -294,8 +299,8 @@ Problem problem_from_desc(const spock_problem_desc* d) {
   }
   P.g_off[nnl] = go;
   P.box_off[nnl] = bo;
-  P.Gx = cp(d->Gx, size_t(go) * nx);
-  P.Gu = cp(d->Gu, size_t(go) * nu);
+  P.Gx = big(d->Gx, size_t(go) * nx);
+  P.Gu = big(d->Gu, size_t(go) * nu);
   P.C_lo = cp(d->C_lo, bo);
   P.C_hi = cp(d->C_hi, bo);
   P.gN_off.resize(nl + 1);
@@ -310,7 +315,7 @@ Problem problem_from_desc(const spock_problem_desc* d) {
   }
   P.gN_off[nl] = go;
   P.boxN_off[nl] = bo;
-  P.GN = cp(d->GN, size_t(go) * nx);
+  P.GN = big(d->GN, size_t(go) * nx);
   P.CN_lo = cp(d->CN_lo, bo);
   P.CN_hi = cp(d->CN_hi, bo);
   const double *E = d->risk_E, *F = d->risk_F, *b = d->risk_b, *pi = d->risk_pi;

@@ -64,14 +64,40 @@ struct Risk {
 };
 
 // Raw problem (host copy of the spock_problem_desc), per-node blocks packed.
+// Large per-node arrays of the problem (GBs on wide trees): an uninitialised
+// allocation filled by parallel slab copies -- std::vector would zero-fill
+// the whole range on one thread first
+struct BigVec {
+  std::unique_ptr<double[]> p;
+  size_t n = 0;
+  BigVec() = default;
+  BigVec(const double* src, size_t count);
+  BigVec(BigVec&&) = default;
+  BigVec& operator=(BigVec&&) = default;
+  BigVec(const BigVec& o) : BigVec(o.data(), o.n) {}
+  BigVec& operator=(const BigVec& o) {
+    if (this != &o) *this = BigVec(o.data(), o.n);
+    return *this;
+  }
+  double* data() { return p.get(); }
+  const double* data() const { return p.get(); }
+  size_t size() const { return n; }
+  bool empty() const { return n == 0; }
+  double& operator[](size_t i) { return p[i]; }
+  const double& operator[](size_t i) const { return p[i]; }
+};
+
 struct Problem {
   Tree tree;
   int nx = 0, nu = 0;
-  Vec A, B, c, Q, R, q, r;  // per non-root, stride nx*nx etc.
-  Vec QN, qN;               // per leaf
+  BigVec A, B, Q, R;        // per non-root, stride nx*nx etc.
+  Vec c, q, r;
+  BigVec QN;                // per leaf
+  Vec qN;
   std::vector<int> nc, ncN;
   std::vector<int64_t> g_off, gN_off, box_off, boxN_off;  // offsets into Gx/Gu (by rows) and boxes
-  Vec Gx, Gu, C_lo, C_hi, GN, CN_lo, CN_hi;
+  BigVec Gx, Gu, GN;
+  Vec C_lo, C_hi, CN_lo, CN_hi;
   std::vector<Risk> risk;
   Vec x_init;
   void validate() const;
