@@ -54,6 +54,15 @@ extern "C" {
 #define SPOCK_STALLED 2
 #define SPOCK_CANCELLED 3
 
+/* spock_problem_desc.layout flags (extensions; 0 = the reference's layout).
+ * ROW_MAJOR: the per-node blocks A, B, Q, R, QN, Gx, Gu, GN are row-major (C
+ *   order, e.g. numpy stacks) instead of column-major.
+ * SHARED_G: Gx / Gu hold ONE block shared by every non-leaf node and GN one
+ *   block shared by every leaf (every nc[i] equal, every ncN[j] equal; the
+ *   generators' box selectors, generators.cpp:99-109). */
+#define SPOCK_LAYOUT_ROW_MAJOR 1
+#define SPOCK_LAYOUT_SHARED_G 2
+
 /* Flat description of a Raocp (proj/include/spock/problem.hpp:29-58) on a
  * ScenarioTree given by raw arrays (ScenarioTree::from_arrays,
  * proj/include/spock/tree.hpp:72-74).  All pointers are host memory. */
@@ -99,6 +108,7 @@ typedef struct spock_problem_desc {
   const int32_t* cone_kind;   /* packed parts */
   const int32_t* cone_dim;    /* packed parts */
   const double* x_init;       /* nx */
+  int32_t layout;             /* SPOCK_LAYOUT_* flags */
 } spock_problem_desc;
 
 /* SpockParams, proj/include/spock/solver.hpp:15-35.  std::function callbacks

@@ -97,7 +97,7 @@ class OracleSolver:
     def __init__(self, problem, progress=None, cancelled=None, **params):
         self.L = lib()
         self.problem = problem
-        self.packed = capi.pack_problem(problem)
+        self.packed = capi.pack_problem(problem, fast=False)  # the reference's column-major layout
         prm = capi.default_params(**params)
         self._cbs = []
         if progress is not None:

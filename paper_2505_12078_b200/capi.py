@@ -35,7 +35,11 @@ class ProblemDesc(C.Structure):
         ("risk_E", _D), ("risk_F", _D), ("risk_b", _D), ("risk_gamma", _D), ("risk_pi", _D),
         ("cone_nparts", _I), ("cone_kind", _I), ("cone_dim", _I),
         ("x_init", _D),
+        ("layout", C.c_int32),
     ]
+
+
+SPOCK_LAYOUT_ROW_MAJOR, SPOCK_LAYOUT_SHARED_G = 1, 2
 
 
 PROGRESS_FN = C.CFUNCTYPE(None, C.c_int32, C.c_double, C.c_char, C.c_void_p)
@@ -117,10 +121,34 @@ def _flat(vecs) -> np.ndarray:
     return out if out.size else np.zeros(1)
 
 
-class PackedProblem:
-    """spock_problem_desc plus the buffers it points into."""
+def _rowmajor_stack(mats) -> np.ndarray:
+    """Per-node matrices back to back in C order (no copy for a C-contiguous stack)."""
+    if isinstance(mats, np.ndarray) and mats.ndim == 3:
+        if mats.shape[0] == 0:
+            return np.zeros(1)
+        return np.ascontiguousarray(mats, dtype=np.float64).reshape(-1)
+    parts = [np.asarray(m, dtype=np.float64).reshape(-1) for m in mats]
+    return np.concatenate(parts) if parts and sum(p.size for p in parts) else np.zeros(1)
 
-    def __init__(self, p: Raocp):
+
+def _shared_block(mats):
+    """The one block of a per-node stack that repeats a single matrix
+    (np.broadcast_to: stride 0 on the node axis), else None."""
+    if isinstance(mats, np.ndarray) and mats.ndim == 3 and mats.shape[0] > 0 and mats.strides[0] == 0:
+        return np.ascontiguousarray(mats[0], dtype=np.float64).reshape(-1)
+    return None
+
+
+class PackedProblem:
+    """spock_problem_desc plus the buffers it points into.
+
+    ``fast`` (the product's default) passes numpy stacks as they are: row-major
+    blocks (SPOCK_LAYOUT_ROW_MAJOR, transposed by the library on host threads)
+    and one shared constraint block when G is a broadcast (SPOCK_LAYOUT_SHARED_G);
+    ``fast=False`` packs the reference's column-major layout (the oracle reads
+    only that)."""
+
+    def __init__(self, p: Raocp, fast: bool = True):
         tr = p.tree
         self.keep = []
         d = ProblemDesc()
@@ -136,24 +164,34 @@ class PackedProblem:
         d.event = _i(K(np.ascontiguousarray(tr.event, dtype=np.int32)))
         d.prob = _d(K(np.ascontiguousarray(tr.prob, dtype=np.float64)))
         d.cond_prob = _d(K(np.ascontiguousarray(tr.cond_prob, dtype=np.float64)))
-        d.A = _d(K(_colmajor_stack(p.A)))
-        d.B = _d(K(_colmajor_stack(p.B)))
+        stack = _rowmajor_stack if fast else _colmajor_stack
+        d.layout = SPOCK_LAYOUT_ROW_MAJOR if fast else 0
+        d.A = _d(K(stack(p.A)))
+        d.B = _d(K(stack(p.B)))
         d.c = _d(K(_flat(p.c)))
-        d.Q = _d(K(_colmajor_stack(p.Q)))
-        d.R = _d(K(_colmajor_stack(p.R)))
+        d.Q = _d(K(stack(p.Q)))
+        d.R = _d(K(stack(p.R)))
         d.q = _d(K(_flat(p.q)))
         d.r = _d(K(_flat(p.r)))
-        d.QN = _d(K(_colmajor_stack(p.QN)))
+        d.QN = _d(K(stack(p.QN)))
         d.qN = _d(K(_flat(p.qN)))
         nc = np.array([b.dim() for b in p.C], dtype=np.int32)
         d.nc = _i(K(nc if nc.size else np.zeros(1, np.int32)))
-        d.Gx = _d(K(_colmajor_stack(p.Gx)))
-        d.Gu = _d(K(_colmajor_stack(p.Gu)))
+        ncN_ = np.array([b.dim() for b in p.CN], dtype=np.int32)
+        shared = None
+        if fast:
+            sh = [_shared_block(p.Gx), _shared_block(p.Gu), _shared_block(p.GN)]
+            if all(x is not None for x in sh) and nc.size and ncN_.size and (nc == nc[0]).all() \
+                    and (ncN_ == ncN_[0]).all():
+                shared = sh
+                d.layout |= SPOCK_LAYOUT_SHARED_G
+        d.Gx = _d(K(shared[0] if shared else stack(p.Gx)))
+        d.Gu = _d(K(shared[1] if shared else stack(p.Gu)))
         d.C_lo = _d(K(_flat([b.lo for b in p.C])))
         d.C_hi = _d(K(_flat([b.hi for b in p.C])))
         ncN = np.array([b.dim() for b in p.CN], dtype=np.int32)
         d.ncN = _i(K(ncN if ncN.size else np.zeros(1, np.int32)))
-        d.GN = _d(K(_colmajor_stack(p.GN)))
+        d.GN = _d(K(shared[2] if shared else stack(p.GN)))
         d.CN_lo = _d(K(_flat([b.lo for b in p.CN])))
         d.CN_hi = _d(K(_flat([b.hi for b in p.CN])))
         rk = np.array([r.kind for r in p.risk], dtype=np.int32)
@@ -179,8 +217,8 @@ class PackedProblem:
         return C.byref(self.desc)
 
 
-def pack_problem(p: Raocp) -> PackedProblem:
-    return PackedProblem(p)
+def pack_problem(p: Raocp, fast: bool = True) -> PackedProblem:
+    return PackedProblem(p, fast)
 
 
 def _lib_path() -> str:

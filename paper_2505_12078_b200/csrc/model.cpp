@@ -249,6 +249,31 @@ BigVec::BigVec(const double* src, size_t count) : p(count ? new double[count] : 
   });
 }
 
+BigVec BigVec::transposed(const double* src, size_t nb, int rows, int cols) {
+  BigVec v;
+  const size_t bs = size_t(rows) * cols;
+  v.n = nb * bs;
+  v.p.reset(v.n ? new double[v.n] : nullptr);
+  double* dst = v.p.get();
+  host_parallel(int64_t(nb), [&](int64_t b) {
+    const double* s = src + size_t(b) * bs;
+    double* o = dst + size_t(b) * bs;
+    for (int j = 0; j < cols; ++j)
+      for (int i = 0; i < rows; ++i) o[i + size_t(j) * rows] = s[size_t(i) * cols + j];
+  });
+  return v;
+}
+
+BigVec BigVec::repeated(const double* blk, size_t nb, int rows, int cols) {
+  BigVec v;
+  const size_t bs = size_t(rows) * cols;
+  v.n = nb * bs;
+  v.p.reset(v.n ? new double[v.n] : nullptr);
+  double* dst = v.p.get();
+  host_parallel(int64_t(nb), [&](int64_t b) { std::memcpy(dst + size_t(b) * bs, blk, sizeof(double) * bs); });
+  return v;
+}
+
 Problem problem_from_desc(const spock_problem_desc* d) {
   require(d != nullptr, "spock: null problem description");
   Problem P;
@@ -272,18 +297,21 @@ Problem problem_from_desc(const spock_problem_desc* d) {
     require(n == 0 || s != nullptr, "Raocp: missing data array");
     return Vec(s, s + n);
   };
-  auto big = [](const double* s, size_t n) {
-    require(n == 0 || s != nullptr, "Raocp: missing data array");
-    return BigVec(s, n);
+  require((d->layout & ~(SPOCK_LAYOUT_ROW_MAJOR | SPOCK_LAYOUT_SHARED_G)) == 0, "Raocp: unknown layout flags");
+  const bool rowm = (d->layout & SPOCK_LAYOUT_ROW_MAJOR) != 0;
+  // nb per-node blocks of rows x cols, column-major in the problem
+  auto big = [&](const double* s, size_t nb, int rows, int cols) {
+    require(nb == 0 || s != nullptr, "Raocp: missing data array");
+    return rowm ? BigVec::transposed(s, nb, rows, cols) : BigVec(s, nb * size_t(rows) * cols);
   };
-  P.A = big(d->A, nr * nx * nx);
-  P.B = big(d->B, nr * nx * nu);
+  P.A = big(d->A, nr, int(nx), int(nx));
+  P.B = big(d->B, nr, int(nx), int(nu));
   P.c = cp(d->c, nr * nx);
-  P.Q = big(d->Q, nr * nx * nx);
-  P.R = big(d->R, nr * nu * nu);
+  P.Q = big(d->Q, nr, int(nx), int(nx));
+  P.R = big(d->R, nr, int(nu), int(nu));
   P.q = cp(d->q, nr * nx);
   P.r = cp(d->r, nr * nu);
-  P.QN = big(d->QN, nl * nx * nx);
+  P.QN = big(d->QN, nl, int(nx), int(nx));
   P.qN = cp(d->qN, nl * nx);
   P.nc.assign(d->nc, d->nc + nnl);
   P.ncN.assign(d->ncN, d->ncN + nl);
@@ -299,8 +327,35 @@ Problem problem_from_desc(const spock_problem_desc* d) {
   }
   P.g_off[nnl] = go;
   P.box_off[nnl] = bo;
-  P.Gx = big(d->Gx, size_t(go) * nx);
-  P.Gu = big(d->Gu, size_t(go) * nu);
+  // constraint blocks: nc[i] x cols per node at row offset off[i]
+  auto gbig = [&](const double* s, const std::vector<int>& ncv, const std::vector<int64_t>& off, int cols) {
+    const size_t nb = ncv.size();
+    const int64_t rows_total = off[nb];
+    require(rows_total == 0 || s != nullptr, "Raocp: missing data array");
+    if (d->layout & SPOCK_LAYOUT_SHARED_G) {
+      const int r0 = nb ? ncv[0] : 0;
+      for (size_t i = 0; i < nb; ++i) require(ncv[i] == r0, "Raocp: shared constraint block needs equal row counts");
+      std::vector<double> blk(size_t(r0) * cols);
+      for (int j = 0; j < cols; ++j)
+        for (int i = 0; i < r0; ++i) blk[i + size_t(j) * r0] = rowm ? s[size_t(i) * cols + j] : s[i + size_t(j) * r0];
+      return BigVec::repeated(blk.data(), nb, r0, cols);
+    }
+    if (!rowm) return BigVec(s, size_t(rows_total) * cols);
+    BigVec v(nullptr, 0);
+    v.n = size_t(rows_total) * cols;
+    v.p.reset(v.n ? new double[v.n] : nullptr);
+    double* dst = v.p.get();
+    host_parallel(int64_t(nb), [&](int64_t b) {
+      const int r = ncv[b];
+      const double* sb = s + size_t(off[b]) * cols;
+      double* o = dst + size_t(off[b]) * cols;
+      for (int j = 0; j < cols; ++j)
+        for (int i = 0; i < r; ++i) o[i + size_t(j) * r] = sb[size_t(i) * cols + j];
+    });
+    return v;
+  };
+  P.Gx = gbig(d->Gx, P.nc, P.g_off, int(nx));
+  P.Gu = gbig(d->Gu, P.nc, P.g_off, int(nu));
   P.C_lo = cp(d->C_lo, bo);
   P.C_hi = cp(d->C_hi, bo);
   P.gN_off.resize(nl + 1);
@@ -315,7 +370,7 @@ Problem problem_from_desc(const spock_problem_desc* d) {
   }
   P.gN_off[nl] = go;
   P.boxN_off[nl] = bo;
-  P.GN = big(d->GN, size_t(go) * nx);
+  P.GN = gbig(d->GN, P.ncN, P.gN_off, int(nx));
   P.CN_lo = cp(d->CN_lo, bo);
   P.CN_hi = cp(d->CN_hi, bo);
   const double *E = d->risk_E, *F = d->risk_F, *b = d->risk_b, *pi = d->risk_pi;

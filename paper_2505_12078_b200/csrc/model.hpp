@@ -79,6 +79,10 @@ struct BigVec {
     if (this != &o) *this = BigVec(o.data(), o.n);
     return *this;
   }
+  // count = nb blocks of rows x cols; src row-major per block -> column-major
+  static BigVec transposed(const double* src, size_t nb, int rows, int cols);
+  // nb copies of one column-major block of rows x cols
+  static BigVec repeated(const double* blk, size_t nb, int rows, int cols);
   double* data() { return p.get(); }
   const double* data() const { return p.get(); }
   size_t size() const { return n; }

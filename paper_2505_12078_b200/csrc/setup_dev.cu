@@ -39,7 +39,7 @@ __device__ __forceinline__ void rr_pair(int n2, int round, int k, int& p, int& q
   }
 }
 
-__global__ void k_sym_eig(const EigJob* __restrict__ jobs) {
+__global__ void __launch_bounds__(1024) k_sym_eig(const EigJob* __restrict__ jobs) {
   extern __shared__ __align__(16) double esm[];
   const EigJob J = jobs[blockIdx.x];
   const int n = J.n;
@@ -184,7 +184,7 @@ __global__ void k_soc_rank(const SocRankArgs A) {
 }
 
 // SMS = S' M S with S = V(:, n-p..n): T = M S (n x p) in shared memory, then S'T
-__global__ void k_soc_sms(const SocBlockJob* __restrict__ jobs) {
+__global__ void __launch_bounds__(1024) k_soc_sms(const SocBlockJob* __restrict__ jobs) {
   extern __shared__ __align__(16) double ssm[];
   const SocBlockJob J = jobs[blockIdx.x];
   const int n = J.n, p = J.p, tid = threadIdx.x, nt = blockDim.x;
@@ -208,7 +208,7 @@ __global__ void k_soc_sms(const SocBlockJob* __restrict__ jobs) {
 
 // sq = U diag(sqrt e) U', isq = U diag(1/sqrt e) U'; H = sq S', qk = v - S S'v,
 // w = isq S'v
-__global__ void k_soc_build(const SocBlockJob* __restrict__ jobs) {
+__global__ void __launch_bounds__(1024) k_soc_build(const SocBlockJob* __restrict__ jobs) {
   extern __shared__ __align__(16) double bsm[];
   const SocBlockJob J = jobs[blockIdx.x];
   const int n = J.n, p = J.p, tid = threadIdx.x, nt = blockDim.x;
@@ -286,7 +286,9 @@ __global__ void k_eye(double* P, int64_t count, int n) {
   P[size_t(b) * n * n + k + size_t(k) * n] = 1.0;
 }
 
-int threads_for(int n) { return n <= 32 ? 64 : (n <= 64 ? 128 : 256); }
+// a Jacobi round updates n2/2 column pairs of n2 entries (then as many rows):
+// enough threads that a round is one or two passes
+int threads_for(int n) { return n <= 32 ? 128 : (n <= 64 ? 512 : 1024); }
 
 }  // namespace
 

@@ -10,11 +10,13 @@ const void* wide_ptr_r1(int ctas);
 const void* wide_ptr_r2(int ctas);
 const void* wide_ptr_r3(int ctas);
 const void* wide_ptr_r4(int ctas);
+const void* wide_ptr_r5(int ctas);
 const void* wide_ptr_r8(int ctas);
 cudaError_t wide_launch_r1(const cudaLaunchConfig_t* cfg, int ctas, const WideArgs& A);
 cudaError_t wide_launch_r2(const cudaLaunchConfig_t* cfg, int ctas, const WideArgs& A);
 cudaError_t wide_launch_r3(const cudaLaunchConfig_t* cfg, int ctas, const WideArgs& A);
 cudaError_t wide_launch_r4(const cudaLaunchConfig_t* cfg, int ctas, const WideArgs& A);
+cudaError_t wide_launch_r5(const cudaLaunchConfig_t* cfg, int ctas, const WideArgs& A);
 cudaError_t wide_launch_r8(const cudaLaunchConfig_t* cfg, int ctas, const WideArgs& A);
 
 namespace {
@@ -81,6 +83,7 @@ int wide_rows(const Dev& D, int max_nc) {
   if (r <= 2) return 2;
   if (r <= 3) return 3;
   if (r <= 4) return 4;
+  if (r <= 5) return 5;  // n_x + n_u = 150 (c5: n_x 100, n_u 50)
   return 8;
 }
 
@@ -90,6 +93,7 @@ const void* wide_kernel_ptr(int rows, int ctas) {
     case 2: return wide_ptr_r2(ctas);
     case 3: return wide_ptr_r3(ctas);
     case 4: return wide_ptr_r4(ctas);
+    case 5: return wide_ptr_r5(ctas);
     default: return wide_ptr_r8(ctas);
   }
 }
@@ -125,6 +129,7 @@ cudaError_t launch_T_wide(const WideArgs& A, int rows, int ctas, int grid, cudaS
     case 2: return wide_launch_r2(&cfg, ctas, A);
     case 3: return wide_launch_r3(&cfg, ctas, A);
     case 4: return wide_launch_r4(&cfg, ctas, A);
+    case 5: return wide_launch_r5(&cfg, ctas, A);
     default: return wide_launch_r8(&cfg, ctas, A);
   }
 }

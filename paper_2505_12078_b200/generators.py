@@ -132,6 +132,11 @@ CONFIGS = {
     "c2p": dict(N=10, nb=8, nw=2, nx=50, nu=25, gamma=None, perturb=0.01),
     "c3": dict(N=12, nb=8, nw=3, nx=50, nu=25, gamma=None, perturb=0.01),
     "c4": dict(N=12, nb=4, nw=10, nx=50, nu=25, gamma=None, perturb=0.01),
+    # configs[4] at one GPU's scale: the c5 state size (n_x 100 = 2 n_u)
+    # on a (12, 4, 7) tree of 103 765 nodes (~56 GB of per-node blocks on the device)
+    "c5s": dict(N=12, nb=7, nw=4, nx=100, nu=50, gamma=None, perturb=0.01),
+    # n_x = 100 tree small enough for the CPU oracle's parity checks (9 557 nodes, wide path)
+    "c5p": dict(N=7, nb=6, nw=4, nx=100, nu=50, gamma=None, perturb=0.01),
 }
 
 

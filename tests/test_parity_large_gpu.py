@@ -24,6 +24,7 @@ CASES = [
     ("c4", "c4", {}, "wide"),
     ("shape-12-100-2", "c4", dict(N=12, nw=100, nb=2), "wide"),
     ("shape-100-10-3", "c4", dict(N=100, nw=10, nb=3), "wide"),
+    ("c5p", "c5p", {}, "wide"),  # n_x = 100, n_u = 50 (the c5 state size): 5 row groups per lane
 ]
 TOL = 1e-10  # relative to the output's max |entry|: fp64, different (fixed) summation orders
 
