@@ -18,7 +18,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-Wno-deprecated-gpu-targets", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr"]
 SOURCES = ["model.cpp", "kernels.cu", "narrow.cu", "fused.cu", "wide.cu", "wide_r1.cu", "wide_r2.cu", "wide_r3.cu", "wide_r4.cu", "wide_r5.cu", "wide_r8.cu", "lop.cu", "loop.cu", "setup_dev.cu", "engine.cu", "capi.cu"]
-HEADERS = ["aa.cuh", "model.hpp", "dev.cuh", "kernels.hpp", "fused.hpp", "fused_impl.cuh", "wide.hpp", "wide_impl.cuh", "loop.hpp", "loop_ctl.cuh", "small.cuh", "engine.hpp", "setup_dev.hpp", os.path.join("..", "..", "include", "spock_b200.h")]
+HEADERS = ["aa.cuh", "model.hpp", "dev.cuh", "kernels.hpp", "fused.hpp", "fused_impl.cuh", "wide.hpp", "wide_impl.cuh", "loop.hpp", "loop_ctl.cuh", "small.cuh", "cluster.cuh", "engine.hpp", "setup_dev.hpp", os.path.join("..", "..", "include", "spock_b200.h")]
 
 
 def _newest_header() -> float:

@@ -206,8 +206,8 @@ __device__ __forceinline__ void warp_gemv(const double* __restrict__ A, int m, i
     for (int k = 0; k < kMaxR; ++k) {
       const int r = l + 32 * k;
       if (k * 32 < m && r < m) {
-        const double a0 = __ldg(c0 + r), a1 = __ldg(c0 + lda + r), a2 = __ldg(c0 + 2 * lda + r),
-                     a3 = __ldg(c0 + 3 * lda + r);
+        const double a0 = c0[r], a1 = c0[lda + r], a2 = c0[2 * lda + r],
+                     a3 = c0[3 * lda + r];
         acc[k] = fma(a0, x0, acc[k]);
         acc[k] = fma(a1, x1, acc[k]);
         acc[k] = fma(a2, x2, acc[k]);
@@ -221,7 +221,7 @@ __device__ __forceinline__ void warp_gemv(const double* __restrict__ A, int m, i
 #pragma unroll
     for (int k = 0; k < kMaxR; ++k) {
       const int r = l + 32 * k;
-      if (k * 32 < m && r < m) acc[k] = fma(__ldg(col + r), xc, acc[k]);
+      if (k * 32 < m && r < m) acc[k] = fma(col[r], xc, acc[k]);
     }
   }
 }

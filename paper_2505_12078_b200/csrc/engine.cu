@@ -63,9 +63,11 @@ template <class Ty>
 Ty* Engine::dalloc(size_t n) {
   void* p = nullptr;
   // two spare elements: aligned 16-byte bulk copies of a trailing odd element stay in bounds
-  CK(cudaMalloc(&p, (std::max<size_t>(n, 1) + 2) * sizeof(Ty)));
-  CK(cudaMemsetAsync(p, 0, (std::max<size_t>(n, 1) + 2) * sizeof(Ty), st_));
+  const size_t bytes = (std::max<size_t>(n, 1) + 2) * sizeof(Ty);
+  CK(cudaMalloc(&p, bytes));
+  CK(cudaMemsetAsync(p, 0, bytes, st_));
   allocs_.push_back(p);
+  alloc_bytes_[reinterpret_cast<uintptr_t>(p)] = bytes;
   return static_cast<Ty*>(p);
 }
 double* Engine::dupload(const BigVec& h) {
@@ -140,8 +142,19 @@ Engine::Engine(const spock_problem_desc* desc, const Params& prm) : prm_(prm) {
     // iteration): one SM cannot hold c1's ~0.2 MB of blocks plus iterates in
     // L1, so every warp-per-node body pays a chain of L2 round trips (~5 k
     // cycles per node; SPOCK_SMALL_PROF=1 breakdown in DESIGN.md §5)
-    (void)b;
     small_ok_ = env && env[0] == '1';
+    // cluster-resident loop: on when the small loop's whole device image fits
+    // in the shared memory of a cluster (SPOCK_CLUSTER=0 disables it)
+    const char* cenv = std::getenv("SPOCK_CLUSTER");
+    const int64_t nv = lay_.nz + lay_.neta;
+    const double image = b[4] + 8.0 * double(nv) * (13 + 2 * prm_.aa_memory);
+    int cl_ok = 0;
+    CK(cudaDeviceGetAttribute(&cl_ok, cudaDevAttrClusterLaunch, dev_));
+    if (!small_ok_ && !(cenv && cenv[0] == '0') && cl_ok && prm_.aa_memory <= kLoopMaxMem &&
+        image < double(kClusterMax) * 150e3) {
+      small_alloc();
+      cluster_ok_ = cluster_plan(prm_.aa_memory);
+    }
   }
   CK(cudaStreamSynchronize(st_));
   mark("power iteration");
@@ -2219,15 +2232,151 @@ bool Engine::small_eligible() const {
   const char* genv = std::getenv("SPOCK_SOLVE_GRAPH");  // 0: the host-driven loop (no device-resident loop)
   if (genv && genv[0] == '0') return false;
   if (prm_.cancelled || prm_.aa_memory > kLoopMaxMem) return false;
-  return small_ok_;
+  return small_ok_ || cluster_ok_;
+}
+
+// Pointer fields of SmallArgs the cluster solve relocates into shared memory
+// (f: the field, writable: copied back to HBM after the solve).
+template <class F>
+static void for_each_small_ptr(SmallArgs& A, int m, F&& f) {
+  Dev& D = A.D;
+  // (auto&: a reference to the pointer field itself, not to a converted temporary)
+  auto c = [&](auto& p) { f(static_cast<const void**>(static_cast<void*>(&p)), false); };
+  auto w = [&](auto& p) { f(static_cast<const void**>(static_cast<void*>(&p)), true); };
+  c(D.anc), c(D.cf), c(D.cc), c(D.y_off), c(D.y_dim), c(D.s1_off), c(D.s1_nc), c(D.s1_ydim), c(D.s2_off);
+  c(D.s2_dim), c(D.s3_off), c(D.s3_nc), c(D.s3_socdim), c(D.px), c(D.pu), c(D.hx_off), c(D.hu_off), c(D.Hx);
+  c(D.HxT), c(D.Hu), c(D.HuT), c(D.qk), c(D.a_off), c(D.a), c(D.pN), c(D.hn_off), c(D.HN), c(D.HNT), c(D.qkN);
+  c(D.aN_off), c(D.aN), c(D.gd), c(D.g_off), c(D.Gx), c(D.Gu), c(D.GxT), c(D.GuT), c(D.lo), c(D.hi), c(D.gNd);
+  c(D.gN_off), c(D.GN), c(D.GNT), c(D.loN), c(D.hiN), c(D.rb), c(D.yc_nonneg), c(D.yc_poff), c(D.yc_kind);
+  c(D.yc_dim), c(D.s2_kind), c(D.s2_gamma), c(D.s2p_off), c(D.s2P), c(D.M1), c(D.M1T), c(D.cvec), c(D.K);
+  c(D.KT), c(D.Rinv), c(D.g), c(D.h), c(D.xinit);
+  w(D.T12), w(D.adj), w(D.dvec);
+  c(A.stage_start), c(A.d1), c(A.d2);
+  w(A.TC), w(A.PV), w(A.Lrz), w(A.cLrz), w(A.Lsre), w(A.tmpz), w(A.tmpe);
+  LoopArgs& L = A.L;
+  w(L.V), w(L.TV), w(L.R), w(L.C), w(L.CR), w(L.PSI);
+  for (int j = 0; j <= m; ++j) w(L.RH[j]);
+  for (int j = 0; j < m; ++j) w(L.DH[j]);
+}
+
+// Pack the allocations the small loop touches into the shared memory of a
+// cluster of CTAs (first fit, largest first; whole allocations per CTA) and
+// upload the placement and relocation tables.  False: does not fit.
+bool Engine::cluster_plan(int m) {
+  if (cplace_d_ && cplan_m_ == m) return true;
+  SmallArgs A = small_;
+  int dev = 0, smem_optin = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  const int cap = ((smem_optin - cluster_static_smem() - 1024) / 16) * 16;
+  if (cap <= 0) return false;
+  struct Al {
+    uintptr_t base;
+    size_t bytes;
+    bool wr;
+    int cta, off;
+  };
+  std::vector<Al> al;
+  std::vector<std::pair<int, std::pair<int, int64_t>>> fld;  // field offset -> (alloc index, delta)
+  bool ok = true;
+  for_each_small_ptr(A, m, [&](const void** f, bool wr) {
+    const uintptr_t p = reinterpret_cast<uintptr_t>(*f);
+    if (!p || !ok) return;
+    auto it = alloc_bytes_.upper_bound(p);
+    if (it == alloc_bytes_.begin()) {
+      ok = false;
+      return;
+    }
+    --it;
+    if (p >= it->first + it->second) {
+      ok = false;
+      return;
+    }
+    int idx = -1;
+    for (size_t k = 0; k < al.size(); ++k)
+      if (al[k].base == it->first) idx = int(k);
+    if (idx < 0) {
+      al.push_back(Al{it->first, (it->second + 15) & ~size_t(15), wr, -1, 0});
+      idx = int(al.size()) - 1;
+    }
+    al[idx].wr = al[idx].wr || wr;
+    fld.push_back({int(reinterpret_cast<const char*>(f) - reinterpret_cast<const char*>(&A)),
+                   {idx, int64_t(p - it->first)}});
+  });
+  if (!ok) return false;
+  std::vector<int> order(al.size());
+  for (size_t k = 0; k < al.size(); ++k) order[k] = int(k);
+  std::sort(order.begin(), order.end(), [&](int x, int y) { return al[x].bytes > al[y].bytes; });
+  auto pack = [&](int C) {
+    std::vector<size_t> used(size_t(C), 0);
+    for (int k : order) {
+      int best = -1;
+      for (int c = 0; c < C; ++c)  // least-filled CTA that fits: spreads the DSMEM traffic
+        if (used[c] + al[k].bytes <= size_t(cap) && (best < 0 || used[c] < used[best])) best = c;
+      if (best < 0) return size_t(0);
+      al[k].cta = best;
+      al[k].off = int(used[best]);
+      used[best] += al[k].bytes;
+    }
+    size_t mx = 0;
+    for (size_t u : used) mx = std::max(mx, u);
+    return std::max<size_t>(mx, 16);
+  };
+  int C = 0;
+  size_t arena = 0;
+  const char* ce = std::getenv("SPOCK_CLUSTER_CTAS");
+  int want = ce && ce[0] ? std::atoi(ce) : 4;
+  want = std::max(1, std::min(kClusterMax, want));
+  for (int c = want; c <= kClusterMax && !arena; ++c) {
+    arena = pack(c);
+    if (arena) C = c;
+  }
+  if (!arena) return false;
+  std::vector<ClusterPlace> pl(al.size());
+  for (size_t k = 0; k < al.size(); ++k)
+    pl[k] = ClusterPlace{reinterpret_cast<const char*>(al[k].base), int64_t(al[k].bytes), al[k].cta, al[k].off,
+                         al[k].wr ? 1 : 0, 0};
+  std::vector<ClusterField> fl(fld.size());
+  for (size_t k = 0; k < fld.size(); ++k) fl[k] = ClusterField{fld[k].first, fld[k].second.first, fld[k].second.second};
+  cplace_d_ = dupload(pl);
+  cfield_d_ = dupload(fl);
+  cplace_n_ = int(pl.size());
+  cfield_n_ = int(fl.size());
+  cluster_ctas_ = C;
+  cluster_arena_ = int(arena);
+  cplan_m_ = m;
+  CK(cudaStreamSynchronize(st_));
+  return true;
 }
 
 const char* Engine::loop_path() const {
   if (shard_.on && shard_.coll) return "host";
-  if (small_eligible()) return "small";
+  if (small_eligible()) return cluster_ok_ ? "cluster" : "small";
   const char* env = std::getenv("SPOCK_SOLVE_GRAPH");
   if (prm_.cancelled || prm_.aa_memory > kLoopMaxMem || (env && env[0] == '0')) return "host";
   return "graph";
+}
+
+void Engine::small_alloc() {
+  SmallArgs& A = small_;
+  if (A.L.V) return;  // buffers, built once per engine
+  const int64_t nz = lay_.nz, ne = lay_.neta, nv = nz + ne;
+  auto pair = [&]() { return dalloc<double>(size_t(nv)); };
+  A.L.V = pair(), A.L.TV = pair(), A.L.R = pair(), A.L.C = pair(), A.L.CR = pair(), A.L.PSI = pair();
+  A.TC = pair(), A.PV = pair();
+  A.Lrz = dalloc<double>(size_t(ne));
+  A.cLrz = dalloc<double>(size_t(ne));
+  A.Lsre = dalloc<double>(size_t(nz));
+  A.tmpz = dalloc<double>(size_t(nz));
+  A.tmpe = dalloc<double>(size_t(ne));
+  for (int j = 0; j < kLoopMaxMem + 1; ++j) A.L.RH[j] = pair();
+  for (int j = 0; j < kLoopMaxMem; ++j) A.L.DH[j] = pair();
+  A.L.st = dalloc<LoopState>(1);
+  A.stage_start = dupload(stage_start_);
+  A.D = D_;
+  A.d1 = d1_;
+  A.d2 = d2_;
+  small_cap_ = 0;
 }
 
 bool Engine::solve_small(const double* x_init, const double* wz, const double* we, double* oz, double* ozs,
@@ -2237,21 +2386,7 @@ bool Engine::solve_small(const double* x_init, const double* wz, const double* w
   const int64_t nz = lay_.nz, ne = lay_.neta, nv = nz + ne;
   set_xinit(x_init ? x_init : raw_xinit_.data());
   SmallArgs& A = small_;
-  if (!A.L.V) {  // buffers, built once per engine
-    auto pair = [&]() { return dalloc<double>(size_t(nv)); };
-    A.L.V = pair(), A.L.TV = pair(), A.L.R = pair(), A.L.C = pair(), A.L.CR = pair(), A.L.PSI = pair();
-    A.TC = pair(), A.PV = pair();
-    A.Lrz = dalloc<double>(size_t(ne));
-    A.cLrz = dalloc<double>(size_t(ne));
-    A.Lsre = dalloc<double>(size_t(nz));
-    A.tmpz = dalloc<double>(size_t(nz));
-    A.tmpe = dalloc<double>(size_t(ne));
-    for (int j = 0; j < kLoopMaxMem + 1; ++j) A.L.RH[j] = pair();
-    for (int j = 0; j < kLoopMaxMem; ++j) A.L.DH[j] = pair();
-    A.L.st = dalloc<LoopState>(1);
-    A.stage_start = dupload(stage_start_);
-    small_cap_ = 0;
-  }
+  small_alloc();
   const int cap = prm_.max_iters + 2;
   if (small_cap_ < cap) {
     A.L.rnorm = dalloc<double>(size_t(cap));
@@ -2284,7 +2419,18 @@ bool Engine::solve_small(const double* x_init, const double* wz, const double* w
   if (pe && pe[0] == '1' && !A.prof) {
     A.prof = dalloc<unsigned long long>(8);
   }
-  launch_small_solve(A, st_);
+  if (cluster_ok_) {
+    if (!cluster_plan(m)) return false;  // (cannot happen after a successful plan at construction)
+    ClusterArgs CA{};
+    CA.S = A;
+    CA.place = cplace_d_;
+    CA.nplace = cplace_n_;
+    CA.field = cfield_d_;
+    CA.nfield = cfield_n_;
+    CK(launch_cluster_solve(CA, cluster_ctas_, cluster_arena_, st_));
+  } else {
+    launch_small_solve(A, st_);
+  }
   CK(cudaGetLastError());
   if (A.prof) {
     unsigned long long h[8];

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <functional>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -94,6 +95,15 @@ class Engine {
   SmallArgs small_{};
   bool small_ok_ = false;  // decided at construction (SPOCK_SMALL=0/1 overrides)
   int small_cap_ = 0;
+  // cluster-resident loop (cluster.cuh): the small loop's allocations packed
+  // into the shared memory of a thread-block cluster (SPOCK_CLUSTER=0/1)
+  bool cluster_ok_ = false;
+  bool cluster_plan(int m);
+  void small_alloc();
+  ClusterPlace* cplace_d_ = nullptr;
+  ClusterField* cfield_d_ = nullptr;
+  int cplace_n_ = 0, cfield_n_ = 0, cluster_ctas_ = 0, cluster_arena_ = 0, cplan_m_ = -1;
+  std::map<uintptr_t, size_t> alloc_bytes_;  // every dalloc allocation: base -> bytes
   void build_loop_graph(GraphLoop& G, bool supermann);
   double bench_T(int k, bool graph, bool flush);
   void bench_kernels(int k, bool flush, double* ms);

@@ -1040,6 +1040,7 @@ __global__ void k_alg1_child_abar(Alg1Args P) {
 }
 
 #include "small.cuh"
+#include "cluster.cuh"
 
 }  // namespace
 
@@ -1081,6 +1082,35 @@ void launch_s2(const Dev& D, double* z, cudaStream_t st) {
 
 void launch_s3(const Dev& D, double* eta, cudaStream_t st) {
   k_s3<<<blocks_for(D.nn, kWarps), 32 * kWarps, 0, st>>>(D, eta);
+}
+
+int cluster_static_smem() {
+  cudaFuncAttributes fa{};
+  if (cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(&k_cluster_solve)) != cudaSuccess) return 48 * 1024;
+  return int(fa.sharedSizeBytes);
+}
+
+cudaError_t launch_cluster_solve(const ClusterArgs& A, int ctas, int arena_bytes, cudaStream_t st) {
+  const void* fn = reinterpret_cast<const void*>(&k_cluster_solve);
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, arena_bytes);
+  if (e != cudaSuccess) return e;
+  if (ctas > 8) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(ctas);
+  cfg.blockDim = dim3(kSmallThreads);
+  cfg.dynamicSmemBytes = size_t(arena_bytes);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = unsigned(ctas);
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_cluster_solve, A);
 }
 
 void launch_small_solve(const SmallArgs& A, cudaStream_t st) {

@@ -84,6 +84,33 @@ struct SmallArgs {
 void launch_small_solve(const SmallArgs& A, cudaStream_t st);
 constexpr int kSmallThreadsHost = 256;
 
+// Cluster-resident solve (cluster.cuh): the device allocations the small loop
+// touches, packed whole into the shared memory of a thread-block cluster.
+constexpr int kClusterMax = 16;
+struct ClusterPlace {  // one device allocation staged into CTA `cta`'s arena
+  const char* src;
+  int64_t bytes;  // multiple of 8
+  int32_t cta, off;  // arena offset (16-byte aligned)
+  int32_t writable;  // copied back to HBM at the end of the solve
+  int32_t pad_;
+};
+struct ClusterField {  // a pointer field of SmallArgs, relocated into a placement
+  int32_t field;  // byte offset of the pointer inside SmallArgs
+  int32_t place;
+  int64_t delta;  // byte offset inside the allocation
+};
+struct ClusterArgs {
+  SmallArgs S;  // global pointers (the staging sources); relocated per CTA in the kernel
+  const ClusterPlace* place;
+  int nplace;
+  const ClusterField* field;
+  int nfield;
+};
+int cluster_static_smem();
+// arena bytes per CTA and cluster size; returns the launch error (cluster
+// launches fail, e.g., when the arena does not fit)
+cudaError_t launch_cluster_solve(const ClusterArgs& A, int ctas, int arena_bytes, cudaStream_t st);
+
 void launch_Lt(const Dev& D, const double* eta, const double* zin, double* zout, double a, double b, double c0,
                cudaStream_t st);
 void launch_L(const Dev& D, const double* z1, double a1, const double* z2, double a2, const double* eta_in,

@@ -153,20 +153,26 @@ SMALL_CASES = [
 ]
 
 
+LOOP_ENV = {"small": {"SPOCK_SMALL": "1"}, "cluster": {"SPOCK_SMALL": "0", "SPOCK_CLUSTER": "1"}}
+
+
 @pytest.mark.parametrize("name,mk", SMALL_CASES, ids=[c[0] for c in SMALL_CASES])
 @pytest.mark.parametrize("method", ["solve", "solve_cp"])
-def test_small_loop_matches_graph_loop(name, mk, method):
-    """The CTA-resident loop (small.cuh: the whole solve in one CTA) runs the
-    graph loop's algorithm on the per-stage operator kernels' arithmetic: over
-    a few dozen iterations the branch strings and counters agree and the traces
-    and iterates agree to rounding."""
+@pytest.mark.parametrize("loop", ["small", "cluster"])
+def test_small_loop_matches_graph_loop(name, mk, method, loop):
+    """The CTA-resident loop (small.cuh: the whole solve in one CTA) and the
+    cluster-resident loop (cluster.cuh: the whole solve in one thread-block
+    cluster, every operand in distributed shared memory) run the graph loop's
+    algorithm on the per-stage operator kernels' arithmetic: over a few dozen
+    iterations the branch strings and counters agree and the traces and
+    iterates agree to rounding (only the reduction partitions differ)."""
     from paper_2505_12078_b200.generators import make_config
     from paper_2505_12078_b200.solver import SpockSolver
     p = make_config("c1", seed=1) if mk is None else mk()
-    s = _with_env({"SPOCK_SMALL": "1"}, lambda: SpockSolver(p, max_iters=40, eps_abs=1e-14, eps_rel=1e-14))
-    assert s.loop_path == "small"
-    g = _with_env({"SPOCK_SMALL": "0"}, lambda: SpockSolver(p, max_iters=40, eps_abs=1e-14, eps_rel=1e-14,
-                                                              alpha=s.alpha))
+    s = _with_env(LOOP_ENV[loop], lambda: SpockSolver(p, max_iters=40, eps_abs=1e-14, eps_rel=1e-14))
+    assert s.loop_path == loop
+    g = _with_env({"SPOCK_SMALL": "0", "SPOCK_CLUSTER": "0"},
+                  lambda: SpockSolver(p, max_iters=40, eps_abs=1e-14, eps_rel=1e-14, alpha=s.alpha))
     assert g.loop_path == "graph"
     a = getattr(s, method)(p.x_init)
     b = getattr(g, method)(p.x_init)
@@ -178,15 +184,16 @@ def test_small_loop_matches_graph_loop(name, mk, method):
         assert float(np.abs(x - y).max()) <= 1e-8 * max(1.0, float(np.abs(y).max()))
 
 
-def test_small_loop_bitwise_deterministic_and_warm_start():
+@pytest.mark.parametrize("loop", ["small", "cluster"])
+def test_small_loop_bitwise_deterministic_and_warm_start(loop):
     from paper_2505_12078_b200.generators import make_config
     from paper_2505_12078_b200.solver import SpockSolver
     p = make_config("c1", seed=1)
-    s = _with_env({"SPOCK_SMALL": "1"}, lambda: SpockSolver(p, max_iters=300))
-    assert s.loop_path == "small"
+    s = _with_env(LOOP_ENV[loop], lambda: SpockSolver(p, max_iters=300))
+    assert s.loop_path == loop
     a, b = s.solve(), s.solve()
     assert np.array_equal(a.z, b.z) and np.array_equal(a.status["rnorm_history"], b.status["rnorm_history"])
-    w = _with_env({"SPOCK_SMALL": "1"}, lambda: SpockSolver(p, max_iters=50000, eps_abs=1e-6, eps_rel=1e-6))
+    w = _with_env(LOOP_ENV[loop], lambda: SpockSolver(p, max_iters=50000, eps_abs=1e-6, eps_rel=1e-6))
     cold = w.solve_cp()
     warm = w.solve_cp(p.x_init, warm=(cold.z_scaled, cold.eta))
     assert cold.status["reason"] == warm.status["reason"] == "converged"

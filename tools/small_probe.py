@@ -1,5 +1,6 @@
-"""c1 solve to tolerance on the CTA-resident loop (small.cuh) against the
-device graph loop and the CPU oracle: time, iterations, per-iteration cost.
+"""c1 solve to tolerance on the cluster-resident loop (cluster.cuh), the
+CTA-resident loop (small.cuh) and the device graph loop, beside the CPU
+oracle: time, iterations, per-iteration cost.
 Usage (GPU box): python tools/small_probe.py [config]"""
 import json
 import os
@@ -19,10 +20,13 @@ def main():
     for method in ("solve_cp", "solve"):
         for tol in tols:
             row = {"config": cfg, "method": method, "tol": tol}
-            for path in ("small", "graph"):
+            paths = os.environ.get("PROBE_PATHS", "cluster,small,graph").split(",")
+            for path in paths:
                 os.environ["SPOCK_SMALL"] = "1" if path == "small" else "0"
+                os.environ["SPOCK_CLUSTER"] = "1" if path == "cluster" else "0"
                 s = SpockSolver(p, max_iters=50000, eps_abs=tol, eps_rel=tol)
                 os.environ.pop("SPOCK_SMALL", None)
+                os.environ.pop("SPOCK_CLUSTER", None)
                 getattr(s, method)(p.x_init)
                 t = time.perf_counter()
                 r = getattr(s, method)(p.x_init)
