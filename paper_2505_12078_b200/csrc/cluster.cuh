@@ -52,6 +52,7 @@ __device__ __forceinline__ void csync() {
 
 struct CDist {  // this thread's share of the cluster's work
   int rank, C, gw, GW, gt, GT;
+  int w, n0, n1;  // warp in the CTA; the CTA's node range (operator phases)
   int nred;  // reductions so far: partial tables alternate between two halves, so a
              // CTA writing the next reduction's partials never overwrites the ones CTA 0
              // is still summing (the two uses of a half are a cluster barrier apart)
@@ -60,14 +61,16 @@ __device__ __forceinline__ double* part_half(CDist& c, double* part0) {
   return part0 + (c.nred++ & 1) * (kClusterMax * 64);
 }
 
+// operator phases: CTA c runs the nodes it owns ([n0, n1): their blocks sit in
+// its shared memory), one warp per node
 __device__ void cl_Lt(const CDist& c, const Dev& D, const double* eta, const double* zin, double* zout, double a,
                       double b, double c0, double* xs) {
-  for (int k = c.gw; k < D.nr; k += c.GW) {
+  for (int k = max(c.n0 - 1, 0) + c.w; k < min(c.n1 - 1, D.nr); k += kSW) {  // child node k + 1
     lt_child_body(D, k, eta, zin, zout, a, b, xs);
     __syncwarp();
   }
   csync();
-  for (int i = c.gw; i < D.nn; i += c.GW) {
+  for (int i = c.n0 + c.w; i < c.n1; i += kSW) {
     lt_node_body(D, i, eta, zin, zout, a, b, c0, xs);
     __syncwarp();
   }
@@ -75,7 +78,7 @@ __device__ void cl_Lt(const CDist& c, const Dev& D, const double* eta, const dou
 }
 
 __device__ void cl_L(const CDist& c, const Dev& D, const double* z, double* eta, double* xs) {
-  for (int i = c.gw; i < D.nn; i += c.GW) {
+  for (int i = c.n0 + c.w; i < c.n1; i += kSW) {
     L_node_body<false>(D, i, z, 1.0, nullptr, 0.0, nullptr, eta, 0.0, xs);
     __syncwarp();
   }
@@ -86,25 +89,25 @@ __device__ void cl_T(const CDist& c, const Dev& D, const int* ss, const double* 
                      double* eo, double alpha, double* xs) {
   cl_Lt(c, D, eta, z, zo, 1.0, -alpha, -alpha, xs);
   for (int t = D.N; t >= 0; --t) {
-    for (int i = ss[t] + c.gw; i < ss[t + 1]; i += c.GW) {
+    for (int i = max(ss[t], c.n0) + c.w; i < min(ss[t + 1], c.n1); i += kSW) {
       s1_back_body(D, i, zo, xs);
       __syncwarp();
     }
     csync();
   }
   for (int t = 0; t <= D.N; ++t) {
-    for (int i = ss[t] + c.gw; i < ss[t + 1]; i += c.GW) {
+    for (int i = max(ss[t], c.n0) + c.w; i < min(ss[t + 1], c.n1); i += kSW) {
       s1_fwd_body(D, i, zo, xs);
       __syncwarp();
     }
     csync();
   }
-  for (int i = c.gw; i < D.nnl; i += c.GW) {
+  for (int i = c.n0 + c.w; i < min(c.n1, D.nnl); i += kSW) {
     s2_node_body(D, i, zo, xs);
     __syncwarp();
   }
   csync();
-  for (int i = c.gw; i < D.nn; i += c.GW) {
+  for (int i = c.n0 + c.w; i < c.n1; i += kSW) {
     L_node_body<true>(D, i, zo, 2.0, z, -1.0, eta, eo, alpha, xs);
     __syncwarp();
   }
@@ -216,6 +219,9 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_cluster_solve(const __grid
   c.gt = c.rank * kSmallThreads + t;
   c.GT = c.C * kSmallThreads;
   c.nred = 0;
+  c.w = w;
+  c.n0 = CA.own[c.rank];
+  c.n1 = CA.own[c.rank + 1];
   double* xs = xs_all[w];
   // stage this CTA's allocations (8-byte granules; every allocation is 16-byte aligned)
   for (int p = 0; p < CA.nplace; ++p) {
@@ -229,6 +235,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_cluster_solve(const __grid
     A = CA.S;
     for (int f = 0; f < CA.nfield; ++f) {
       const ClusterField F = CA.field[f];
+      if (F.cta >= 0 && F.cta != c.rank) continue;
       const ClusterPlace P = CA.place[F.place];
       char* base = reinterpret_cast<char*>(cl_map(arena + P.off, P.cta));
       *reinterpret_cast<char**>(reinterpret_cast<char*>(&A) + F.field) = base + F.delta;

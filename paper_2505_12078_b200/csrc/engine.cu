@@ -1413,6 +1413,7 @@ void Engine::upload() {
     D.hx_off = dupload(hxo);
     D.hu_off = dupload(huo);
     D.a_off = dupload(ao);
+    hxo_ = hxo, huo_ = huo, ao_ = ao;
     if (soc_dev_) {
       D.Hx = dalloc<double>(sx);
       D.HxT = dalloc<double>(sx);
@@ -1458,6 +1459,7 @@ void Engine::upload() {
     D.pN = dupload(pN);
     D.hn_off = dupload(ho);
     D.aN_off = dupload(ao);
+    hno_ = ho, aNo_ = ao;
     if (soc_dev_) {
       D.HN = dalloc<double>(sh);
       D.HNT = dalloc<double>(sh);
@@ -2259,9 +2261,15 @@ static void for_each_small_ptr(SmallArgs& A, int m, F&& f) {
   for (int j = 0; j < m; ++j) w(L.DH[j]);
 }
 
-// Pack the allocations the small loop touches into the shared memory of a
-// cluster of CTAs (first fit, largest first; whole allocations per CTA) and
-// upload the placement and relocation tables.  False: does not fit.
+// Pack the small loop's device image into the shared memory of a cluster of C
+// CTAs.  CTA c owns the contiguous node range [own[c], own[c+1]) and runs every
+// operator phase for those nodes, so each node-indexed block array (H, M1, K,
+// R~^-1, translations, boxes, ...) is split: CTA c holds the slice of its nodes
+// in its own shared memory and its pointer is rebased onto that slice (local
+// latency).  Small read-only tables (tree, layouts, offsets) are replicated in
+// every CTA; everything else -- iterates, history rings, the child-to-parent
+// scratch -- is placed whole (largest first, least-filled CTA) and reached
+// through DSMEM by the other CTAs.  False: does not fit.
 bool Engine::cluster_plan(int m) {
   if (cplace_d_ && cplan_m_ == m) return true;
   SmallArgs A = small_;
@@ -2270,83 +2278,163 @@ bool Engine::cluster_plan(int m) {
   CK(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   const int cap = ((smem_optin - cluster_static_smem() - 1024) / 16) * 16;
   if (cap <= 0) return false;
-  struct Al {
-    uintptr_t base;
-    size_t bytes;
-    bool wr;
-    int cta, off;
+  const Tree& tr = p_.tree;
+  const int nn = tr.nn(), nnl = tr.nnl(), nx = p_.nx, nu = p_.nu;
+  const int64_t mm = nx + nu;
+  using Span = std::pair<int64_t, int64_t>;  // (first element, count) of node i's block; count 0: none
+  std::map<uintptr_t, std::function<Span(int)>> split;
+  auto sp = [&](const double* base, std::function<Span(int)> f) {
+    if (base) split[reinterpret_cast<uintptr_t>(base)] = std::move(f);
   };
-  std::vector<Al> al;
-  std::vector<std::pair<int, std::pair<int, int64_t>>> fld;  // field offset -> (alloc index, delta)
+  auto nr_ = [&](int i, auto f) -> Span { return i > 0 ? f(i - 1) : Span{0, 0}; };
+  auto nl_ = [&](int i, auto f) -> Span { return i < nnl ? f(i) : Span{0, 0}; };
+  auto lf_ = [&](int i, auto f) -> Span { return i >= nnl ? f(i - nnl) : Span{0, 0}; };
+  const Dev& D = D_;
+  const auto& px = soc_.stage;
+  sp(D.Hx, [&](int i) { return nr_(i, [&](int k) { return Span{hxo_[k], pad2(int64_t(px[k].px) * nx)}; }); });
+  sp(D.HxT, [&](int i) { return nr_(i, [&](int k) { return Span{hxo_[k], pad2(int64_t(px[k].px) * nx)}; }); });
+  sp(D.Hu, [&](int i) { return nr_(i, [&](int k) { return Span{huo_[k], pad2(int64_t(px[k].pu) * nu)}; }); });
+  sp(D.HuT, [&](int i) { return nr_(i, [&](int k) { return Span{huo_[k], pad2(int64_t(px[k].pu) * nu)}; }); });
+  sp(D.qk, [&](int i) { return nr_(i, [&](int k) { return Span{k * mm, mm}; }); });
+  sp(D.a, [&](int i) { return nr_(i, [&](int k) { return Span{ao_[k], px[k].px + px[k].pu + 2}; }); });
+  sp(D.M1, [&](int i) { return nr_(i, [&](int k) { return Span{k * D.m1_stride, D.m1_stride}; }); });
+  sp(D.M1T, [&](int i) { return nr_(i, [&](int k) { return Span{k * D.m1_stride, D.m1_stride}; }); });
+  sp(D.cvec, [&](int i) { return nr_(i, [&](int k) { return Span{int64_t(k) * nx, nx}; }); });
+  sp(D.HN, [&](int i) { return lf_(i, [&](int j) { return Span{hno_[j], pad2(int64_t(soc_.leaf[j].px) * nx)}; }); });
+  sp(D.HNT, [&](int i) { return lf_(i, [&](int j) { return Span{hno_[j], pad2(int64_t(soc_.leaf[j].px) * nx)}; }); });
+  sp(D.qkN, [&](int i) { return lf_(i, [&](int j) { return Span{int64_t(j) * nx, nx}; }); });
+  sp(D.aN, [&](int i) { return lf_(i, [&](int j) { return Span{aNo_[j], soc_.leaf[j].px + 2}; }); });
+  sp(D.gNd, [&](int i) { return lf_(i, [&](int j) { return Span{int64_t(j) * nx, nx}; }); });
+  sp(D.GN, [&](int i) { return lf_(i, [&](int j) { return Span{p_.gN_off[j] * nx, int64_t(p_.ncN[j]) * nx}; }); });
+  sp(D.GNT, [&](int i) { return lf_(i, [&](int j) { return Span{p_.gN_off[j] * nx, int64_t(p_.ncN[j]) * nx}; }); });
+  sp(D.loN, [&](int i) { return lf_(i, [&](int j) { return Span{p_.gN_off[j], p_.ncN[j]}; }); });
+  sp(D.hiN, [&](int i) { return lf_(i, [&](int j) { return Span{p_.gN_off[j], p_.ncN[j]}; }); });
+  sp(D.gd, [&](int i) { return nl_(i, [&](int q) { return Span{q * mm, mm}; }); });
+  sp(D.Gx, [&](int i) { return nl_(i, [&](int q) { return Span{p_.g_off[q] * nx, int64_t(p_.nc[q]) * nx}; }); });
+  sp(D.GxT, [&](int i) { return nl_(i, [&](int q) { return Span{p_.g_off[q] * nx, int64_t(p_.nc[q]) * nx}; }); });
+  sp(D.Gu, [&](int i) { return nl_(i, [&](int q) { return Span{p_.g_off[q] * nu, int64_t(p_.nc[q]) * nu}; }); });
+  sp(D.GuT, [&](int i) { return nl_(i, [&](int q) { return Span{p_.g_off[q] * nu, int64_t(p_.nc[q]) * nu}; }); });
+  sp(D.lo, [&](int i) { return nl_(i, [&](int q) { return Span{p_.g_off[q], p_.nc[q]}; }); });
+  sp(D.hi, [&](int i) { return nl_(i, [&](int q) { return Span{p_.g_off[q], p_.nc[q]}; }); });
+  sp(D.K, [&](int i) { return nl_(i, [&](int q) { return Span{q * D.k_stride, D.k_stride}; }); });
+  sp(D.KT, [&](int i) { return nl_(i, [&](int q) { return Span{q * D.k_stride, D.k_stride}; }); });
+  sp(D.Rinv, [&](int i) { return nl_(i, [&](int q) { return Span{q * D.r_stride, D.r_stride}; }); });
+  sp(D.g, [&](int i) { return nl_(i, [&](int q) { return Span{int64_t(q) * nu, nu}; }); });
+  sp(D.h, [&](int i) { return nl_(i, [&](int q) { return Span{int64_t(q) * nx, nx}; }); });
+  sp(D.rb, [&](int i) {
+    return nl_(i, [&](int q) { return Span{int64_t(lay_.y_off[q]) - D.y_base, lay_.y_dim[q]}; });
+  });
+  // every pointer field: allocation, delta, writable
+  struct Fld {
+    int field;
+    uintptr_t ptr, base;
+    size_t abytes;
+    bool wr;
+  };
+  std::vector<Fld> flds;
   bool ok = true;
   for_each_small_ptr(A, m, [&](const void** f, bool wr) {
     const uintptr_t p = reinterpret_cast<uintptr_t>(*f);
     if (!p || !ok) return;
     auto it = alloc_bytes_.upper_bound(p);
-    if (it == alloc_bytes_.begin()) {
+    if (it == alloc_bytes_.begin() || p >= std::prev(it)->first + std::prev(it)->second) {
       ok = false;
       return;
     }
     --it;
-    if (p >= it->first + it->second) {
-      ok = false;
-      return;
-    }
-    int idx = -1;
-    for (size_t k = 0; k < al.size(); ++k)
-      if (al[k].base == it->first) idx = int(k);
-    if (idx < 0) {
-      al.push_back(Al{it->first, (it->second + 15) & ~size_t(15), wr, -1, 0});
-      idx = int(al.size()) - 1;
-    }
-    al[idx].wr = al[idx].wr || wr;
-    fld.push_back({int(reinterpret_cast<const char*>(f) - reinterpret_cast<const char*>(&A)),
-                   {idx, int64_t(p - it->first)}});
+    flds.push_back(Fld{int(reinterpret_cast<const char*>(f) - reinterpret_cast<const char*>(&A)), p, it->first,
+                       it->second, wr});
   });
   if (!ok) return false;
-  std::vector<int> order(al.size());
-  for (size_t k = 0; k < al.size(); ++k) order[k] = int(k);
-  std::sort(order.begin(), order.end(), [&](int x, int y) { return al[x].bytes > al[y].bytes; });
-  auto pack = [&](int C) {
-    std::vector<size_t> used(size_t(C), 0);
-    for (int k : order) {
-      int best = -1;
-      for (int c = 0; c < C; ++c)  // least-filled CTA that fits: spreads the DSMEM traffic
-        if (used[c] + al[k].bytes <= size_t(cap) && (best < 0 || used[c] < used[best])) best = c;
-      if (best < 0) return size_t(0);
-      al[k].cta = best;
-      al[k].off = int(used[best]);
-      used[best] += al[k].bytes;
-    }
-    size_t mx = 0;
-    for (size_t u : used) mx = std::max(mx, u);
-    return std::max<size_t>(mx, 16);
-  };
-  int C = 0;
-  size_t arena = 0;
   const char* ce = std::getenv("SPOCK_CLUSTER_CTAS");
   int want = ce && ce[0] ? std::atoi(ce) : 4;
   want = std::max(1, std::min(kClusterMax, want));
-  for (int c = want; c <= kClusterMax && !arena; ++c) {
-    arena = pack(c);
-    if (arena) C = c;
+  for (int C = want; C <= kClusterMax; ++C) {
+    std::vector<int> own(size_t(C) + 1);
+    for (int c = 0; c <= C; ++c) own[c] = int(int64_t(nn) * c / C);
+    std::vector<size_t> used(size_t(C), 0);
+    std::vector<ClusterPlace> pl;
+    std::vector<ClusterField> fl;
+    bool fits = true;
+    auto put = [&](int c, uintptr_t src, size_t bytes, bool wr) -> int {  // -> placement index (16-aligned)
+      size_t off = (used[c] + 15) & ~size_t(15);
+      off += src & 15;  // keep the 16-byte phase of the source (8-byte granules)
+      if (off + bytes > size_t(cap)) {
+        fits = false;
+        return -1;
+      }
+      used[c] = off + bytes;
+      pl.push_back(ClusterPlace{reinterpret_cast<const char*>(src), int64_t((bytes + 7) & ~size_t(7)), c, int(off),
+                                wr ? 1 : 0, 0});
+      return int(pl.size()) - 1;
+    };
+    // 1. split block arrays: each CTA's node slice
+    std::map<uintptr_t, bool> done;
+    for (const Fld& F : flds) {
+      auto sit = split.find(F.ptr);
+      if (sit == split.end() || F.wr) continue;
+      for (int c = 0; c < C && fits; ++c) {
+        int64_t lo = INT64_MAX, hi = -1;
+        for (int i = own[c]; i < own[c + 1]; ++i) {
+          const Span s2 = sit->second(i);
+          if (s2.second <= 0) continue;
+          lo = std::min(lo, s2.first);
+          hi = std::max(hi, s2.first + s2.second);
+        }
+        if (hi < 0) continue;  // no node of this CTA has a block here: never dereferenced by it
+        const int pi = put(c, F.ptr + uintptr_t(lo) * 8, size_t(hi - lo) * 8, false);
+        if (pi >= 0) fl.push_back(ClusterField{F.field, pi, -lo * 8, c});
+      }
+      done[F.ptr] = true;
+    }
+    // 2. small read-only tables: replicated
+    for (const Fld& F : flds) {
+      if (done.count(F.ptr) || F.wr || F.abytes > 16384) continue;
+      for (int c = 0; c < C && fits; ++c) {
+        const int pi = put(c, F.base, F.abytes, false);
+        if (pi >= 0) fl.push_back(ClusterField{F.field, pi, int64_t(F.ptr - F.base), c});
+      }
+    }
+    // 3. the rest: whole allocations, largest first, least-filled CTA
+    std::map<uintptr_t, int> whole;  // allocation base -> placement
+    std::vector<const Fld*> rest;
+    for (const Fld& F : flds)
+      if (!(done.count(F.ptr) && !F.wr) && (F.wr || F.abytes > 16384)) rest.push_back(&F);
+    std::vector<uintptr_t> bases;
+    std::map<uintptr_t, std::pair<size_t, bool>> abyte;
+    for (const Fld* F : rest) {
+      auto& e = abyte[F->base];
+      e.first = F->abytes;
+      e.second = e.second || F->wr;
+    }
+    for (auto& kv : abyte) bases.push_back(kv.first);
+    std::sort(bases.begin(), bases.end(), [&](uintptr_t x, uintptr_t y) { return abyte[x].first > abyte[y].first; });
+    for (uintptr_t b : bases) {
+      if (!fits) break;
+      int best = 0;
+      for (int c = 1; c < C; ++c)
+        if (used[c] < used[best]) best = c;
+      whole[b] = put(best, b, abyte[b].first, abyte[b].second);
+    }
+    for (const Fld* F : rest)
+      if (fits && whole.count(F->base)) fl.push_back(ClusterField{F->field, whole[F->base], int64_t(F->ptr - F->base), -1});
+    if (!fits) continue;
+    size_t arena = 16;
+    for (size_t u : used) arena = std::max(arena, (u + 15) & ~size_t(15));
+    cplace_d_ = dupload(pl);
+    cfield_d_ = dupload(fl);
+    cplace_n_ = int(pl.size());
+    cfield_n_ = int(fl.size());
+    cluster_ctas_ = C;
+    cluster_arena_ = int(arena);
+    cown_.assign(own.begin(), own.end());
+    cplan_m_ = m;
+    CK(cudaStreamSynchronize(st_));
+    if (std::getenv("SPOCK_DEBUG_SETUP"))
+      std::fprintf(stderr, "[cluster] ctas %d arena %zu B placements %d fields %d\n", C, arena, cplace_n_, cfield_n_);
+    return true;
   }
-  if (!arena) return false;
-  std::vector<ClusterPlace> pl(al.size());
-  for (size_t k = 0; k < al.size(); ++k)
-    pl[k] = ClusterPlace{reinterpret_cast<const char*>(al[k].base), int64_t(al[k].bytes), al[k].cta, al[k].off,
-                         al[k].wr ? 1 : 0, 0};
-  std::vector<ClusterField> fl(fld.size());
-  for (size_t k = 0; k < fld.size(); ++k) fl[k] = ClusterField{fld[k].first, fld[k].second.first, fld[k].second.second};
-  cplace_d_ = dupload(pl);
-  cfield_d_ = dupload(fl);
-  cplace_n_ = int(pl.size());
-  cfield_n_ = int(fl.size());
-  cluster_ctas_ = C;
-  cluster_arena_ = int(arena);
-  cplan_m_ = m;
-  CK(cudaStreamSynchronize(st_));
-  return true;
+  return false;
 }
 
 const char* Engine::loop_path() const {
@@ -2427,6 +2515,7 @@ bool Engine::solve_small(const double* x_init, const double* wz, const double* w
     CA.nplace = cplace_n_;
     CA.field = cfield_d_;
     CA.nfield = cfield_n_;
+    for (int c = 0; c <= cluster_ctas_; ++c) CA.own[c] = cown_[c];
     CK(launch_cluster_solve(CA, cluster_ctas_, cluster_arena_, st_));
   } else {
     launch_small_solve(A, st_);

@@ -103,7 +103,9 @@ class Engine {
   ClusterPlace* cplace_d_ = nullptr;
   ClusterField* cfield_d_ = nullptr;
   int cplace_n_ = 0, cfield_n_ = 0, cluster_ctas_ = 0, cluster_arena_ = 0, cplan_m_ = -1;
+  std::vector<int> cown_;  // node range of each CTA
   std::map<uintptr_t, size_t> alloc_bytes_;  // every dalloc allocation: base -> bytes
+  std::vector<int64_t> hxo_, huo_, ao_, hno_, aNo_;  // host copies of the SOC block offsets
   void build_loop_graph(GraphLoop& G, bool supermann);
   double bench_T(int k, bool graph, bool flush);
   void bench_kernels(int k, bool flush, double* ms);

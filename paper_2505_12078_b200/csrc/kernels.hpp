@@ -97,7 +97,9 @@ struct ClusterPlace {  // one device allocation staged into CTA `cta`'s arena
 struct ClusterField {  // a pointer field of SmallArgs, relocated into a placement
   int32_t field;  // byte offset of the pointer inside SmallArgs
   int32_t place;
-  int64_t delta;  // byte offset inside the allocation
+  int64_t delta;  // byte offset from the placement's start (negative: a rebased node slice)
+  int32_t cta;    // -1: every CTA applies it; else only that CTA
+  int32_t pad_;
 };
 struct ClusterArgs {
   SmallArgs S;  // global pointers (the staging sources); relocated per CTA in the kernel
@@ -105,6 +107,7 @@ struct ClusterArgs {
   int nplace;
   const ClusterField* field;
   int nfield;
+  int own[kClusterMax + 1];  // CTA c runs the operator phases of nodes [own[c], own[c+1])
 };
 int cluster_static_smem();
 // arena bytes per CTA and cluster size; returns the launch error (cluster
