@@ -1130,7 +1130,7 @@ void Engine::wide_profile(unsigned long long* out) {
 
 void Engine::set_grid_cap(int ctas) {
   if (ctas < 0) throw std::invalid_argument("set_grid_cap: negative CTA count");
-  if (gloop_[0].exec || gloop_[1].exec || bench_graph_)
+  if (gloop_[0].exec || gloop_[1].exec || bench_graph_ || small_solved_)
     throw std::invalid_argument("set_grid_cap: must be called before the first solve or bench");
   if (!fused_ok_) return;  // the streaming schedules are HBM-bound: nothing to share
   fused_grid_ = ctas > 0 ? std::min(fused_grid_full_, ctas) : fused_grid_full_;
@@ -2507,6 +2507,7 @@ bool Engine::solve_small(const double* x_init, const double* wz, const double* w
   if (pe && pe[0] == '1' && !A.prof) {
     A.prof = dalloc<unsigned long long>(8);
   }
+  small_solved_ = true;
   if (cluster_ok_) {
     if (!cluster_plan(m)) return false;  // (cannot happen after a successful plan at construction)
     ClusterArgs CA{};

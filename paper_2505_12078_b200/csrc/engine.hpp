@@ -98,6 +98,7 @@ class Engine {
   // cluster-resident loop (cluster.cuh): the small loop's allocations packed
   // into the shared memory of a thread-block cluster (SPOCK_CLUSTER=0/1)
   bool cluster_ok_ = false;
+  bool small_solved_ = false;  // a small / cluster solve ran (set_grid_cap is then rejected, as after a graph solve)
   bool cluster_plan(int m);
   void small_alloc();
   ClusterPlace* cplace_d_ = nullptr;
