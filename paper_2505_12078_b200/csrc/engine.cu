@@ -462,11 +462,20 @@ void Engine::setup_wide(bool force) {
   A = WideArgs{};
   A.warps = std::max(1, std::min(8, knob("SPOCK_WIDE_WARPS", 8)));
   {
-    const int sl = std::max(1, std::min(16, knob("SPOCK_WIDE_SLOTS", 2)));
+    // Deep, narrow trees (a 100-stage horizon: ~1 000 items per level for ~1 800
+    // resident warps) are bound by the latency of one item per level, not by
+    // bandwidth: a 4-slot ring per warp (fewer warps) shortens each item
+    // (measured (100, 10, 3): 6.14 -> 5.31 ms per T; wide levels prefer 2 slots)
+    const double width = double(nn) / double(tr.horizon + 1);
+    const int lat_slots = width < 148.0 * 2 * 6 ? 4 : 2;
+    const int sl = std::max(1, std::min(16, knob("SPOCK_WIDE_SLOTS", lat_slots)));
     A.slots = sl >= 16 ? 16 : (sl >= 8 ? 8 : (sl >= 4 ? 4 : (sl >= 2 ? 2 : 1)));  // power of two
   }
   A.chunk = std::max(512, knob("SPOCK_WIDE_CHUNK", 512)) & ~1;
-  A.ycap = std::min(max_ny, 256);
+  // staging capacities sized for the common items: rare wide parents (a 100-way
+  // fan-out has 201-row risk blocks) read their large spans in place, so they
+  // do not inflate every warp's shared memory (fewer resident warps)
+  A.ycap = std::min(max_ny, 64);
   A.l2_prefetch = knob("SPOCK_WIDE_L2PF", 0);  // measured slower (c3 1.80 vs 1.40 ms)
   A.vecd = int((std::max({m, max_nc, max_dense_s2_, 2 * nu + 2 + A.ycap}) + 2 + 7) & ~7);
   wide_ctas_ = knob("SPOCK_WIDE_CTAS", 2) >= 2 ? 2 : 1;
@@ -519,7 +528,7 @@ void Engine::setup_wide(bool force) {
   auto span = [&](WRec& R, int id, int base, int64_t off, int64_t cnt) {
     R.vbase[id] = uint8_t(base);
     R.voff[id] = int32_t(off);
-    if (cnt > 1024 || off > INT32_MAX) {  // read in place (huge fan-out y blocks)
+    if (cnt > 160 || off > INT32_MAX) {  // read in place (wide fan-out risk blocks)
       R.unstaged |= 1 << id;
       R.vcnt[id] = 0;
     } else {
