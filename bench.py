@@ -410,6 +410,8 @@ def main():
     ap.add_argument("--sweep", default="c3,c2p,c2", help="extra single-GPU configs (N=1 only); '' disables")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--side-by-side", default="quick", choices=["quick", "full", "none"])
+    ap.add_argument("--sharded", action="store_true", help="run the subtree-sharded path even on one rank "
+                    "(exercises the N > 1 code path, NCCL included, on a single GPU)")
     ap.add_argument("--backend", default="nccl", help="process group backend for N>1 (gloo: code-path smoke test "
                                                           "with several ranks on one GPU)")
     args = ap.parse_args()
@@ -423,8 +425,13 @@ def main():
     local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     peak, peak_kind = _peaks()
-    if ws > 1:
+    if ws > 1 or args.sharded:
         import torch.distributed as dist
+        if ws == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", str(29500 + (os.getpid() % 1000)))
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         if args.backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
