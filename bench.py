@@ -390,7 +390,8 @@ def sharded_run(args, dist, peak: float, local: int) -> dict:
             "sb": sb, "lean": bytes5[4], "nz": sh.nz, "neta": sh.neta, "p": p,
             "plan": {"ranks": pl.world, "split_stage": pl.split_stage, "stage_nodes_per_rank": pl.q,
                      "exchange_bytes": pl.xbuf_len * 8,
-                     "collective": f"all_gather ({dist.get_backend()}) of stage-ts records, once per T"}}
+                     "collective": f"all_gather ({dist.get_backend()}) of stage-ts records, once per T"
+                                   + (", ncclAllGather enqueued by the library on the solver stream" if sh.native else "")}}
 
 
 def _rand_vec(n, seed):

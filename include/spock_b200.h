@@ -262,6 +262,17 @@ typedef int (*spock_collective_fn)(void* user, int32_t op, double* dev_buf, int6
  * whole vector. */
 int spock_shard_weights(spock_solver* s, uint8_t* z_w, uint8_t* eta_w);
 int spock_shard_set_collectives(spock_solver* s, spock_collective_fn fn, void* user);
+/* Native collectives instead of the callback: rank 0 gets a 128-byte NCCL
+ * unique id (spock_nccl_unique_id), the host broadcasts it, and every rank
+ * calls spock_shard_nccl_init (after spock_shard_setup, same world / rank).
+ * From then on the exchanges and the sharded solves' reductions are
+ * ncclAllGather / ncclAllReduce calls enqueued by the library on
+ * spock_solver_stream's stream (no host round trip), and phase 2 of
+ * spock_shard_apply_T / spock_shard_bench runs a whole sharded T (phase 0,
+ * all-gather, phase 1) in one call.  NCCL is loaded at run time
+ * (libnccl.so.2). */
+int spock_nccl_unique_id(void* id_out);
+int spock_shard_nccl_init(spock_solver* s, const void* id, int32_t nranks, int32_t rank);
 void* spock_solver_stream(const spock_solver* s);
 
 /* The least-squares step of AndersonAccelerator::direction

@@ -17,8 +17,8 @@ LIB = os.path.join(OUT, "libspock_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-Wno-deprecated-gpu-targets", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr"]
-SOURCES = ["model.cpp", "kernels.cu", "narrow.cu", "fused.cu", "wide.cu", "wide_r1.cu", "wide_r2.cu", "wide_r3.cu", "wide_r4.cu", "wide_r5.cu", "wide_r8.cu", "lop.cu", "loop.cu", "setup_dev.cu", "engine.cu", "capi.cu"]
-HEADERS = ["aa.cuh", "model.hpp", "dev.cuh", "kernels.hpp", "fused.hpp", "fused_impl.cuh", "wide.hpp", "wide_impl.cuh", "loop.hpp", "loop_ctl.cuh", "small.cuh", "cluster.cuh", "engine.hpp", "setup_dev.hpp", os.path.join("..", "..", "include", "spock_b200.h")]
+SOURCES = ["model.cpp", "nccl_dl.cpp", "kernels.cu", "narrow.cu", "fused.cu", "wide.cu", "wide_r1.cu", "wide_r2.cu", "wide_r3.cu", "wide_r4.cu", "wide_r5.cu", "wide_r8.cu", "lop.cu", "loop.cu", "setup_dev.cu", "engine.cu", "capi.cu"]
+HEADERS = ["aa.cuh", "model.hpp", "dev.cuh", "kernels.hpp", "fused.hpp", "fused_impl.cuh", "wide.hpp", "wide_impl.cuh", "loop.hpp", "loop_ctl.cuh", "small.cuh", "cluster.cuh", "engine.hpp", "setup_dev.hpp", "nccl_dl.hpp", os.path.join("..", "..", "include", "spock_b200.h")]
 
 
 def _newest_header() -> float:
@@ -48,7 +48,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
             if r.returncode != 0:
                 raise subprocess.CalledProcessError(r.returncode, r.args)
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
-        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs]
+        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs, "-ldl"]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.run(cmd, check=True)

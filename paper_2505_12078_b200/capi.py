@@ -285,6 +285,8 @@ def load_library() -> C.CDLL:
     lib.spock_solver_loop_path.argtypes = [C.c_void_p]
     lib.spock_solver_loop_path.restype = C.c_char_p
     lib.spock_anderson_lstsq.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p]
+    lib.spock_nccl_unique_id.argtypes = [C.c_void_p]
+    lib.spock_shard_nccl_init.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32]
     _LIB = lib
     return lib
 
@@ -297,7 +299,7 @@ EXPORTED_SYMBOLS = [
     "spock_bench_kernels", "spock_traffic_model", "spock_solver_t_path", "spock_shard_setup", "spock_shard_apply_T",
     "spock_shard_bench", "spock_shard_masks", "spock_shard_weights", "spock_shard_set_collectives",
     "spock_solver_stream", "spock_solver_set_grid_cap", "spock_solver_grid", "spock_anderson_lstsq",
-    "spock_solver_loop_path",
+    "spock_solver_loop_path", "spock_nccl_unique_id", "spock_shard_nccl_init",
 ]
 
 

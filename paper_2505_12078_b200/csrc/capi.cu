@@ -8,6 +8,7 @@
 
 #include "../../include/spock_b200.h"
 #include "engine.hpp"
+#include "nccl_dl.hpp"
 
 struct spock_solver {
   spock::Engine* eng = nullptr;
@@ -229,6 +230,23 @@ int spock_shard_apply_T(spock_solver* s, int32_t phase, const double* z, const d
                         double* eta_out) {
   if (int rc = check(s)) return rc;
   return guard([&] { s->eng->shard_apply_T_b(phase, z, eta, z_out, eta_out); });
+}
+
+int spock_nccl_unique_id(void* id_out) {
+  return guard([&] {
+    if (!id_out) throw std::invalid_argument("spock_nccl_unique_id: null output");
+    ncclUniqueId u;
+    spock::nccl_check(spock::nccl_dl().GetUniqueId(&u), "ncclGetUniqueId");
+    std::memcpy(id_out, &u, sizeof(u));
+  });
+}
+
+int spock_shard_nccl_init(spock_solver* s, const void* id, int32_t nranks, int32_t rank) {
+  if (int rc = check(s)) return rc;
+  return guard([&] {
+    if (!id) throw std::invalid_argument("spock_shard_nccl_init: null id");
+    s->eng->shard_nccl_init(id, nranks, rank);
+  });
 }
 
 int spock_shard_bench(spock_solver* s, int32_t phase, int32_t parity) {

@@ -9,6 +9,7 @@
 #include "engine.hpp"
 #include "aa.cuh"
 #include "setup_dev.hpp"
+#include "nccl_dl.hpp"
 
 #include <chrono>
 #include <climits>
@@ -939,7 +940,7 @@ void Engine::gram_update(int cols, bool sharded) {
   const int n = 4 * cols;
   const double* src = gram_out_;
   int G = 1;
-  if (sharded && shard_.coll && shard_.G > 1) {
+  if (sharded && shard_coll_on() && shard_.G > 1) {
     G = shard_.G;
     if (!gram_gather_) gram_gather_ = dalloc<double>(size_t(G) * 4 * kAaHostMax);
     CK(cudaMemcpyAsync(gram_gather_ + size_t(shard_.rank) * n, gram_out_, sizeof(double) * n,
@@ -977,7 +978,7 @@ void Engine::gram_update(int cols, bool sharded) {
 // stops at this iteration or none does (a lone rank leaving would strand the
 // others in their next collective).  Unsharded: the callback's own answer.
 bool Engine::agree_cancel(bool mine) {
-  if (!shard_solving_ || !shard_.coll || shard_.G == 1) return mine;
+  if (!shard_solving_ || !shard_coll_on() || shard_.G == 1) return mine;
   if (!cancel_dev_) cancel_dev_ = dalloc<double>(1);
   host_red_[511] = mine ? 1.0 : 0.0;
   CK(cudaMemcpyAsync(cancel_dev_, host_red_ + 511, sizeof(double), cudaMemcpyHostToDevice, st_));
@@ -987,8 +988,32 @@ bool Engine::agree_cancel(bool mine) {
   return host_red_[511] != 0.0;
 }
 
+void Engine::shard_nccl_init(const void* id, int nranks, int rank) {
+  require(shard_.on, "spock_shard_nccl_init: call spock_shard_setup first");
+  require(nranks == shard_.G && rank == shard_.rank, "spock_shard_nccl_init: world / rank differ from the shard plan");
+  const NcclDl& N = nccl_dl();
+  ncclUniqueId u;
+  std::memcpy(&u, id, sizeof(u));
+  ncclComm_t c = nullptr;
+  nccl_check(N.CommInitRank(&c, nranks, u, rank), "ncclCommInitRank");
+  shard_.nccl = c;
+}
+
 void Engine::coll(int op, double* buf, int64_t n) {
-  if (!shard_.coll || shard_.G == 1 || n <= 0) return;
+  if (n <= 0) return;
+  if (shard_.nccl) {  // on the solver stream, ordered after the kernels that wrote buf
+    const NcclDl& N = nccl_dl();
+    ncclComm_t c = static_cast<ncclComm_t>(shard_.nccl);
+    if (op == 0 || op == 3) {  // all-gather in place: rank r's slice at r * count
+      const size_t cnt = op == 0 ? size_t(n / shard_.G) : size_t(n);
+      nccl_check(N.AllGather(buf + size_t(shard_.rank) * cnt, buf, cnt, ncclDouble, c, st_), "ncclAllGather");
+    } else {
+      nccl_check(N.AllReduce(buf, buf, size_t(n), ncclDouble, op == 1 ? ncclSum : ncclMax, c, st_),
+                 "ncclAllReduce");
+    }
+    return;
+  }
+  if (!shard_.coll || shard_.G == 1) return;
   if (shard_.coll(shard_.coll_user, op, buf, n) != 0) throw std::runtime_error("sharded solve: collective failed");
 }
 
@@ -1082,6 +1107,16 @@ void Engine::shard_masks(uint8_t* zm, uint8_t* em) const {
 // boundary-layout sharded T, in two calls around the host's all-gather
 void Engine::shard_apply_T_b(int phase, const double* z, const double* eta, double* zo, double* eo) {
   double *iz = scratch_z_[0], *ie = scratch_e_[0], *oz = scratch_z_[1], *oe = scratch_e_[1];
+  if (phase == 2) {  // the whole sharded T with the exchange in C++ (NCCL)
+    require(shard_.nccl != nullptr, "spock_shard_apply_T phase 2 needs spock_shard_nccl_init");
+    copy_in_z(z, iz);
+    to_internal_eta(eta, ie);
+    shard_T(iz, ie, oz, oe);
+    copy_out(oz, zo, lay_.nz);
+    from_internal_eta(oe, eo);
+    sync();
+    return;
+  }
   if (phase == 0) {
     copy_in_z(z, iz);
     to_internal_eta(eta, ie);
@@ -1098,10 +1133,14 @@ void Engine::shard_apply_T_b(int phase, const double* z, const double* eta, doub
 void Engine::shard_bench(int phase, int parity) {
   double *z0 = scratch_z_[parity], *e0 = scratch_e_[parity], *z1 = scratch_z_[1 - parity],
          *e1 = scratch_e_[1 - parity];
-  if (phase == 0)
+  if (phase == 2) {
+    require(shard_.nccl != nullptr, "spock_shard_bench phase 2 needs spock_shard_nccl_init");
+    shard_T(z0, e0, z1, e1);
+  } else if (phase == 0) {
     shard_T_A(z0, e0, z1, e1);
-  else
+  } else {
     shard_T_B(z0, e0, z1, e1);
+  }
 }
 
 void Engine::shard_T_A(const double* z, const double* eta, double* zo, double* eo) {
@@ -1148,6 +1187,12 @@ void Engine::set_grid_cap(int ctas) {
 Engine::~Engine() {
   for (GraphLoop& G : gloop_)
     if (G.exec) cudaGraphExecDestroy(G.exec);
+  if (shard_.nccl) {
+    try {
+      nccl_dl().CommDestroy(static_cast<ncclComm_t>(shard_.nccl));
+    } catch (...) {
+    }
+  }
   if (wargs_.prof) {  // SPOCK_WIDE_PROF=1: per-warp cycle shares of the wide kernel
     unsigned long long p[13] = {};
     try {
@@ -2447,7 +2492,7 @@ bool Engine::cluster_plan(int m) {
 }
 
 const char* Engine::loop_path() const {
-  if (shard_.on && shard_.coll) return "host";
+  if (shard_.on && shard_coll_on()) return "host";
   if (small_eligible()) return cluster_ok_ ? "cluster" : "small";
   const char* env = std::getenv("SPOCK_SOLVE_GRAPH");
   if (prm_.cancelled || prm_.aa_memory > kLoopMaxMem || (env && env[0] == '0')) return "host";
@@ -2809,7 +2854,7 @@ void Engine::solve_b(const double* x_init, const double* wz, const double* we, d
   // sharded solve: host-driven loop, T / L / L* over this rank's
   // items with the exchanges, every reduction over this rank's entries and
   // all-reduced (sums of dots, max of the xi norms) through the host's collectives
-  const bool sharded = shard_.on && shard_.coll != nullptr;
+  const bool sharded = shard_.on && shard_coll_on();
   struct Flag {
     bool& f;
     ~Flag() { f = false; }

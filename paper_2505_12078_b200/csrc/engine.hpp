@@ -124,6 +124,11 @@ class Engine {
   // exchange buffer, 1: all-reduce sum, 2: all-reduce max, on device buffers)
   typedef int (*CollFn)(void* user, int op, double* buf, int64_t n);
   void shard_set_collectives(CollFn fn, void* user);
+  // NCCL communicator over the ranks of the sharded solver (id: ncclUniqueId
+  // from rank 0); afterwards T, L*, the solves' reductions and the exchange all
+  // enqueue ncclAllGather / ncclAllReduce on the solver stream
+  void shard_nccl_init(const void* id, int nranks, int rank);
+  bool shard_coll_on() const { return shard_.coll != nullptr || shard_.nccl != nullptr; }
   cudaStream_t stream() const { return st_; }
   int device() const { return dev_; }
   double* scratch_z(int k) const { return scratch_z_[k]; }
@@ -228,6 +233,7 @@ class Engine {
   std::vector<WRec> wrecs_;  // host copy of the full ticket list (shard subsets are drawn from it)
   struct ShardState {
     bool on = false;
+    void* nccl = nullptr;  // ncclComm_t: the collectives run from C++ on the solver stream (shard_nccl_init)
     int G = 1, rank = 0, ts = 0, bfirst = 0, nbound = 0, q = 0, b0 = 0, b1 = 0, E = 0, nA = 0, nB = 0;
     WRec* recA = nullptr;
     WRec* recB = nullptr;

@@ -184,6 +184,21 @@ class ShardedSolver:
         self.stream = torch.cuda.ExternalStream(self.lib.spock_solver_stream(self.solver.h))
         self._capi = capi
         self._raise = _raise
+        # NCCL groups: the library runs the collectives itself (spock_shard_nccl_init:
+        # ncclAllGather / ncclAllReduce on the solver stream, no Python per
+        # exchange or reduction); SPOCK_SHARD_NCCL=0 keeps the torch.distributed path
+        import os
+        self.native = dist.get_backend(group) == "nccl" and os.environ.get("SPOCK_SHARD_NCCL", "1") != "0"
+        if self.native:
+            uid = (C.c_char * 128)()
+            if self.rank == 0:
+                _raise(self.lib, self.lib.spock_nccl_unique_id(C.cast(uid, C.c_void_p)))
+            box = [bytes(uid)]
+            dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                                       group=group)
+            uid = (C.c_char * 128).from_buffer_copy(box[0])
+            _raise(self.lib, self.lib.spock_shard_nccl_init(self.solver.h, C.cast(uid, C.c_void_p), self.world,
+                                                             self.rank))
 
     @property
     def alpha(self) -> float:
@@ -216,6 +231,11 @@ class ShardedSolver:
         z_out = np.zeros_like(z) if z_out is None else z_out
         eta_out = np.zeros_like(eta) if eta_out is None else eta_out
         nz, ne = self.nz, self.neta
+        if self.native:  # phase 0, the NCCL all-gather and phase 1 in one call
+            self._raise(self.lib, self.lib.spock_shard_apply_T(
+                self.solver.h, 2, _ptr(z, nz, "apply_T: z"), _ptr(eta, ne, "apply_T: eta"),
+                _ptr(z_out, nz, "apply_T: z_out"), _ptr(eta_out, ne, "apply_T: eta_out")))
+            return z_out, eta_out
         self._raise(self.lib, self.lib.spock_shard_apply_T(self.solver.h, 0, _ptr(z, nz, "apply_T: z"),
                                                            _ptr(eta, ne, "apply_T: eta"), None, None))
         self._exchange()
@@ -270,7 +290,7 @@ class ShardedSolver:
     def _solve(self, fn, x_init, history_capacity):
         from .capi import COLLECTIVE_FN
         from .solver import SolveResult, _ptr, make_status, status_dict
-        if not hasattr(self, "_cb"):
+        if not self.native and not hasattr(self, "_cb"):
             self._cb = COLLECTIVE_FN(self._collective)
             self._raise(self.lib, self.lib.spock_shard_set_collectives(self.solver.h, self._cb, None))
         st, rn, br = make_status(history_capacity)
@@ -304,6 +324,9 @@ class ShardedSolver:
 
     def bench_step(self, parity: int) -> None:
         """One sharded T on the device-resident scratch iterates (no host copies)."""
+        if self.native:
+            self._raise(self.lib, self.lib.spock_shard_bench(self.solver.h, 2, parity))
+            return
         self._raise(self.lib, self.lib.spock_shard_bench(self.solver.h, 0, parity))
         self._exchange()
         self._raise(self.lib, self.lib.spock_shard_bench(self.solver.h, 1, parity))

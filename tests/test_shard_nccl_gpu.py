@@ -24,8 +24,9 @@ def _free_port():
     return p
 
 
-def _worker(port, name, q):
+def _worker(port, name, native, q):
     sys.path.insert(0, ROOT)
+    os.environ["SPOCK_SHARD_NCCL"] = "1" if native else "0"
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -40,6 +41,7 @@ def _worker(port, name, q):
         from paper_2505_12078_b200.solver import SpockSolver
         p = make_config(name, seed=1)
         sh = ShardedSolver(p, split_stage=2, max_iters=30)
+        assert sh.native == native
         one = SpockSolver(p, alpha=sh.alpha, max_iters=30)
         z = -1.0 + 2.0 * Philox(3).uniform_array(sh.nz)
         e = -1.0 + 2.0 * Philox(53).uniform_array(sh.neta)
@@ -56,11 +58,15 @@ def _worker(port, name, q):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("native", [True, False], ids=["library-nccl", "torch-nccl"])
 @pytest.mark.parametrize("name", ["c1", "c2p"])
-def test_sharded_nccl_one_rank_matches_one_gpu(name):
+def test_sharded_nccl_one_rank_matches_one_gpu(name, native):
+    """native: the library's own NCCL communicator (spock_shard_nccl_init, every
+    collective enqueued from C++); else torch.distributed's NCCL collectives
+    through the host callback."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    pr = ctx.Process(target=_worker, args=(_free_port(), name, q))
+    pr = ctx.Process(target=_worker, args=(_free_port(), name, native, q))
     pr.start()
     err_T, same, err_s, iters = q.get(timeout=600)
     pr.join(timeout=60)
@@ -80,3 +86,4 @@ def test_bench_sharded_path_one_rank():
     line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
     assert line["n_gpus"] == 1 and line["value"] > 0 and line["scaling"] == "strong"
     assert line["sharded"]["collective"].startswith("all_gather (nccl)")
+    assert "enqueued by the library" in line["sharded"]["collective"]
