@@ -129,6 +129,8 @@ Engine::Engine(const spock_problem_desc* desc, const Params& prm) : prm_(prm) {
   mark("factorize (Alg. 1)");
   norm_.analytic_bound = analytic_norm_bound(p_, soc_);
   mark("analytic bound");
+  compute_pool();
+  mark("pooled blocks");
   setup_fused();
   setup_wide(false);
   CK(cudaStreamSynchronize(st_));
@@ -436,6 +438,108 @@ void Engine::setup_fused() {
 // per-warp TMA rings.  Default for trees the CTA-granular kernel does not take
 // (>= 4096 nodes); SPOCK_T_WIDE=0 selects the per-stage kernels instead,
 // SPOCK_T_WIDE=1 forces it on any tree the fused kernel is not used for.
+// Pooled blocks: nodes whose per-node matrices are bitwise identical share one
+// copy in the streaming kernel's records.  The generators share A, B, Q, R per
+// event (generators.cpp:89-95); on an iid tree every node of the same stage and
+// event then has the same subtree, hence the same Alg. 1 factors.  Exact
+// classes, bottom-up: a node's class is (its A, B, Q, R [, QN], its children's
+// classes in order); its blocks (H, H', M1, M1', K, K', R~^-1) depend only on
+// its class and its parent's class, so nodes agreeing on both stream the same
+// matrices (from L2 after the first).  Per-node perturbed problems have no
+// duplicates (every node is its own class) and are unchanged.
+void Engine::compute_pool() {
+  const Tree& tr = p_.tree;
+  const int nn = tr.nn(), nnl = tr.nnl(), N = tr.horizon;
+  const size_t nx = p_.nx, nu = p_.nu;
+  pool_rep_.resize(size_t(nn));
+  for (int i = 0; i < nn; ++i) pool_rep_[i] = i;
+  const char* env = std::getenv("SPOCK_POOL");
+  if (env && env[0] == '0') return;
+  struct Blk {
+    const double* p;
+    size_t n;
+  };
+  auto blocks = [&](int i, Blk (&b)[5]) {
+    int k = 0;
+    if (i > 0) {
+      const size_t r = size_t(i - 1);
+      b[k++] = {&p_.A[r * nx * nx], nx * nx};
+      b[k++] = {&p_.B[r * nx * nu], nx * nu};
+      b[k++] = {&p_.Q[r * nx * nx], nx * nx};
+      b[k++] = {&p_.R[r * nu * nu], nu * nu};
+    }
+    if (i >= nnl) b[k++] = {&p_.QN[size_t(i - nnl) * nx * nx], nx * nx};
+    return k;
+  };
+  std::vector<uint64_t> dh(size_t(nn), 0);
+  parallel_for(nn, [&](int64_t ii) {
+    Blk b[5];
+    const int nb = blocks(int(ii), b);
+    uint64_t h = 0x9E3779B97F4A7C15ull ^ uint64_t(nb);
+    for (int q = 0; q < nb; ++q) {
+      const uint64_t* w = reinterpret_cast<const uint64_t*>(b[q].p);
+      for (size_t t = 0; t < b[q].n; ++t) {
+        h = (h ^ w[t]) * 0xFF51AFD7ED558CCDull;
+        h ^= h >> 31;
+      }
+    }
+    dh[size_t(ii)] = h;
+  });
+  auto same_data = [&](int a, int b) {
+    Blk x[5], y[5];
+    const int na = blocks(a, x), nb = blocks(b, y);
+    if (na != nb) return false;
+    for (int q = 0; q < na; ++q)
+      if (std::memcmp(x[q].p, y[q].p, sizeof(double) * x[q].n) != 0) return false;
+    return true;
+  };
+  // exact classes bottom-up (stage by stage, leaves first)
+  std::vector<int> cls(size_t(nn), -1);
+  std::vector<int> rep_of_cls;
+  std::unordered_map<uint64_t, std::vector<int>> cand;  // signature hash -> class ids
+  for (int t = N; t >= 0; --t) {
+    for (int i = tr.stage_start[t]; i < tr.stage_start[t + 1]; ++i) {
+      const int c0 = tr.child_first[i], nc = tr.child_count[i];
+      uint64_t h = dh[size_t(i)] ^ (uint64_t(nc) << 48);
+      for (int c = 0; c < nc; ++c) h = (h ^ uint64_t(cls[size_t(c0 + c)] + 1)) * 0x9E3779B97F4A7C15ull;
+      int found = -1;
+      for (int k : cand[h]) {
+        const int r = rep_of_cls[size_t(k)];
+        if (tr.child_count[r] != nc || !same_data(i, r)) continue;
+        bool ok = true;
+        for (int c = 0; c < nc && ok; ++c) ok = cls[size_t(c0 + c)] == cls[size_t(tr.child_first[r] + c)];
+        if (ok) {
+          found = k;
+          break;
+        }
+      }
+      if (found < 0) {
+        found = int(rep_of_cls.size());
+        rep_of_cls.push_back(i);
+        cand[h].push_back(found);
+      }
+      cls[size_t(i)] = found;
+    }
+  }
+  // blocks of node i depend on (class of i, class of its parent)
+  std::map<std::pair<int, int>, int> first;
+  int shared = 0;
+  for (int i = 0; i < nn; ++i) {
+    const std::pair<int, int> key{cls[size_t(i)], i > 0 ? cls[size_t(tr.anc[i])] : -1};
+    auto it = first.find(key);
+    if (it == first.end()) {
+      first.emplace(key, i);
+    } else {
+      pool_rep_[size_t(i)] = it->second;
+      ++shared;
+    }
+  }
+  pool_unique_ = nn - shared;
+  if (std::getenv("SPOCK_DEBUG_SETUP"))
+    std::fprintf(stderr, "[pool] %d nodes, %d classes, %d distinct block sets\n", nn, int(rep_of_cls.size()),
+                 pool_unique_);
+}
+
 void Engine::setup_wide(bool force) {
   wide_ok_ = false;
   t_wide_ = false;
@@ -542,34 +646,35 @@ void Engine::setup_wide(bool force) {
   enum { B_SEG3 = B_ZU, B_GDN = B_GD, B_QKN = B_H };
   enum { F_ZX = 0, F_ZU, F_AX, F_AU, F_CV, F_SEG2, F_A, F_QK, F_SEG1, F_RB, F_GD, F_LO, F_HI, F_ZY, F_ZT, F_ZS };
   enum { F_SEG3 = F_SEG1, F_AN = F_RB, F_QKN = F_GD, F_GDN = F_LO, F_LON = F_HI, F_HIN = F_ZY };
+  const std::vector<int>& pr = pool_rep_;  // matrix blocks: the node's pooled representative
   for (int k = 0; k < nn; ++k) {  // backward items
     const int i = nn - 1 - k;
     WRec& R = recs[size_t(k)];
     meta(R, 0, i);
     const bool leaf = tr.leaf(i), root = i == 0;
     if (!root) {
-      mat(R, D_.HxT + hxo[i - 1], nx, R.px);
-      mat(R, D_.HuT + huo[i - 1], nu, R.pu);
+      mat(R, D_.HxT + hxo[pr[i] - 1], nx, R.px);
+      mat(R, D_.HuT + huo[pr[i] - 1], nu, R.pu);
       span(R, B_HEAD, WB_ETA, R.s2o, R.px + R.pu + 2);
       span(R, B_QK, WB_QK, int64_t(i - 1) * m, m);
     }
     span(R, B_ZX, WB_Z, 1 + int64_t(i) * nx, nx);
     if (leaf) {
       const int j = i - nnl;
-      mat(R, D_.HNT + hno[j], nx, R.pN);
+      mat(R, D_.HNT + hno[pr[i] - nnl], nx, R.pN);
       span(R, B_SEG3, WB_ETA, R.so, R.nc + R.pN + 2);
       if (D_.gN_diag) span(R, B_GDN, WB_GDN, int64_t(j) * nx, nx);
       span(R, B_QKN, WB_QKN, int64_t(j) * nx, nx);
     } else {
-      mat(R, D_.KT + size_t(i) * D_.k_stride, nx, nu);
-      mat(R, D_.Rinv + size_t(i) * D_.r_stride, nu, nu);
+      mat(R, D_.KT + size_t(pr[i]) * D_.k_stride, nx, nu);
+      mat(R, D_.Rinv + size_t(pr[i]) * D_.r_stride, nu, nu);
       span(R, B_ZU, WB_Z, lay_.u_base + int64_t(i) * nu, nu);
       span(R, B_EC, WB_ETA, R.so + R.ny, 1 + R.nc);
       if (D_.g_diag) span(R, B_GD, WB_GD, int64_t(i) * m, m);
       span(R, B_H, WB_H, int64_t(i) * nx, nx);
       span(R, B_G, WB_G, int64_t(i) * nu, nu);
     }
-    if (!root) mat(R, D_.M1T + size_t(i - 1) * D_.m1_stride, m, nx);
+    if (!root) mat(R, D_.M1T + size_t(pr[i] - 1) * D_.m1_stride, m, nx);
   }
   for (int i = 0; i < nnl; ++i) meta(recs[size_t(nn) + i], 1, i);
   for (int c = 0; c < nn; ++c) {  // forward items
@@ -580,7 +685,7 @@ void Engine::setup_wide(bool force) {
     span(R, F_ZX, WB_Z, 1 + int64_t(c) * nx, nx);
     if (!leaf) span(R, F_ZU, WB_Z, lay_.u_base + int64_t(c) * nu, nu);
     if (!root) {
-      mat(R, D_.M1 + size_t(c - 1) * D_.m1_stride, nx, m);
+      mat(R, D_.M1 + size_t(pr[c] - 1) * D_.m1_stride, nx, m);
       span(R, F_AX, WB_Z, 1 + int64_t(an) * nx, nx);
       span(R, F_AU, WB_Z, lay_.u_base + int64_t(an) * nu, nu);
       span(R, F_CV, WB_CV, int64_t(c - 1) * nx, nx);
@@ -589,10 +694,10 @@ void Engine::setup_wide(bool force) {
       span(R, F_QK, WB_QK, int64_t(c - 1) * m, m);
       span(R, F_ZT, WB_Z, lay_.tau_base + c - 1, 1);
     }
-    if (!leaf) mat(R, D_.K + size_t(c) * D_.k_stride, nu, nx);
+    if (!leaf) mat(R, D_.K + size_t(pr[c]) * D_.k_stride, nu, nx);
     if (!root) {
-      mat(R, D_.Hx + hxo[c - 1], R.px, nx);
-      mat(R, D_.Hu + huo[c - 1], R.pu, nu);
+      mat(R, D_.Hx + hxo[pr[c] - 1], R.px, nx);
+      mat(R, D_.Hu + huo[pr[c] - 1], R.pu, nu);
     }
     span(R, F_ZS, WB_Z, root ? 0 : lay_.s_base + c - 1, 1);
     if (!leaf) {
@@ -606,7 +711,7 @@ void Engine::setup_wide(bool force) {
     } else {
       const int j = c - nnl;
       const int64_t go = p_.gN_off[j];
-      mat(R, D_.HN + hno[j], R.pN, nx);
+      mat(R, D_.HN + hno[pr[c] - nnl], R.pN, nx);
       span(R, F_SEG3, WB_ETA, R.so, R.nc + R.pN + 2);
       span(R, F_AN, WB_AN, aNo[j], R.pN + 2);
       span(R, F_QKN, WB_QKN, int64_t(j) * nx, nx);
@@ -635,8 +740,8 @@ void Engine::setup_wide(bool force) {
     }
     if (!root) {
       const int an = R.anc;
-      mat(R, D_.Hx + hxo[i - 1], R.px, nx);
-      mat(R, D_.Hu + huo[i - 1], R.pu, nu);
+      mat(R, D_.Hx + hxo[pr[i] - 1], R.px, nx);
+      mat(R, D_.Hu + huo[pr[i] - 1], R.pu, nu);
       span(R, L_AX, WB_Z, 1 + int64_t(an) * nx, nx);
       span(R, L_AU, WB_Z, lay_.u_base + int64_t(an) * nu, nu);
       span(R, L_QK, WB_QK, int64_t(i - 1) * m, m);
@@ -644,7 +749,7 @@ void Engine::setup_wide(bool force) {
     }
     if (leaf) {
       const int j = i - nnl;
-      mat(R, D_.HN + hno[j], R.pN, nx);
+      mat(R, D_.HN + hno[pr[i] - nnl], R.pN, nx);
       if (D_.gN_diag) span(R, L_GD, WB_GDN, int64_t(j) * nx, nx);
       span(R, L_QKN, WB_QKN, int64_t(j) * nx, nx);
       span(R, L_ZS, WB_Z, lay_.s_base + i - 1, 1);
@@ -653,8 +758,8 @@ void Engine::setup_wide(bool force) {
   for (int i = 1; i < nn; ++i) {
     WRec R;
     meta(R, 4, i);
-    mat(R, D_.HxT + hxo[i - 1], nx, R.px);
-    mat(R, D_.HuT + huo[i - 1], nu, R.pu);
+    mat(R, D_.HxT + hxo[pr[i] - 1], nx, R.px);
+    mat(R, D_.HuT + huo[pr[i] - 1], nu, R.pu);
     span(R, LC_HEAD, WB_ETA, R.s2o, R.px + R.pu + 2);
     span(R, LC_QK, WB_QK, int64_t(i - 1) * m, m);
     ltrecs.push_back(R);
@@ -668,7 +773,7 @@ void Engine::setup_wide(bool force) {
       if (D_.g_diag) span(R, LN_GD, WB_GD, int64_t(i) * m, m);
     } else {
       const int j = i - nnl;
-      mat(R, D_.HNT + hno[j], nx, R.pN);
+      mat(R, D_.HNT + hno[pr[i] - nnl], nx, R.pN);
       span(R, LN_SEG1, WB_ETA, R.so, R.nc + R.pN + 2);
       if (D_.gN_diag) span(R, LN_GD, WB_GDN, int64_t(j) * nx, nx);
       span(R, LN_QKN, WB_QKN, int64_t(j) * nx, nx);

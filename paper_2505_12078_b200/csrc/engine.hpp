@@ -8,6 +8,7 @@
 
 #include <functional>
 #include <map>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -162,6 +163,9 @@ class Engine {
                         const std::vector<int64_t>& aNo);
   void setup_fused();
   void setup_wide(bool force);
+  void compute_pool();
+  std::vector<int> pool_rep_;  // node whose matrix blocks the streaming kernel reads for node i
+  int pool_unique_ = 0;
   void factorize();
   void power_iteration();
   void set_xinit(const double* x_orig_host);
