@@ -566,17 +566,18 @@ void Engine::setup_wide(bool force) {
   WideArgs& A = wargs_;
   A = WideArgs{};
   A.warps = std::max(1, std::min(8, knob("SPOCK_WIDE_WARPS", 8)));
+  // deep narrow trees: fewer items per level than resident warps
+  const bool latency_mode = double(nn) / double(tr.horizon + 1) < 148.0 * 2 * 6;
   {
     // Deep, narrow trees (a 100-stage horizon: ~1 000 items per level for ~1 800
     // resident warps) are bound by the latency of one item per level, not by
     // bandwidth: a 4-slot ring per warp (fewer warps) shortens each item
     // (measured (100, 10, 3): 6.14 -> 5.31 ms per T; wide levels prefer 2 slots)
-    const double width = double(nn) / double(tr.horizon + 1);
-    const int lat_slots = width < 148.0 * 2 * 6 ? 4 : 2;
+    const int lat_slots = latency_mode ? 4 : 2;
     const int sl = std::max(1, std::min(16, knob("SPOCK_WIDE_SLOTS", lat_slots)));
     A.slots = sl >= 16 ? 16 : (sl >= 8 ? 8 : (sl >= 4 ? 4 : (sl >= 2 ? 2 : 1)));  // power of two
   }
-  A.chunk = std::max(512, knob("SPOCK_WIDE_CHUNK", 512)) & ~1;
+  A.chunk = std::max(256, knob("SPOCK_WIDE_CHUNK", 512)) & ~1;
   // staging capacities sized for the common items: rare wide parents (a 100-way
   // fan-out has 201-row risk blocks) read their large spans in place, so they
   // do not inflate every warp's shared memory (fewer resident warps)
@@ -630,10 +631,17 @@ void Engine::setup_wide(bool force) {
     R.mcols[R.nmat] = int16_t(cols);
     ++R.nmat;
   };
+  // Only the iterate spans (z, eta) are staged: the per-node constants (boxes,
+  // diagonal G, q_kernel, translations, c, g, h, risk b) are read in place, which
+  // shrinks every warp's staging buffer (c4: 814 -> 358 doubles) and fits 8 warps
+  // per CTA instead of 6 (c4 T 3.31 -> 3.06 ms, c5s 13.4 -> 11.8 ms).  Deep narrow
+  // trees keep them staged: there every item is on the latency-bound critical
+  // path ((100, 10, 3): 5.31 ms staged, 6.34 ms in place)
+  const bool stage_const = knob("SPOCK_WIDE_STAGE_CONST", latency_mode ? 1 : 0) != 0;
   auto span = [&](WRec& R, int id, int base, int64_t off, int64_t cnt) {
     R.vbase[id] = uint8_t(base);
     R.voff[id] = int32_t(off);
-    if (cnt > 160 || off > INT32_MAX) {  // read in place (wide fan-out risk blocks)
+    if (cnt > 160 || off > INT32_MAX || (!stage_const && base != WB_Z && base != WB_ETA)) {  // read in place
       R.unstaged |= 1 << id;
       R.vcnt[id] = 0;
     } else {
