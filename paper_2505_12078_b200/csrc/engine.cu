@@ -2588,6 +2588,7 @@ bool Engine::cluster_plan(int m) {
     if (!fits) continue;
     size_t arena = 16;
     for (size_t u : used) arena = std::max(arena, (u + 15) & ~size_t(15));
+    if (cluster_max_active(C, int(arena)) < 1) continue;  // the device cannot co-schedule this cluster
     cplace_d_ = dupload(pl);
     cfield_d_ = dupload(fl);
     cplace_n_ = int(pl.size());

@@ -1090,26 +1090,54 @@ int cluster_static_smem() {
   return int(fa.sharedSizeBytes);
 }
 
-cudaError_t launch_cluster_solve(const ClusterArgs& A, int ctas, int arena_bytes, cudaStream_t st) {
-  const void* fn = reinterpret_cast<const void*>(&k_cluster_solve);
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, arena_bytes);
-  if (e != cudaSuccess) return e;
-  if (ctas > 8) {
-    e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (e != cudaSuccess) return e;
-  }
+// attributes are process-wide per function: set once, to the device's opt-in
+// maximum, so concurrent solvers with different arenas never lower each
+// other's limit between attribute and launch
+static cudaError_t cluster_attrs_once() {
+  static cudaError_t err = [] {
+    const void* fn = reinterpret_cast<const void*>(&k_cluster_solve);
+    int dev = 0, optin = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - cluster_static_smem());
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    return e;
+  }();
+  return err;
+}
+
+static cudaLaunchConfig_t cluster_cfg(int ctas, int arena_bytes, cudaStream_t st, cudaLaunchAttribute* at) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(ctas);
   cfg.blockDim = dim3(kSmallThreads);
   cfg.dynamicSmemBytes = size_t(arena_bytes);
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = unsigned(ctas);
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  return cfg;
+}
+
+int cluster_max_active(int ctas, int arena_bytes) {
+  if (cluster_attrs_once() != cudaSuccess) return 0;
+  cudaLaunchAttribute at[1];
+  cudaLaunchConfig_t cfg = cluster_cfg(ctas, arena_bytes, nullptr, at);
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, reinterpret_cast<const void*>(&k_cluster_solve), &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+cudaError_t launch_cluster_solve(const ClusterArgs& A, int ctas, int arena_bytes, cudaStream_t st) {
+  if (cudaError_t e = cluster_attrs_once(); e != cudaSuccess) return e;
+  cudaLaunchAttribute at[1];
+  cudaLaunchConfig_t cfg = cluster_cfg(ctas, arena_bytes, st, at);
   return cudaLaunchKernelEx(&cfg, k_cluster_solve, A);
 }
 

@@ -113,6 +113,8 @@ int cluster_static_smem();
 // arena bytes per CTA and cluster size; returns the launch error (cluster
 // launches fail, e.g., when the arena does not fit)
 cudaError_t launch_cluster_solve(const ClusterArgs& A, int ctas, int arena_bytes, cudaStream_t st);
+// clusters of this shape the device can hold at once (0: it cannot launch)
+int cluster_max_active(int ctas, int arena_bytes);
 
 void launch_Lt(const Dev& D, const double* eta, const double* zin, double* zout, double a, double b, double c0,
                cudaStream_t st);
