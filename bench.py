@@ -264,6 +264,35 @@ def sweep_point(config: str, seed: int, steps: int, peak: float, cpu: bool) -> d
     return row
 
 
+def seed_block(config: str, peak: float, cpu: bool, seeds=(1, 2, 3, 4, 5)) -> dict:
+    """BASELINE.md §4 inputs are Philox seeds 1-5: the headline T on every
+    seed (device ms, L2 flushed; lean-byte roofline), and c1's CP solve to
+    1e-4 on every seed beside the CPU oracle (same iterations expected)."""
+    from paper_2505_12078_b200.solver import SpockSolver
+    out = {"config": config, "T": [], "c1_cp_1e-4": []}
+    for sd in seeds:
+        r = sweep_point(config, sd, 20, peak, False)
+        out["T"].append({"seed": sd, "ms_per_T": r["ms_per_T"], "frac_lean": r["frac_lean"],
+                         "frac_survey": r["frac_survey"]})
+    if cpu:
+        from oracle import oracle
+        for sd in seeds:
+            p = _problem("c1", sd)
+            kw = dict(eps_abs=1e-4, eps_rel=1e-4, max_iters=50000)
+            g = SpockSolver(p, **kw)
+            g.solve_cp(p.x_init)
+            a, gms = _timed(g.solve_cp, p.x_init)
+            o = oracle.OracleSolver(p, alpha=g.alpha, **kw)
+            b, cms = _timed(o.solve_cp, p.x_init)
+            out["c1_cp_1e-4"].append({
+                "seed": sd, "gpu_ms": gms, "cpu_ms": cms, "gpu_iterations": a.status["iterations"],
+                "cpu_iterations": b.status["iterations"], "loop": g.loop_path,
+                "solution_rel_diff": float(np.abs(a.z - b.z).max() / max(1.0, np.abs(b.z).max()))})
+    ts = [x["ms_per_T"] for x in out["T"]]
+    out["T_ms_min_median_max"] = [min(ts), sorted(ts)[len(ts) // 2], max(ts)]
+    return out
+
+
 def _prefix(a: str, b: str) -> int:
     n = min(len(a), len(b))
     for k in range(n):
@@ -411,6 +440,8 @@ def main():
     ap.add_argument("--sweep", default="c3,c2p,c2", help="extra single-GPU configs (N=1 only); '' disables")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--side-by-side", default="quick", choices=["quick", "full", "none"])
+    ap.add_argument("--seeds", type=int, default=1, help="1: the seeds 1-5 block (headline T per seed, c1 CP "
+                    "to 1e-4 per seed beside the oracle); 0: skip")
     ap.add_argument("--sharded", action="store_true", help="run the subtree-sharded path even on one rank "
                     "(exercises the N > 1 code path, NCCL included, on a single GPU)")
     ap.add_argument("--backend", default="nccl", help="process group backend for N>1 (gloo: code-path smoke test "
@@ -519,6 +550,12 @@ def main():
                 sweep.append(sweep_point(c, args.seed, max(20, min(args.steps, 100)), peak, not args.no_cpu))
             except Exception as ex:  # keep the headline line even if a sweep point fails
                 sweep.append({"config": c, "error": str(ex)[:200]})
+    seeds = None
+    if args.seeds:
+        try:
+            seeds = seed_block(args.config, peak, not args.no_cpu)
+        except Exception as ex:
+            seeds = {"error": str(ex)[:300]}
     side = None
     if args.side_by_side != "none" and not args.no_cpu:
         try:
@@ -546,6 +583,7 @@ def main():
         "setup_s": setup_s,
         "sweep": sweep,
         "solve_side_by_side": side,
+        "seeds": seeds,
     }
     print(json.dumps(line), flush=True)
 

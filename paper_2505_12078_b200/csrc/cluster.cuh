@@ -175,6 +175,7 @@ __device__ void cl_gram(CDist& c, const LoopArgs& A, const LoopState* S, double*
   double* wl = wred + 2 * M * kSW;
 #pragma unroll
   for (int j = 0; j < 2 * M; ++j) {
+    if ((j < M ? j : j - M) >= cols) continue;  // only the 2 cols sums in use (block-uniform)
     dd v = acc[j];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {

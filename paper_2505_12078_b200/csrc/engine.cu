@@ -2892,11 +2892,11 @@ void Engine::build_loop_graph(GraphLoop& G, bool supermann) {
     X.x[1] = R + nz, X.y[1] = Lrz, X.d[1] = d2_, X.n[1] = int(ne);
     X.alpha = alpha;
     launch_xi(X, partial_ + kRedRegion, red_out_ + 4, st_);
-    if (supermann) {
-      loop_push(A, st_);
+    if (supermann) {  // history push, Gram update and the controller in one launch
       loop_gram(A, gram_partial_, red_out_ + 8, st_);
+    } else {
+      loop_begin(A, st_);
     }
-    loop_begin(A, st_);
     if (supermann) loop_psi(A, st_);
   });
   cudaGraphNode_t n_top = child(body, gtop, nullptr);

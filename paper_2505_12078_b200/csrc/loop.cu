@@ -54,9 +54,19 @@ __device__ __forceinline__ dd warp_sum_dd(dd v) {
   return v;
 }
 
+// push (graph loop): the history push fused in -- dnew = first ? r : r - rp is
+// written to the new difference column as it is read, and r to the new
+// residual slot; ctl: the controller (ctl_begin) runs in the last block
+struct GramPush {
+  double* dn;
+  double* rn;
+  const double* rp;
+  int first;
+  const LoopArgs* ctl;
+};
 __device__ void gram_dd_body(const double* __restrict__ dnew, const double* __restrict__ r,
                              const double* const* D, const double* __restrict__ w, int cols, int64_t n,
-                             double* __restrict__ partial, double* out) {
+                             double* __restrict__ partial, double* out, const GramPush* push = nullptr) {
   constexpr int M = kLoopMaxMem;
   constexpr int NW = kRedThreads / 32;
   __shared__ double sh[2 * M][NW], sl[2 * M][NW];
@@ -68,11 +78,19 @@ __device__ void gram_dd_body(const double* __restrict__ dnew, const double* __re
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += stride) {
     // entries with weight 0 may hold anything (another rank computes them): skipped, not multiplied
     if (w && w[i] == 0.0) continue;
-    const double x = dnew[i], rr = r[i];
+    const double rr = r[i];
+    double x;
+    if (push) {
+      x = push->first ? rr : rr - push->rp[i];
+      push->dn[i] = x;
+      push->rn[i] = rr;
+    } else {
+      x = dnew[i];
+    }
 #pragma unroll
     for (int b = 0; b < M; ++b)
       if (b < cols) {
-        const double db = D[b][i];
+        const double db = (push && b == 0) ? x : D[b][i];  // push: column 0 is the one being written
         acc[b] = dd_fma(acc[b], x, db);
         acc[M + b] = dd_fma(acc[M + b], db, rr);
       }
@@ -80,6 +98,7 @@ __device__ void gram_dd_body(const double* __restrict__ dnew, const double* __re
   const int wp = threadIdx.x >> 5, nd = 2 * cols;
 #pragma unroll
   for (int j = 0; j < 2 * M; ++j) {
+    if ((j < M ? j : j - M) >= cols) continue;  // only the 2 cols sums in use (warp-uniform)
     const dd v = warp_sum_dd(acc[j]);
     if ((threadIdx.x & 31) == 0) sh[j][wp] = v.hi, sl[j][wp] = v.lo;
   }
@@ -115,7 +134,10 @@ __device__ void gram_dd_body(const double* __restrict__ dnew, const double* __re
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) *counter = 0u;
+  if (threadIdx.x == 0) {
+    *counter = 0u;
+    if (push && push->ctl) ctl_begin<true>(*push->ctl);
+  }
 }
 
 // graph loop: the history columns come from the device ring (head hn = h + 1)
@@ -126,7 +148,8 @@ __global__ void __launch_bounds__(kRedThreads) k_gram(const __grid_constant__ Lo
   const double* D[kLoopMaxMem];
 #pragma unroll
   for (int b = 0; b < kLoopMaxMem; ++b) D[b] = A.DH[ring(hn - min(b, cols - 1), m)];
-  gram_dd_body(D[0], A.R, D, nullptr, cols, A.nv, partial, out);
+  const GramPush P{A.DH[ring(hn, m)], A.RH[ring(hn, m + 1)], A.RH[ring(hn - 1, m + 1)], S.aa_k == 0 ? 1 : 0, &A};
+  gram_dd_body(D[0], A.R, D, nullptr, cols, A.nv, partial, out, &P);
 }
 
 __global__ void __launch_bounds__(kRedThreads) k_gram_args(const __grid_constant__ GramArgs G, double* __restrict__ partial,
