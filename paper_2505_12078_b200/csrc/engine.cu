@@ -2923,12 +2923,15 @@ void Engine::build_loop_graph(GraphLoop& G, bool supermann) {
     child(lsb, capture([&] {
             loop_axpy_tau(A, st_);
             refresh(C, TC, CR, cLrz);
-            mnorm(CR, cLrz);
+            // the candidate's M-norm dots and <r~, M psi> in one launch: red[0..3), red[3..5)
             DotArgs D{};
-            D.x[0] = CR, D.y[0] = PV, D.n[0] = int(nz);
-            D.x[1] = CR + nz, D.y[1] = PV + nz, D.n[1] = int(ne);
-            D.ndots = 2;
-            launch_dots(D, partial_ + 3 * kRedRegion, red_out_ + 3, st_);
+            D.x[0] = CR, D.y[0] = CR, D.n[0] = int(nz);
+            D.x[1] = CR + nz, D.y[1] = cLrz, D.n[1] = int(ne);
+            D.x[2] = CR + nz, D.y[2] = CR + nz, D.n[2] = int(ne);
+            D.x[3] = CR, D.y[3] = PV, D.n[3] = int(nz);
+            D.x[4] = CR + nz, D.y[4] = PV + nz, D.n[4] = int(ne);
+            D.ndots = 5;
+            launch_dots(D, partial_, red_out_, st_);
             loop_ls(A, st_);
           }),
           nullptr);
