@@ -377,39 +377,41 @@ struct Spans {
   }
 };
 
-// lane 0: bulk-copy the item's staged spans (16-byte aligned supersets) into
-// vrec; one mbarrier phase per item (completes at once when nothing is staged)
+// bulk-copy the item's staged spans (16-byte aligned supersets) into vrec, one
+// span per lane (offsets by a warp prefix sum); one mbarrier phase per item
+// (completes at once when nothing is staged)
 __device__ void stage_spans(const WideArgs& A, const WRec& rc, double* vrec, int* doff, uint64_t* sbar) {
-  if (lane_id() != 0) return;
+  const int l = lane_id();
   // z / eta may be 8-byte aligned sub-vectors (SuperMann's stacked (z | eta)):
   // the alignment shift is taken from the address
-  int off = 0;
-  uint32_t total = 0;
-  for (int k = 0; k < rc.nspan; ++k) {
-    const int n = rc.vcnt[k];
-    if (((rc.unstaged >> k) & 1) || n == 0) {
-      doff[k] = 0;
-      continue;
+  int nn = 0, sh = 0;
+  const double* src = nullptr;
+  if (l < rc.nspan) {
+    const int n = rc.vcnt[l];
+    if (!(((rc.unstaged >> l) & 1) || n == 0)) {
+      const int b = rc.vbase[l];
+      src = (b == WB_Z ? A.z : (b == WB_ETA ? A.eta : A.vb[b])) + rc.voff[l];
+      sh = int((reinterpret_cast<uintptr_t>(src) >> 3) & 1);
+      nn = (n + sh + 1) & ~1;
     }
-    const int b = rc.vbase[k];
-    const double* src = (b == WB_Z ? A.z : (b == WB_ETA ? A.eta : A.vb[b])) + rc.voff[k];
-    const int sh = int((reinterpret_cast<uintptr_t>(src) >> 3) & 1);
-    doff[k] = off + sh;
-    off += (n + sh + 1) & ~1;
   }
-  total = uint32_t(off) * 8u;
-  fence_proxy_async();
-  mbar_expect_tx(sbar, total);
-  off = 0;
-  for (int k = 0; k < rc.nspan; ++k) {
-    const int n = rc.vcnt[k];
-    if (((rc.unstaged >> k) & 1) || n == 0) continue;
-    const int b = rc.vbase[k];
-    const double* src = (b == WB_Z ? A.z : (b == WB_ETA ? A.eta : A.vb[b])) + rc.voff[k];
-    const int sh = int((reinterpret_cast<uintptr_t>(src) >> 3) & 1);
-    const int nn = (n + sh + 1) & ~1;
+  int incl = nn;  // inclusive prefix sum over the lanes (span order)
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (l >= o) incl += v;
+  }
+  const int off = incl - nn;
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  if (l < rc.nspan) doff[l] = nn ? off + sh : 0;
+  if (l == 0) {
+    fence_proxy_async();
+    mbar_expect_tx(sbar, uint32_t(total) * 8u);
+  }
+  __syncwarp();
+  if (nn) {
+    fence_proxy_async();
     bulk_g2s(vrec + off, src - sh, uint32_t(nn) * 8u, sbar);
-    off += nn;
   }
 }
 
