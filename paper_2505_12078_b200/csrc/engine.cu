@@ -637,7 +637,14 @@ void Engine::setup_wide(bool force) {
   // per CTA instead of 6 (c4 T 3.31 -> 3.06 ms, c5s 13.4 -> 11.8 ms).  Deep narrow
   // trees keep them staged: there every item is on the latency-bound critical
   // path ((100, 10, 3): 5.31 ms staged, 6.34 ms in place)
-  const bool stage_const = knob("SPOCK_WIDE_STAGE_CONST", latency_mode ? 1 : 0) != 0;
+  int max_fan = 0;
+  for (int i = 0; i < nnl; ++i) max_fan = std::max(max_fan, tr.child_count[i]);
+  // latency-sensitive shapes keep the constants staged: deep or narrow trees (many
+  // dependent levels) and wide fan-outs (slow parents on the critical path).
+  // Measured: staged wins on (48, 3, 7) 3.27 vs 3.60 ms, (12, 100, 2) 4.12 vs 4.41,
+  // (100, 10, 3) 4.94 vs 6.32; in place wins on c3, c4, (12, 4, 7) and c5s.
+  const bool lat_sensitive = latency_mode || tr.horizon >= 40 || max_fan >= 50;
+  const bool stage_const = knob("SPOCK_WIDE_STAGE_CONST", lat_sensitive ? 1 : 0) != 0;
   auto span = [&](WRec& R, int id, int base, int64_t off, int64_t cnt) {
     R.vbase[id] = uint8_t(base);
     R.voff[id] = int32_t(off);
