@@ -307,11 +307,17 @@ Problem problem_from_desc(const spock_problem_desc* d) {
   P.A = big(d->A, nr, int(nx), int(nx));
   P.B = big(d->B, nr, int(nx), int(nu));
   P.c = cp(d->c, nr * nx);
-  P.Q = big(d->Q, nr, int(nx), int(nx));
-  P.R = big(d->R, nr, int(nu), int(nu));
+  // Q, R, QN must be symmetric (validate() rejects them otherwise), so their
+  // row-major and column-major images coincide: plain parallel copies
+  auto sym = [&](const double* s, size_t nb, int n) {
+    require(nb == 0 || s != nullptr, "Raocp: missing data array");
+    return BigVec(s, nb * size_t(n) * n);
+  };
+  P.Q = sym(d->Q, nr, int(nx));
+  P.R = sym(d->R, nr, int(nu));
   P.q = cp(d->q, nr * nx);
   P.r = cp(d->r, nr * nu);
-  P.QN = big(d->QN, nl, int(nx), int(nx));
+  P.QN = sym(d->QN, nl, int(nx));
   P.qN = cp(d->qN, nl * nx);
   P.nc.assign(d->nc, d->nc + nnl);
   P.ncN.assign(d->ncN, d->ncN + nl);
