@@ -66,3 +66,42 @@ def test_default_schedule_matches_oracle(name, cfg, over, path):
     _close(zg2, zo2, f"{name} T^2 z")
     _close(eg2, eo2, f"{name} T^2 eta")
     print(f"{name}: nodes {p.tree.num_nodes()} path {g.t_path} rel err z {rz:.1e} eta {re_:.1e}")
+
+
+def test_pooled_blocks_bitwise_equal_per_node():
+    """Shared-matrix instance (the generator's per-event A, B, Q, R, perturbation
+    off): the streaming kernel's records point every node at its class
+    representative's blocks (Engine::compute_pool).  T, L and L* are bitwise
+    those of the per-node records (SPOCK_POOL=0) and match the oracle."""
+    from paper_2505_12078_b200.solver import SpockSolver
+    p = make_config("c2p", seed=1, perturb=0.0)
+    env = {"SPOCK_T_WIDE": "1", "SPOCK_LOP_WIDE": "1"}
+    out = {}
+    for pool in ("1", "0"):
+        old = {k: os.environ.get(k) for k in list(env) + ["SPOCK_POOL"]}
+        os.environ.update(env)
+        os.environ["SPOCK_POOL"] = pool
+        try:
+            g = SpockSolver(p)
+        finally:
+            for k, v in old.items():
+                if v is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = v
+        assert g.t_path == "wide"
+        z = _rand(g.nz, 41)
+        e = _rand(g.neta, 42)
+        out[pool] = (g.apply_T(z, e), g.apply_L(z), g.apply_Lt(e), g.alpha, z, e)
+    (za, ea), la, lta, alpha, z, e = out["1"]
+    (zb, eb), lb, ltb, _, _, _ = out["0"]
+    assert np.array_equal(za, zb) and np.array_equal(ea, eb)
+    assert np.array_equal(la, lb) and np.array_equal(lta, ltb)
+    os.environ["ORACLE_SKIP_NORM"] = "1"
+    try:
+        o = OracleSolver(p, alpha=alpha)
+    finally:
+        os.environ.pop("ORACLE_SKIP_NORM", None)
+    zo, eo = o.apply_T(z, e)
+    _close(za, zo, "pooled T z")
+    _close(ea, eo, "pooled T eta")
