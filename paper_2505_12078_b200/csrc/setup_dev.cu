@@ -288,7 +288,9 @@ __global__ void k_eye(double* P, int64_t count, int n) {
 
 // a Jacobi round updates n2/2 column pairs of n2 entries (then as many rows):
 // enough threads that a round is one or two passes
-int threads_for(int n) { return n <= 32 ? 128 : (n <= 64 ? 512 : 1024); }
+// (n <= 64: the smaller CTAs keep several matrices per SM in flight, measured
+// faster on c4's 50 x 50 blocks; n > 64 holds one matrix per SM anyway)
+int threads_for(int n) { return n <= 32 ? 64 : (n <= 64 ? 128 : 1024); }
 
 }  // namespace
 
