@@ -117,3 +117,41 @@ def test_dual_cone_projection_on_device():
                 assert got[off + 2 * n] == e[off + 2 * n]
             else:
                 assert np.array_equal(got[off:off + n], e[off:off + n])
+
+
+def test_layout_flags_pack():
+    """The product's packer hands numpy stacks over as they are (row-major
+    blocks, one shared constraint block when G is a broadcast); the oracle's
+    packer keeps the reference's column-major layout."""
+    from paper_2505_12078_b200 import capi
+    from paper_2505_12078_b200.generators import make_config
+    p = make_config("c1", seed=1)
+    fast = capi.pack_problem(p)
+    slow = capi.pack_problem(p, fast=False)
+    assert fast.desc.layout == capi.SPOCK_LAYOUT_ROW_MAJOR | capi.SPOCK_LAYOUT_SHARED_G
+    assert slow.desc.layout == 0
+
+
+@pytest.mark.gpu
+def test_layout_flags_same_solver():
+    """Row-major / shared-G descriptor and the reference's column-major one give
+    bitwise the same solver (same alpha, same T)."""
+    import ctypes as C
+    from paper_2505_12078_b200 import capi
+    from paper_2505_12078_b200.generators import make_config
+    from paper_2505_12078_b200.rng import Philox
+    from paper_2505_12078_b200.solver import SpockSolver
+    p = make_config("c2", seed=2)
+    a = SpockSolver(p)
+    orig = capi.pack_problem
+    try:
+        capi.pack_problem = lambda q, fast=True: orig(q, fast=False)
+        b = SpockSolver(p)
+    finally:
+        capi.pack_problem = orig
+    assert a.alpha == b.alpha
+    z = -1.0 + 2.0 * Philox(5).uniform_array(a.nz)
+    e = -1.0 + 2.0 * Philox(6).uniform_array(a.neta)
+    za, ea = a.apply_T(z, e)
+    zb, eb = b.apply_T(z, e)
+    assert np.array_equal(za, zb) and np.array_equal(ea, eb)
