@@ -66,3 +66,24 @@ def test_grid_cap_after_solve_rejected():
     s.solve()
     with pytest.raises(ValueError):
         s.set_grid_cap(4)
+
+
+@pytest.mark.parametrize("algo", ["solve", "solve_cp"])
+def test_batch_matches_oracle(algo):
+    """Every x_init of a batch against the CPU oracle's solve from the same
+    x_init (solver.cpp:176-187): same branch string and iteration count over a
+    short run, traces and iterates to rounding."""
+    from oracle.oracle import OracleSolver
+    from paper_2505_12078_b200.solver import BatchSolver
+    p = make_tiny(ScenarioTree.from_branching([2, 2, 1]), 3, 2, 7, TinyOpts(gamma=0.5, box_halfwidth=1.0))
+    kw = dict(max_iters=25, eps_abs=1e-14, eps_rel=1e-14)
+    xs = _x_inits(p, 4, seed=13)
+    b = BatchSolver(p, streams=2, **kw)
+    got = getattr(b, algo)(xs)
+    o = OracleSolver(p, alpha=b.solvers[0].alpha, **kw)
+    for x, g in zip(xs, got):
+        r = getattr(o, algo)(x)
+        assert g.status["branches"] == r.status["branches"]
+        assert g.status["iterations"] == r.status["iterations"]
+        np.testing.assert_allclose(g.status["rnorm_history"], r.status["rnorm_history"], rtol=1e-8, atol=1e-12)
+        np.testing.assert_allclose(g.z, r.z, rtol=1e-7, atol=1e-9)

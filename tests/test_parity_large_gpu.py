@@ -75,7 +75,7 @@ def test_pooled_blocks_bitwise_equal_per_node():
     those of the per-node records (SPOCK_POOL=0) and match the oracle."""
     from paper_2505_12078_b200.solver import SpockSolver
     p = make_config("c2p", seed=1, perturb=0.0)
-    env = {"SPOCK_T_WIDE": "1", "SPOCK_LOP_WIDE": "1"}
+    env = {"SPOCK_T_UNFUSED": "1", "SPOCK_T_WIDE": "1", "SPOCK_LOP_WIDE": "1"}
     out = {}
     for pool in ("1", "0"):
         old = {k: os.environ.get(k) for k in list(env) + ["SPOCK_POOL"]}
