@@ -105,3 +105,26 @@ def test_pooled_blocks_bitwise_equal_per_node():
     zo, eo = o.apply_T(z, e)
     _close(za, zo, "pooled T z")
     _close(ea, eo, "pooled T eta")
+
+
+@pytest.mark.parametrize("method", ["solve", "solve_cp"])
+def test_nx100_solve_trace_matches_oracle(method):
+    """The c5 state size (n_x 100, n_u 50; c5p, 9 557 nodes) through a whole
+    device-resident solve against the oracle's: branch strings, iteration
+    counts and ||r||_M traces over a short run (solver.cpp:189-350, 182-187)."""
+    from paper_2505_12078_b200.solver import SpockSolver
+    p = make_config("c5p", seed=1)
+    kw = dict(max_iters=8, eps_abs=1e-14, eps_rel=1e-14)
+    g = SpockSolver(p, **kw)
+    assert g.t_path == "wide" and g.loop_path == "graph"
+    os.environ["ORACLE_SKIP_NORM"] = "1"
+    try:
+        o = OracleSolver(p, alpha=g.alpha, **kw)
+    finally:
+        os.environ.pop("ORACLE_SKIP_NORM", None)
+    a, b = getattr(g, method)(p.x_init), getattr(o, method)(p.x_init)
+    assert a.status["branches"] == b.status["branches"]
+    assert a.status["iterations"] == b.status["iterations"] == 8
+    np.testing.assert_allclose(a.status["rnorm_history"], b.status["rnorm_history"], rtol=1e-9, atol=1e-12)
+    sc = max(1.0, float(np.abs(b.z).max()))
+    assert float(np.abs(a.z - b.z).max()) <= 1e-8 * sc
