@@ -382,7 +382,13 @@ def sharded_run(args, dist, peak: float, local: int) -> dict:
     ranks; e2e through ShardedSolver.apply_T with host buffers."""
     import torch
     from paper_2505_12078_b200.shard import ShardedSolver
-    p = _problem(args.config, args.seed)
+    # the ranks share one host: generate the instance one rank at a time (the
+    # generator's temporaries are several times the problem's ~5 GB on c4)
+    p = None
+    for r in range(dist.get_world_size()):
+        if r == dist.get_rank():
+            p = _problem(args.config, args.seed)
+        dist.barrier()
     t0 = time.time()
     sh = ShardedSolver(p)
     setup_s = time.time() - t0

@@ -161,6 +161,16 @@ Engine::Engine(const spock_problem_desc* desc, const Params& prm) : prm_(prm) {
   }
   CK(cudaStreamSynchronize(st_));
   mark("power iteration");
+  // the per-node blocks now live on the device: release the host copies (GBs on
+  // wide trees; several ranks of a sharded run share one host)
+  p_.A = BigVec();
+  p_.B = BigVec();
+  p_.Q = BigVec();
+  p_.R = BigVec();
+  p_.QN = BigVec();
+  p_.Gx = BigVec();
+  p_.Gu = BigVec();
+  p_.GN = BigVec();
 }
 
 // Persistent dataflow T (fused.cu): flags, ticket, shared-memory staging size
