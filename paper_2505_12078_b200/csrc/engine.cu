@@ -2548,7 +2548,9 @@ bool Engine::cluster_plan(int m) {
         return -1;
       }
       used[c] = off + bytes;
-      pl.push_back(ClusterPlace{reinterpret_cast<const char*>(src), int64_t((bytes + 7) & ~size_t(7)), c, int(off),
+      // whole 8-byte granules inside the allocation (every dalloc allocation
+      // carries two spare elements, so the last data element is covered)
+      pl.push_back(ClusterPlace{reinterpret_cast<const char*>(src), int64_t(bytes & ~size_t(7)), c, int(off),
                                 wr ? 1 : 0, 0});
       return int(pl.size()) - 1;
     };
