@@ -266,10 +266,17 @@ void Engine::setup_fused() {
     return;
   }
   const int bytes = fused_smem_bytes(F);
-  CK(fused_configure(bytes, F.threads));
+  // register-resident GEMVs (~250 registers per thread): with the two-slot
+  // ring a CTA fills an SM's shared memory anyway; measured on c2 (m = 75):
+  // GEMV round 1.9 k -> 1.0 k cycles per tree level, T 82.5 -> 77.6 us
+  {
+    const int r = knob("SPOCK_FUSED_REG", -1);
+    F.reg_gemv = r >= 0 ? (r != 0 && F.threads == 256) : (F.threads == 256 && F.nslots == 2 && m >= 32);
+  }
+  CK(fused_configure(bytes, F.threads, F.reg_gemv));
   int occ = 0;
   F.D = D_;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fused_kernel_ptr(F.threads), F.threads, bytes));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fused_kernel_ptr(F.threads, F.reg_gemv), F.threads, bytes));
   const int occ_cap = std::max(1, knob("SPOCK_FUSED_OCC", 4));
   fused_grid_ = std::max(1, std::min(occ, occ_cap)) * sms;
   const int total = nnl + 2 * nn;

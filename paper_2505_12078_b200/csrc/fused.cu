@@ -42,13 +42,27 @@ namespace spock {
 
 namespace fused256 {
 #define FUSED_FT 256
+#define FUSED_REG 0
 #include "fused_impl.cuh"
+#undef FUSED_REG
 #undef FUSED_FT
 }  // namespace fused256
 
+// the register-resident GEMV variant (~250 registers per thread: one CTA of
+// 256 threads per SM, the two-slot configuration)
+namespace fused256r {
+#define FUSED_FT 256
+#define FUSED_REG 1
+#include "fused_impl.cuh"
+#undef FUSED_REG
+#undef FUSED_FT
+}  // namespace fused256r
+
 namespace fused128 {
 #define FUSED_FT 128
+#define FUSED_REG 0
 #include "fused_impl.cuh"
+#undef FUSED_REG
 #undef FUSED_FT
 }  // namespace fused128
 
@@ -103,19 +117,20 @@ int fused_smem_bytes(const FusedArgs& F) {
                                kScratchSlots * kSlotD + size_t(F.red_doubles)));
 }
 
-cudaError_t fused_configure(int smem_bytes, int threads) {
-  const void* f = threads == 128 ? reinterpret_cast<const void*>(&fused128::k_T_fused)
-                                 : reinterpret_cast<const void*>(&fused256::k_T_fused);
+const void* fused_kernel_ptr(int threads, int reg) {
+  if (threads == 128) return reinterpret_cast<const void*>(&fused128::k_T_fused);
+  return reg ? reinterpret_cast<const void*>(&fused256r::k_T_fused)
+             : reinterpret_cast<const void*>(&fused256::k_T_fused);
+}
+
+cudaError_t fused_configure(int smem_bytes, int threads, int reg) {
+  const void* f = fused_kernel_ptr(threads, reg);
   // every kernel of the engine prefers the maximum shared-memory carveout, so
   // consecutive launches never wait for an SM to change its L1 / smem split
   cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   return set_smem_limit(f, smem_bytes);
 }
 
-const void* fused_kernel_ptr(int threads) {
-  return threads == 128 ? reinterpret_cast<const void*>(&fused128::k_T_fused)
-                        : reinterpret_cast<const void*>(&fused256::k_T_fused);
-}
 
 void launch_build_combined(const Dev& D, double* Bm, double* Fm, double* fc, int64_t stride, cudaStream_t st) {
   if (D.nr > 0) k_build_combined<<<D.nr, 256, 0, st>>>(D, Bm, Fm, fc, stride);
@@ -124,6 +139,8 @@ void launch_build_combined(const Dev& D, double* Bm, double* Fm, double* fc, int
 void launch_T_fused(const FusedArgs& F, int grid, cudaStream_t st) {
   if (F.threads == 128)
     fused128::k_T_fused<<<grid, 128, fused_smem_bytes(F), st>>>(F);
+  else if (F.reg_gemv)
+    fused256r::k_T_fused<<<grid, 256, fused_smem_bytes(F), st>>>(F);
   else
     fused256::k_T_fused<<<grid, 256, fused_smem_bytes(F), st>>>(F);
 }

@@ -50,6 +50,7 @@ struct FusedArgs {
   int stage_all;               // 1: stage every block; 0: only the critical-path blocks
   int nslots;                  // 1 or 2 (prefetch ring depth)
   int threads;                 // 128 or 256 threads per CTA
+  int reg_gemv;                // 256 threads: register-resident critical-path GEMVs
   int red_doubles;             // shared scratch of the CTA GEMVs: (threads / 32) * max GEMV rows
   const ItemRec* items;        // [nnl + 2 nn]
   unsigned long long* trace;   // optional: 4 globaltimer stamps per item (debug/profiling)
@@ -57,9 +58,9 @@ struct FusedArgs {
 };
 
 int fused_smem_bytes(const FusedArgs& F);
-cudaError_t fused_configure(int smem_bytes, int threads);
+cudaError_t fused_configure(int smem_bytes, int threads, int reg);
 void launch_T_fused(const FusedArgs& F, int grid, cudaStream_t st);
 void launch_build_combined(const Dev& D, double* Bm, double* Fm, double* fc, int64_t stride, cudaStream_t st);
-const void* fused_kernel_ptr(int threads);
+const void* fused_kernel_ptr(int threads, int reg);
 
 }  // namespace spock

@@ -2,6 +2,7 @@
 // (FUSED_FT threads per CTA).  See fused.cu for the design notes.
 
 constexpr int kFT = FUSED_FT;  // threads per CTA
+constexpr bool kReg = FUSED_REG != 0;  // register-resident critical-path GEMVs (RegGemv)
 constexpr int kSlot = kMaxD + 8;  // doubles per scratch vector slot
 constexpr int kScratch = 6;       // scratch slots per CTA
 
@@ -165,6 +166,85 @@ __device__ void cta_gemv2(const double* A1, int m1, int n1, int lda1, const doub
       y1[t] = o;
     else
       y2[t - m1] = o;
+  }
+  __syncthreads();
+}
+
+// Register-resident GEMV pair for the critical path: the matrix entries a
+// thread needs are loaded from shared memory into registers BEFORE the
+// dependency wait, so after it only the FMAs over the (new) input vectors, one
+// partial store and the ordered partial sums remain.  Stacked rows [A1; A2]:
+// P1 threads per row of A1 and P2 per row of A2, each over a contiguous column
+// chunk of at most kRegCols; the per-row partials are summed in chunk order.
+constexpr int kRegCols = 32;
+struct RegGemv {
+  double a[kRegCols];
+  int row;   // stacked output row (-1: idle thread)
+  int c0;    // first column
+  int cnt;   // columns held
+  int slot;  // partial index: part * (m1 + m2) + row
+  int p1, p2;
+};
+// plan + load; false when a chunk would exceed kRegCols (caller keeps cta_gemv2)
+__device__ __forceinline__ bool reg_gemv_load(RegGemv& G, const double* A1, int m1, int n1, int lda1,
+                                              const double* A2, int m2, int n2, int lda2) {
+  int best = 1 << 30, p1b = 0, p2b = 0;
+  constexpr int NW = kFT / 32;  // partials fit the cta_gemv scratch: at most NW per row
+  for (int p1 = 1; p1 * m1 <= kFT && p1 <= n1 && p1 <= NW; ++p1) {
+    const int p2 = m2 > 0 ? min(min((kFT - p1 * m1) / m2, n2), NW) : 0;
+    if (m2 > 0 && p2 < 1) break;
+    const int c = max((n1 + p1 - 1) / p1, m2 > 0 ? (n2 + p2 - 1) / p2 : 0);
+    if (c < best) best = c, p1b = p1, p2b = p2;
+  }
+  if (best > kRegCols) return false;
+  G.p1 = p1b, G.p2 = p2b;
+  const int t = threadIdx.x, m = m1 + m2;
+  const double* src = nullptr;
+  int lda = 0;
+  G.row = -1, G.cnt = 0, G.c0 = 0, G.slot = 0;
+  if (t < p1b * m1) {
+    const int part = t / m1, cb = (n1 + p1b - 1) / p1b;
+    G.row = t - part * m1;
+    G.c0 = part * cb;
+    G.cnt = max(0, min(cb, n1 - G.c0));
+    G.slot = part * m + G.row;
+    src = A1 + G.row, lda = lda1;
+  } else if (t - p1b * m1 < p2b * m2) {
+    const int u = t - p1b * m1, part = u / m2, cb = (n2 + p2b - 1) / p2b;
+    const int r = u - part * m2;
+    G.row = m1 + r;
+    G.c0 = part * cb;
+    G.cnt = max(0, min(cb, n2 - G.c0));
+    G.slot = part * m + G.row;
+    src = A2 + r, lda = lda2;
+  }
+#pragma unroll
+  for (int k = 0; k < kRegCols; ++k) G.a[k] = k < G.cnt ? src[size_t(G.c0 + k) * lda] : 0.0;
+  return true;
+}
+// y1 = A1 x1, y2 = A2 x2 from the registers of reg_gemv_load (two barriers)
+__device__ __forceinline__ void reg_gemv_run(const RegGemv& G, int m1, const double* x1, double* y1, int m2,
+                                             const double* x2, double* y2, double* red) {
+  const int m = m1 + m2;
+  if (G.row >= 0) {
+    const double* x = (G.row < m1 ? x1 : x2) + G.c0;
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < kRegCols; k += 2) {
+      if (k < G.cnt) s0 = fma(G.a[k], x[k], s0);
+      if (k + 1 < G.cnt) s1 = fma(G.a[k + 1], x[k + 1], s1);
+    }
+    red[G.slot] = s0 + s1;
+  }
+  __syncthreads();
+  for (int r = threadIdx.x; r < m; r += kFT) {
+    const int np = r < m1 ? G.p1 : G.p2;
+    double o = 0.0;
+    for (int j = 0; j < np; ++j) o += red[size_t(j) * m + r];
+    if (r < m1)
+      y1[r] = o;
+    else
+      y2[r - m1] = o;
   }
   __syncthreads();
 }
@@ -460,7 +540,9 @@ __device__ void item_back(const FusedArgs& F, const ItemRec& P, const Slot& S, d
     for (int r = t; r < nx; r += kFT) q[r] = h[r] - zx[r] + al * gx[r] - tv[r];  // cst (into v_x)
     __syncthreads();
   }
-  // ---- children
+  // ---- children (the GEMV round's matrix entries into registers first)
+  RegGemv G;
+  const bool rg = kReg && !root && reg_gemv_load(G, Mb, m, m, m, Ri, nu, nu, nu);
   const int c0 = P.c0, nch = P.nch;
   wait_flags_par(F.flagB + c0, nch);
   stamp(F, item, 1);
@@ -493,8 +575,10 @@ __device__ void item_back(const FusedArgs& F, const ItemRec& P, const Slot& S, d
   }
   __syncthreads();
   stamp(F, item, 5);
-  if (!root)
-    cta_gemv2(Mb, m, m, m, q, tv, Ri, nu, nu, nu, rhs, gx, red);  // T12 ; Rt^-1 w
+  if (rg)
+    reg_gemv_run(G, m, q, tv, nu, rhs, gx, red);  // T12 ; Rt^-1 w
+  else if (!root)
+    cta_gemv2(Mb, m, m, m, q, tv, Ri, nu, nu, nu, rhs, gx, red);
   else
     cta_gemv(Ri, nu, nu, nu, rhs, gx, false, red);
   stamp(F, item, 6);
@@ -543,7 +627,11 @@ __device__ void item_fwd(const FusedArgs& F, const ItemRec& P, const Slot& S, do
     __syncthreads();
     cta_gemv(K, nu, nx, nu, xn, xn + nx, false, red);
   }
-  // ---- parent forward (root: own backward), S2 of self and parent
+  // ---- parent forward (root: own backward), S2 of self and parent; the
+  // GEMV's matrix entries into registers first
+  RegGemv G;
+  const int mr = leaf ? nx : m;
+  const bool rg = kReg && !root && reg_gemv_load(G, Mf, mr, m, mr, nullptr, 0, 0, 0);
   if (t == 0) wait_flag(root ? F.flagB : F.flagF + an);
   else if (t == 32 && !leaf) wait_flag(F.flagS2 + c);
   else if (t == 64 && !root) wait_flag(F.flagS2 + an);
@@ -568,7 +656,10 @@ __device__ void item_fwd(const FusedArgs& F, const ItemRec& P, const Slot& S, do
       }
     }
     __syncthreads();
-    cta_gemv(Mf, leaf ? nx : m, m, leaf ? nx : m, xd, xn, false, red);  // [x; u - d] = Mf xd
+    if (rg)
+      reg_gemv_run(G, mr, xd, xn, 0, nullptr, nullptr, red);  // [x; u - d] = Mf xd
+    else
+      cta_gemv(Mf, mr, m, mr, xd, xn, false, red);
     // one owner per entry: u rows get their own d in the same pass (a second
     // pass indexed by r - nx would race with this one on xn[nx..m))
     const double* fc = sp(F_FC);
