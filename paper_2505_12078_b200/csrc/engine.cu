@@ -601,7 +601,10 @@ void Engine::setup_wide(bool force) {
   A.ycap = std::min(max_ny, 64);
   A.l2_prefetch = knob("SPOCK_WIDE_L2PF", 0);  // measured slower (c3 1.80 vs 1.40 ms)
   A.vecd = int((std::max({m, max_nc, max_dense_s2_, 2 * nu + 2 + A.ycap}) + 2 + 7) & ~7);
-  wide_ctas_ = knob("SPOCK_WIDE_CTAS", 2) >= 2 ? 2 : 1;
+  // one CTA of 8 warps per SM on deep narrow trees: ~1 200 warps for ~1 000
+  // items per level, each warp's ring less contended (measured (100, 10, 3):
+  // 4.89 -> 4.67 ms per T; 6 or 7 warps per CTA, 8 slots or 2 slots lose)
+  wide_ctas_ = knob("SPOCK_WIDE_CTAS", latency_mode ? 1 : 2) >= 2 ? 2 : 1;
   wide_rows_ = wide_rows(D_, max_nc);
   // ---- per-ticket records: [backward nn-1..0][S2 0..nnl-1][forward 0..nn-1]
   std::vector<int64_t> hxo(std::max(nn - 1, 1)), huo(std::max(nn - 1, 1)), ao(std::max(nn - 1, 1));
