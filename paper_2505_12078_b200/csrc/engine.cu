@@ -2541,7 +2541,9 @@ bool Engine::cluster_plan(int m) {
   });
   if (!ok) return false;
   const char* ce = std::getenv("SPOCK_CLUSTER_CTAS");
-  int want = ce && ce[0] ? std::atoi(ce) : 4;
+  // smallest cluster tried: 8 CTAs (c1: CP 64 vs 67 us and SuperMann 199 vs
+  // 216 us per iteration at 4; 2-3 CTAs 80 us; tools/c1_cluster_ctas.py)
+  int want = ce && ce[0] ? std::atoi(ce) : 8;
   want = std::max(1, std::min(kClusterMax, want));
   for (int C = want; C <= kClusterMax; ++C) {
     std::vector<int> own(size_t(C) + 1);
