@@ -198,3 +198,31 @@ def test_small_loop_bitwise_deterministic_and_warm_start(loop):
     warm = w.solve_cp(p.x_init, warm=(cold.z_scaled, cold.eta))
     assert cold.status["reason"] == warm.status["reason"] == "converged"
     assert warm.status["iterations"] <= cold.status["iterations"] // 4  # test_solver.cpp:373-384
+
+
+@pytest.mark.parametrize("cfg", ["c2", "c2p"])
+def test_fused_register_gemv_variant(cfg):
+    """The register-resident GEMV variant of the fused T (default on c2: 256
+    threads, two slots, m >= 32) and the shared-memory GEMV variant
+    (SPOCK_FUSED_REG=0; c2p's default) both match the oracle; they differ only
+    in the GEMV's partial-sum split (rounding)."""
+    import os
+    from paper_2505_12078_b200.generators import make_config
+    from paper_2505_12078_b200.solver import SpockSolver
+    p = make_config(cfg, seed=1)
+    env = {"SPOCK_SMALL": "0", "SPOCK_CLUSTER": "0"}
+    a = _with_env({**env, "SPOCK_FUSED_REG": "1"}, lambda: SpockSolver(p))
+    b = _with_env({**env, "SPOCK_FUSED_REG": "0"}, lambda: SpockSolver(p, alpha=a.alpha))
+    assert a.t_path == b.t_path == "fused"
+    rng = np.random.default_rng(5)
+    z, e = rng.standard_normal(a.nz), rng.standard_normal(a.neta)
+    za, ea = a.apply_T(z, e)
+    zb, eb = b.apply_T(z, e)
+    os.environ["ORACLE_SKIP_NORM"] = "1"
+    try:
+        o = OracleSolver(p, alpha=a.alpha)
+    finally:
+        os.environ.pop("ORACLE_SKIP_NORM", None)
+    zo, eo = o.apply_T(z, e)
+    for x, y in ((za, zo), (ea, eo), (zb, zo), (eb, eo), (za, zb), (ea, eb)):
+        assert float(np.abs(x - y).max()) <= 1e-10 * max(1.0, float(np.abs(y).max()))
