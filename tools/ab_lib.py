@@ -27,6 +27,15 @@ def child(out):
         r = getattr(s, method)(p1.x_init)
         tim["c1_" + method + "_us_per_iter"] = round((time.perf_counter() - t) * 1e6 / r.status["iterations"], 2)
         res["c1_" + method] = r.z
+    for cfg in ("c1", "c2", "c2p"):  # default schedule (fused T on these)
+        p = make_config(cfg, seed=1)
+        g = SpockSolver(p)
+        rng = np.random.default_rng(3)
+        z, e = rng.standard_normal(g.nz), rng.standard_normal(g.neta)
+        zo, eo = g.apply_T(z, e)
+        res[cfg + "_T_" + g.t_path + "_z"], res[cfg + "_T_" + g.t_path + "_eta"] = zo, eo
+        g.bench_T(20)
+        tim[cfg + "_T_" + g.t_path + "_us"] = round(min(g.bench_T(400) for _ in range(3)) * 1e3 / 400, 2)
     for cfg in ("c1", "c2"):
         os.environ.update({"SPOCK_T_UNFUSED": "1", "SPOCK_T_WIDE": "0"})
         p = make_config(cfg, seed=1)
