@@ -290,6 +290,18 @@ void Engine::setup_fused() {
   F.flagS2 = reinterpret_cast<int*>(buf + 8);
   F.flagB = F.flagS2 + nnl;
   F.flagF = F.flagB + nn;
+  // child -> parent hand-off slots: a parent polls its children's T12 and L*
+  // terms themselves, with no release fence and no flag on that hop
+  // (bit 0: backward sweep; bit 1: forward sweep, parent -> child (x+, d, u+))
+  const int hand = nn > 1 ? knob("SPOCK_FUSED_HAND", 3) : 0;
+  if (hand & 1) {
+    F.hand = dalloc<double>(size_t(nn - 1) * 2 * m);
+    launch_hand_clear(F.hand, int64_t(nn - 1) * 2 * m, st_);
+  }
+  if (hand & 2) {
+    F.fhand = dalloc<double>(size_t(nn - 1) * (m + nu));
+    launch_hand_clear(F.fhand, int64_t(nn - 1) * (m + nu), st_);
+  }
   // offline combined blocks B = [M1' | M1'K'], F = [M1; K M1], f = [c; K c]
   const int64_t cs = pad2(int64_t(m) * m);
   double* dBm = dalloc<double>(size_t(std::max(nn - 1, 1)) * cs);

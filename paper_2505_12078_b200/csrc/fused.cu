@@ -33,6 +33,7 @@
 //   p = eta + a L(2 z+ - z).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "dev.cuh"
@@ -131,6 +132,17 @@ cudaError_t fused_configure(int smem_bytes, int threads, int reg) {
   return set_smem_limit(f, smem_bytes);
 }
 
+
+namespace {
+__global__ void k_hand_clear(double* h, int64_t n) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    h[i] = __longlong_as_double((long long)fused256::kHandEmpty);
+}
+}  // namespace
+
+void launch_hand_clear(double* hand, int64_t n, cudaStream_t st) {
+  if (n > 0) k_hand_clear<<<int(std::min<int64_t>((n + 255) / 256, 1184)), 256, 0, st>>>(hand, n);
+}
 
 void launch_build_combined(const Dev& D, double* Bm, double* Fm, double* fc, int64_t stride, cudaStream_t st) {
   if (D.nr > 0) k_build_combined<<<D.nr, 256, 0, st>>>(D, Bm, Fm, fc, stride);

@@ -53,6 +53,8 @@ struct FusedArgs {
   int reg_gemv;                // 256 threads: register-resident critical-path GEMVs
   int red_doubles;             // shared scratch of the CTA GEMVs: (threads / 32) * max GEMV rows
   const ItemRec* items;        // [nnl + 2 nn]
+  double* hand;                // optional [nn - 1] x 2m child -> parent slots (T12, adj), empty between launches
+  double* fhand;               // optional [nn - 1] x (m + nu) parent -> child slots (x+, d, u+), likewise
   unsigned long long* trace;   // optional: 4 globaltimer stamps per item (debug/profiling)
   const double* base[FB_COUNT];
 };
@@ -60,6 +62,7 @@ struct FusedArgs {
 int fused_smem_bytes(const FusedArgs& F);
 cudaError_t fused_configure(int smem_bytes, int threads, int reg);
 void launch_T_fused(const FusedArgs& F, int grid, cudaStream_t st);
+void launch_hand_clear(double* hand, int64_t n, cudaStream_t st);
 void launch_build_combined(const Dev& D, double* Bm, double* Fm, double* fc, int64_t stride, cudaStream_t st);
 const void* fused_kernel_ptr(int threads, int reg);
 

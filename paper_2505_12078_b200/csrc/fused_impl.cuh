@@ -54,6 +54,26 @@ __device__ __forceinline__ void st_release(int* p, int v) {
 }
 // loads of data produced by other CTAs in this launch: L2 only (no stale L1)
 __device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
+// child -> parent hand-off slots (FusedArgs::hand): an empty slot holds
+// kHandEmpty, a NaN payload no stored value carries (hand_canon maps every NaN
+// to the canonical one), so a parent polls its children's values themselves:
+// each 8-byte value is read whole or not yet, and nothing else the parent
+// reads comes from the child, so no fence or flag sits on this hop
+constexpr unsigned long long kHandEmpty = 0x7FF4DEAD7FF4DEADull;
+__device__ __forceinline__ double hand_canon(double v) {
+  return v != v ? __longlong_as_double(0x7FF8000000000000ll) : v;
+}
+__device__ __forceinline__ void st_relaxed(double* p, double v) {
+  asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ double ld_relaxed(const double* p) {
+  double v;
+  asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ bool hand_empty(double v) {
+  return (unsigned long long)__double_as_longlong(v) == kHandEmpty;
+}
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -512,14 +532,24 @@ __device__ void item_back(const FusedArgs& F, const ItemRec& P, const Slot& S, d
     __syncthreads();
     cta_gemv(HxT, nx, px, nx, head, tv, true, red);
     cta_gemv(HuT, nu, pu, nu, head + px, tv + nx, true, red);
-    double* adj = D.adj + size_t(i - 1) * m;
-    for (int r = t; r < m; r += kFT) adj[r] = tv[r];
+    if (F.hand) {
+      double* h = F.hand + size_t(i - 1) * 2 * m + m;
+      for (int r = t; r < m; r += kFT) st_relaxed(h + r, hand_canon(tv[r]));
+    } else {
+      double* adj = D.adj + size_t(i - 1) * m;
+      for (int r = t; r < m; r += kFT) adj[r] = tv[r];
+    }
   }
   if (leaf) {
     __syncthreads();
     cta_gemv(Mb, m, nx, m, q, tv, false, red);  // T12 = M1' q
-    double* T12 = D.T12 + size_t(i - 1) * m;
-    for (int r = t; r < m; r += kFT) T12[r] = tv[r];
+    if (F.hand) {
+      double* h = F.hand + size_t(i - 1) * 2 * m;
+      for (int r = t; r < m; r += kFT) st_relaxed(h + r, hand_canon(tv[r]));
+    } else {
+      double* T12 = D.T12 + size_t(i - 1) * m;
+      for (int r = t; r < m; r += kFT) T12[r] = tv[r];
+    }
     cta_release(F.flagB + i);
     stamp(F, item, 2);
     return;
@@ -544,7 +574,7 @@ __device__ void item_back(const FusedArgs& F, const ItemRec& P, const Slot& S, d
   RegGemv G;
   const bool rg = kReg && !root && reg_gemv_load(G, Mb, m, m, m, Ri, nu, nu, nu);
   const int c0 = P.c0, nch = P.nch;
-  wait_flags_par(F.flagB + c0, nch);
+  if (!F.hand) wait_flags_par(F.flagB + c0, nch);
   stamp(F, item, 1);
   stamp(F, item, 4);
   for (int r = t; r < m; r += kFT) {
@@ -553,11 +583,32 @@ __device__ void item_back(const FusedArgs& F, const ItemRec& P, const Slot& S, d
     double sa = 0.0, st = 0.0;
     for (int c = 0; c < nch; c += 4) {
       double va[4], vt[4];
+      if (F.hand) {  // poll the children's slots, then empty them for the next T
+        bool full;
+        do {
+          full = true;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const size_t o = size_t(c0 + c + k - 1) * m + r;
-        va[k] = c + k < nch ? ldcg(D.adj + o) : 0.0;
-        vt[k] = c + k < nch ? ldcg(D.T12 + o) : 0.0;
+          for (int k = 0; k < 4; ++k) {
+            const double* h = F.hand + size_t(c0 + c + k - 1) * 2 * m + r;
+            vt[k] = c + k < nch ? ld_relaxed(h) : 0.0;
+            va[k] = c + k < nch ? ld_relaxed(h + m) : 0.0;
+            full = full && !hand_empty(vt[k]) && !hand_empty(va[k]);
+          }
+        } while (!full);  // (a backed-off poll measured slower)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (c + k < nch) {
+            double* h = F.hand + size_t(c0 + c + k - 1) * 2 * m + r;
+            h[0] = __longlong_as_double((long long)kHandEmpty);
+            h[m] = __longlong_as_double((long long)kHandEmpty);
+          }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const size_t o = size_t(c0 + c + k - 1) * m + r;
+          va[k] = c + k < nch ? ldcg(D.adj + o) : 0.0;
+          vt[k] = c + k < nch ? ldcg(D.T12 + o) : 0.0;
+        }
       }
 #pragma unroll
       for (int k = 0; k < 4; ++k)
@@ -584,7 +635,10 @@ __device__ void item_back(const FusedArgs& F, const ItemRec& P, const Slot& S, d
   stamp(F, item, 6);
   double* dv = D.dvec + size_t(i) * nu;
   for (int r = t; r < nu; r += kFT) dv[r] = dc[r] - gx[r];
-  if (!root) {
+  if (!root && F.hand) {
+    double* h = F.hand + size_t(i - 1) * 2 * m;
+    for (int r = t; r < m; r += kFT) st_relaxed(h + r, hand_canon(tv[r]));
+  } else if (!root) {
     double* T12 = D.T12 + size_t(i - 1) * m;
     for (int r = t; r < m; r += kFT) T12[r] = tv[r];
   } else if (t == 0) {
@@ -632,9 +686,13 @@ __device__ void item_fwd(const FusedArgs& F, const ItemRec& P, const Slot& S, do
   RegGemv G;
   const int mr = leaf ? nx : m;
   const bool rg = kReg && !root && reg_gemv_load(G, Mf, mr, m, mr, nullptr, 0, 0, 0);
-  if (t == 0) wait_flag(root ? F.flagB : F.flagF + an);
+  const bool fh = F.fhand != nullptr;  // parent values by hand-off slot instead of flagF + L2
+  if (t == 0 && (root || !fh)) wait_flag(root ? F.flagB : F.flagF + an);
   else if (t == 32 && !leaf) wait_flag(F.flagS2 + c);
   else if (t == 64 && !root) wait_flag(F.flagS2 + an);
+  // own d: with hand-offs no flag chain runs from this node's backward item
+  // through the root to here, so a non-leaf acquires its own backward flag
+  else if (t == 96 && (F.hand || fh) && !leaf && !root) wait_flag(F.flagB + c);
   __syncthreads();
   stamp(F, F.D.nn + F.D.nnl + c, 1);
   if (!root) {
@@ -643,16 +701,26 @@ __device__ void item_fwd(const FusedArgs& F, const ItemRec& P, const Slot& S, do
     // hat tau_c, hat s_c (written by the parent's S2): in the same load round
     if (t == kFT - 1) early[nu] = 2.0 * ldcg(zo + D.tau_base + c - 1) - z[D.tau_base + c - 1];
     if (t == kFT - 2) early[nu + 1] = 2.0 * ldcg(zo + D.s_base + c - 1) - z[D.s_base + c - 1];
+    // the parent's slot for this node: [x_anc+ | d_anc | u_anc+], emptied after the read
+    double* hs = fh ? F.fhand + size_t(c - 1) * (m + nu) : nullptr;
+    auto take = [&](int k) {
+      double v;
+      while (hand_empty(v = ld_relaxed(hs + k))) {
+      }
+      hs[k] = __longlong_as_double((long long)kHandEmpty);
+      return v;
+    };
     for (int r = t; r < m; r += kFT) {
       if (r < nx) {
-        const double xp = ldcg(zo + 1 + size_t(an) * nx + r);
+        const double xp = fh ? take(r) : ldcg(zo + 1 + size_t(an) * nx + r);
         xd[r] = xp;
         ahat[r] = 2.0 * xp - zax[r];
       } else {
-        xd[r] = ldcg(D.dvec + size_t(an) * nu + (r - nx));
+        xd[r] = fh ? take(r) : ldcg(D.dvec + size_t(an) * nu + (r - nx));
         // own d in the same load round (final: every backward item precedes the root forward)
         if (!leaf) early[r - nx] = ldcg(D.dvec + size_t(c) * nu + (r - nx));
-        ahat[r] = 2.0 * ldcg(zo + D.u_base + size_t(an) * nu + (r - nx)) - zau[r - nx];
+        const double up = fh ? take(m + r - nx) : ldcg(zo + D.u_base + size_t(an) * nu + (r - nx));
+        ahat[r] = 2.0 * up - zau[r - nx];
       }
     }
     __syncthreads();
@@ -669,7 +737,11 @@ __device__ void item_fwd(const FusedArgs& F, const ItemRec& P, const Slot& S, do
       xn[r] = v;
     }
   } else {
-    for (int r = t; r < nu; r += kFT) xn[nx + r] += ldcg(D.dvec + r);
+    for (int r = t; r < nu; r += kFT) {
+      const double d0 = ldcg(D.dvec + r);
+      early[r] = d0;  // (own d, for the children's slots)
+      xn[nx + r] += d0;
+    }
   }
   __syncthreads();
   for (int r = t; r < (leaf ? nx : m); r += kFT) {
@@ -678,8 +750,17 @@ __device__ void item_fwd(const FusedArgs& F, const ItemRec& P, const Slot& S, do
     else
       zo[D.u_base + size_t(c) * nu + (r - nx)] = xn[r];
   }
-  // children need only (x+, u+) and d: publish before the dual work
-  cta_release(F.flagF + c);
+  if (fh) {  // children's slots [x+ | d | u+]: no fence, no flag on this hop
+    for (int k = 0; k < P.nch; ++k) {
+      double* hs = F.fhand + size_t(P.c0 + k - 1) * (m + nu);
+      for (int r = t; r < m + nu; r += kFT)
+        st_relaxed(hs + r, hand_canon(r < nx ? xn[r] : (r < m ? early[r - nx] : xn[nx + r - m])));
+    }
+    __syncthreads();  // (xn is doubled in place below)
+  } else {
+    // children need only (x+, u+) and d: publish before the dual work
+    cta_release(F.flagF + c);
+  }
   stamp(F, F.D.nn + F.D.nnl + c, 2);
   {
     const double* zx = sp(F_ZX);

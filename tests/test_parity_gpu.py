@@ -226,3 +226,50 @@ def test_fused_register_gemv_variant(cfg):
     zo, eo = o.apply_T(z, e)
     for x, y in ((za, zo), (ea, eo), (zb, zo), (eb, eo), (za, zb), (ea, eb)):
         assert float(np.abs(x - y).max()) <= 1e-10 * max(1.0, float(np.abs(y).max()))
+
+
+HAND_CASES = [
+    ("c2", None),
+    ("c2p", None),
+    ("mixed-3-1-2", lambda: make_tiny(ScenarioTree.from_branching([3, 1, 2]), 3, 2, 5, TinyOpts(gamma=0.3))),
+    ("chain-1-1-2-1", lambda: make_tiny(ScenarioTree.from_branching([1, 1, 2, 1]), 4, 2, 9, TinyOpts(gamma=0.4))),
+]
+
+
+@pytest.mark.parametrize("name,mk", HAND_CASES, ids=[c[0] for c in HAND_CASES])
+def test_fused_handoff_bitwise(name, mk):
+    """Hand-off slots of the fused T (a parent polls its children's T12 / L*
+    terms, a child its parent's (x+, d, u+), each slot emptied by its one reader
+    for the next launch; SPOCK_FUSED_HAND bits 0 / 1) change no arithmetic: T,
+    repeated T (slots reused across launches) and a graph-loop CP solve are
+    bitwise those of the flag schedule (SPOCK_FUSED_HAND=0) and of either sweep
+    alone, and T matches the oracle."""
+    import os
+    from paper_2505_12078_b200.generators import make_config
+    from paper_2505_12078_b200.solver import SpockSolver
+    p = make_config(name, seed=1) if mk is None else mk()
+    env = {"SPOCK_SMALL": "0", "SPOCK_CLUSTER": "0"}
+    a = _with_env(env, lambda: SpockSolver(p, max_iters=60))  # default: both sweeps
+    assert a.t_path == "fused"
+    rng = np.random.default_rng(11)
+    z, e = rng.standard_normal(a.nz), rng.standard_normal(a.neta)
+    za, ea = a.apply_T(z, e)
+    seq = [a.apply_T(za, ea) for _ in range(3)]
+    ra = a.solve_cp()
+    for hand in ("0", "1", "2"):
+        b = _with_env({**env, "SPOCK_FUSED_HAND": hand}, lambda: SpockSolver(p, max_iters=60, alpha=a.alpha))
+        zb, eb = b.apply_T(z, e)
+        assert np.array_equal(za, zb) and np.array_equal(ea, eb), hand
+        for zc, ec in seq:
+            zd, ed = b.apply_T(za, ea)
+            assert np.array_equal(zc, zd) and np.array_equal(ec, ed), hand
+        rb = b.solve_cp()
+        assert np.array_equal(ra.z, rb.z) and np.array_equal(ra.status["rnorm_history"], rb.status["rnorm_history"])
+    os.environ["ORACLE_SKIP_NORM"] = "1"
+    try:
+        o = OracleSolver(p, alpha=a.alpha)
+    finally:
+        os.environ.pop("ORACLE_SKIP_NORM", None)
+    zo, eo = o.apply_T(z, e)
+    for x, y in ((za, zo), (ea, eo)):
+        assert float(np.abs(x - y).max()) <= 1e-9 * max(1.0, float(np.abs(y).max()))
